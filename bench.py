@@ -1,0 +1,470 @@
+"""Benchmark: sliding-window pooling / convolution on B200 vs the roofline and
+the reference CPU path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json configs[1]): 256 signals x 262,144 samples
+N(0,1), window 16; one STEP = average pooling + max pooling of the batch
+through the drop-in API on HBM-resident inputs.  value = algorithmic bytes
+(4 * (|x| + |y|) per op) / device time, summed over ranks (weak scaling: every
+rank pools its own 256-signal batch; no collective on the data path).
+`per_config` adds every other BASELINE config (1-D conv, k sweep, 2-D 3x3 /
+5x5, NCHW, 65536^2 7x7 row bands) with GB/s, GFLOP/s, roofline fraction and
+the im2col + cuBLAS contrast on the same GPU.  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "output GB/s + GFLOP/s per kernel vs HBM/FP32 roofline, 1/2/4/8 B200, vs CPU ref"
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived FFMA peak at max clock
+B, L, K = 256, 262144, 16
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- helpers
+def roofline(alg_bytes, flops, seconds, hbm_peak):
+    """bound = max(t_hbm, t_fp32); frac vs the HBM (or FP32) peak."""
+    gbs = alg_bytes / seconds / 1e9
+    gflops = flops / seconds / 1e9
+    t_hbm = alg_bytes / (hbm_peak * 1e9)
+    t_fp = flops / (FP32_PEAK_TFLOPS * 1e12)
+    bound = "hbm" if t_hbm >= t_fp else "fp32"
+    return {"gbs": round(gbs, 1), "gflops": round(gflops, 1), "bound": bound,
+            "frac_of_bound": round(max(t_hbm, t_fp) / seconds, 4),
+            "hbm_frac": round(gbs / hbm_peak, 4)}
+
+
+def time_launches(torch, fn, reps, warmup, flush=None):
+    """Per-launch device time (CUDA events on the current stream), median."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    st = torch.cuda.current_stream()
+    for _ in range(reps):
+        if flush is not None:
+            flush()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        times.append(a.elapsed_time(b) / 1e3)
+    return statistics.median(times)
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    """`--impl reference`: the reference's algorithm (oracle port, pinned to
+    the reference's outputs) on all host cores, same workload / metric."""
+    if rank != 0:
+        return
+    from oracle import cpu_runner
+    p = {"cfg": 2, "n": L, "k": K, "ops": ("avg", "max")}
+    cores = len(cpu_runner.host_cores())
+    units = B  # the full 256-signal batch per step
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_runner.time_units("pool", p, units, cores)
+        if i >= args.warmup:
+            times.append(r["seconds"])
+    sec = statistics.median(times)
+    alg = 2 * 4 * (B * L + B * (L - K + 1))
+    val = alg / sec / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic N(0,1) signals, seeded per signal",
+            "config": {"workload": "cfg2 pool1d avg+max k=16, 256 x 262144 fp32",
+                       "signals": B, "length": L, "window": K},
+            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": cores,
+                             "kind": "port", "cpu": cpu_runner.cpu_model(),
+                             "sample": f"full batch ({B} signals) per step, numpy restatement of "
+                                       "pooling.py:28-78 (avg = sum / float32(k)), one pinned "
+                                       "process per core"},
+            "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def cpu_baseline_main():
+    from oracle import cpu_runner
+    p = {"cfg": 2, "n": L, "k": K, "ops": ("avg", "max")}
+    cores = len(cpu_runner.host_cores())
+    secs = []
+    t_end = time.time() + 10.0
+    while time.time() < t_end or len(secs) < 3:
+        secs.append(cpu_runner.time_units("pool", p, B, cores)["seconds"])
+        if len(secs) >= 20:
+            break
+    sec = statistics.median(secs)
+    alg = 2 * 4 * (B * L + B * (L - K + 1))
+    one = cpu_runner.time_one_core("pool", p, 16) * (B / 16)
+    return {"value": round(alg / sec / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+            "cpu": cpu_runner.cpu_model(),
+            "sample": f"{len(secs)} x full {B}-signal batch (avg+max, k=16) on {cores} pinned "
+                      f"processes, median; oracle = numpy restatement of pooling.py:28-78",
+            "one_core_value": round(alg / one / 1e9, 3)}
+
+
+def per_config(torch, sc, hbm_peak, args, traffic):
+    """Every other BASELINE config at full size, device-resident inputs."""
+    out = {}
+    reps, warm = max(5, min(args.steps, 20)), 3
+    dev = torch.device("cuda")
+    gen = torch.Generator(device=dev)
+    from oracle import cpu_runner
+
+    def cpu_rate(kind, p, units, unit_bytes, unit_flops):
+        r = cpu_runner.time_units(kind, p, units)
+        return {"gbs": round(unit_bytes * units / r["seconds"] / 1e9, 4),
+                "gflops": round(unit_flops * units / r["seconds"] / 1e9, 4),
+                "cores": r["cores"], "sample_units": units, "seconds": round(r["seconds"], 3)}
+
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.zero_()
+
+    # ---- cfg1: 64 x 1,048,576, k = 7 (conv2d_slide_generic with a 1x7 filter)
+    gen.manual_seed(1)
+    x = torch.rand((64, 1 << 20), generator=gen, device=dev) * 2 - 1
+    w = np.random.default_rng([0x5EED, 1, 0xFFFF]).standard_normal((1, 7), dtype=np.float32)
+    vm = sc.VectorModel(16)
+    t = time_launches(torch, lambda: sc.conv2d_slide_generic(x, w, vm), reps, warm)
+    nb = 4 * (x.numel() + 64 * ((1 << 20) - 6) + 7)
+    fl = 2 * 64 * ((1 << 20) - 6) * 7
+    fd = torch.from_numpy(w.reshape(-1)).to(dev)
+    cols = torch.empty(((1 << 20) - 6) * 7, device=dev)
+    yc = torch.empty((1 << 20) - 6, device=dev)
+    from paper_2310_05218_b200 import _lib as L_
+    lib = L_.load()
+
+    def contrast1():  # im2col + cuBLAS per signal (gemm.py:62-69 per conv1d call)
+        for r in range(64):
+            lib.sc_conv2d_im2col_f32(x[r].data_ptr(), 1, 1 << 20, fd.data_ptr(), 1, 7,
+                                     cols.data_ptr(), 1, yc.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream)
+    tc = time_launches(torch, contrast1, 3, 1)
+    out["cfg1_conv1d_k7"] = {"ms": round(t * 1e3, 4), **roofline(nb, fl, t, hbm_peak),
+                             "im2col_cublas_ms": round(tc * 1e3, 3),
+                             "cpu": cpu_rate("conv1d", {"cfg": 1, "n": 1 << 20, "k": 7}, 8,
+                                             nb / 64, fl / 64)}
+    del x, cols, yc
+
+    # ---- cfg2 window sweep k in {3, 64, 255} (16 is the headline)
+    gen.manual_seed(2)
+    xp = torch.randn((B, L), generator=gen, device=dev)
+    for k in (3, 16, 64, 255):
+        row = {}
+        for name, fn in (("avg", sc.sliding_window_mean), ("max", sc.sliding_window_max),
+                         ("sum", sc.sliding_window_sum)):
+            t = time_launches(torch, lambda: fn(xp, k), reps, warm)
+            nb = 4 * (B * L + B * (L - k + 1))
+            fl = (math.floor(math.log2(k)) + bin(k).count("1") - 1 if name != "max" else
+                  math.floor(math.log2(k)) + (1 if (k & (k - 1)) else 0)) * B * (L - k + 1)
+            row[name] = {"ms": round(t * 1e3, 4), **roofline(nb, fl, t, hbm_peak)}
+        row["cpu_sum"] = cpu_rate("pool", {"cfg": 2, "n": L, "k": k, "ops": ("sum",)}, 32,
+                                  4 * (L + L - k + 1), 0)
+        out[f"cfg2_pool_k{k}"] = row
+    del xp
+
+    # ---- cfg3: 32 x 4096^2, 3x3 and 5x5
+    gen.manual_seed(3)
+    xi = torch.rand((32, 4096, 4096), generator=gen, device=dev)
+    for k, fn in ((3, sc.conv2d_custom3), (5, sc.conv2d_custom5)):
+        f = (np.random.default_rng([0x5EED, 3, k]).standard_normal((k, k), dtype=np.float32)
+             / np.float32(k)).astype(np.float32)
+        t = time_launches(torch, lambda: fn(xi, f, vm), reps, warm)
+        o = 4096 - k + 1
+        nb = 4 * (xi.numel() + 32 * o * o + k * k)
+        fl = 2 * 32 * o * o * k * k
+        # contrast: im2col + cuBLAS on one image (column matrix o*o*k*k floats), x32
+        cols = torch.empty(o * o * k * k, device=dev)
+        yc = torch.empty((o, o), device=dev)
+        fdk = torch.from_numpy(f.reshape(-1)).to(dev)
+
+        def contrast3():
+            lib.sc_conv2d_im2col_f32(xi[0].data_ptr(), 4096, 4096, fdk.data_ptr(), k, k,
+                                     cols.data_ptr(), o, yc.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream)
+        tc = time_launches(torch, contrast3, 3, 1) * 32
+        del cols, yc
+        out[f"cfg3_conv2d_{k}x{k}"] = {"ms": round(t * 1e3, 4), **roofline(nb, fl, t, hbm_peak),
+                                       "im2col_cublas_ms": round(tc * 1e3, 3),
+                                       "cpu": cpu_rate("conv2d", {"cfg": 3, "h": 4096, "w": 4096,
+                                                                  "k": k}, 8, nb / 32, fl / 32)}
+    del xi
+
+    # ---- cfg4: NCHW 16x64x112^2, 64 out, 3x3 pad 1 (inputs < L2: flush between reps)
+    gen.manual_seed(4)
+    xn = torch.randn((16, 64, 112, 112), generator=gen, device=dev)
+    wn = torch.randn((64, 64, 3, 3), generator=gen, device=dev) / 24.0
+    t = time_launches(torch, lambda: sc.conv2d_nchw(xn, wn, 1), reps, warm, flush=flush)
+    nb = 4 * (xn.numel() * 2 + wn.numel())
+    fl = 2 * 16 * 64 * 112 * 112 * 64 * 9
+    prev = torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    import torch.nn.functional as F
+
+    def contrast4():
+        cols = F.unfold(xn, 3, padding=1)                      # im2col (N, 576, 12544)
+        return torch.matmul(wn.reshape(64, 576), cols)          # cuBLAS SGEMM
+    tc = time_launches(torch, contrast4, 5, 2, flush=flush)
+    tcd = time_launches(torch, lambda: F.conv2d(xn, wn, padding=1), 5, 2, flush=flush)
+    torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = prev
+    out["cfg4_nchw_3x3"] = {"ms": round(t * 1e3, 4), **roofline(nb, fl, t, hbm_peak),
+                            "im2col_cublas_ms": round(tc * 1e3, 3),
+                            "cudnn_fp32_ms": round(tcd * 1e3, 3),
+                            "cpu": cpu_rate("nchw", {"cfg": 4, "cin": 64, "cout": 64, "h": 112,
+                                                     "w": 112}, 2, nb / 16, fl / 16)}
+    del xn, wn
+
+    # ---- cfg5: one 65536^2 image, 7x7 (1 GPU: the whole image in one launch)
+    gen.manual_seed(5)
+    xb = torch.empty((65536, 65536), device=dev)
+    for r0 in range(0, 65536, 8192):
+        xb[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
+    f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
+          / np.float32(7)).astype(np.float32)
+    t = time_launches(torch, lambda: sc.conv2d_slide_generic(xb, f7, vm), 3, 1)
+    o = 65530
+    nb = 4 * (65536 * 65536 + o * o + 49)
+    fl = 2 * o * o * 49
+    out["cfg5_7x7_65536"] = {"ms": round(t * 1e3, 3), **roofline(nb, fl, t, hbm_peak),
+                             "cpu": cpu_rate("conv2d", {"cfg": 5, "h": 262, "w": 65536, "k": 7,
+                                                        "lo": -1.0}, 8,
+                                             4 * (262 * 65536 + 256 * 65530), 2 * 256 * 65530 * 49)}
+    del xb
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_05218_b200 as sc
+    from paper_2310_05218_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    hbm_peak, peak_src = load_peaks()
+    traffic = load_traffic()
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(0x5EED + rank)
+    x = torch.randn((B, L), generator=gen, device=dev)
+    st = torch.cuda.current_stream()
+    alg_bytes_op = 4 * (B * L + B * (L - K + 1))
+
+    def step():
+        sc.sliding_window_mean(x, K)
+        sc.sliding_window_max(x, K)
+
+    # warm-up, then ~1 s of sustained load so the clocks we sample are loaded
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.2)
+    t_sustain = time.time() + 1.0
+    while time.time() < t_sustain:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, events around each launch
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(st)
+    for i in range(args.steps):
+        ev[i][0].record(st)
+        sc.sliding_window_mean(x, K)
+        ev[i][1].record(st)
+        sc.sliding_window_max(x, K)
+        ev[i][2].record(st)
+    t_all1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    elapsed = t_all0.elapsed_time(t_all1) / 1e3
+    t_avg = statistics.mean(e[0].elapsed_time(e[1]) for e in ev) / 1e3
+    t_max = statistics.mean(e[1].elapsed_time(e[2]) for e in ev) / 1e3
+    if world > 1:
+        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    value = world * args.steps * 2 * alg_bytes_op / elapsed / 1e9
+
+    # ---- end-to-end through the public API with pinned host buffers
+    xh = sc.pinned_empty((B, L))
+    xh[...] = x.cpu().numpy()
+    sc.sliding_window_mean(xh, K)
+    sc.sliding_window_max(xh, K)
+    e2e_steps = max(3, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ya, _ = sc.sliding_window_mean(xh, K)
+        ym, _ = sc.sliding_window_max(xh, K)
+    e2e_sec = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_sec], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_sec = float(tt.item())
+    e2e_val = world * e2e_steps * 2 * alg_bytes_op / e2e_sec / 1e9
+
+    if rank != 0:
+        return
+    dom = max(t_avg, t_max)
+    dom_name = "pool_reg_kernel<AVG,T=16,k=16>" if t_avg >= t_max else "pool_reg_kernel<MAX,T=16,k=16>"
+    achieved = alg_bytes_op / dom / 1e9
+    tr = traffic.get(dom_name)
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: torch.randn N(0,1) signals on device, seed 0x5EED+rank",
+        "config": {"workload": "cfg2 pool1d avg+max k=16 (BASELINE configs[1])",
+                   "signals_per_rank": B, "length": L, "window": K,
+                   "l2": "inputs (268 MB) larger than L2 (126 MB), no flush",
+                   "parallelism": f"signals sharded, {world} rank(s), no collective"},
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     "traffic": tr, "alg_bytes_per_launch": alg_bytes_op,
+                     "peak_source": peak_src,
+                     "per_launch_us": {"avg": round(t_avg * 1e6, 2), "max": round(t_max * 1e6, 2)}},
+        "e2e": {"value": round(e2e_val, 2), "unit": "GB/s",
+                "h2d_bytes_per_step": 2 * 4 * B * L,
+                "d2h_bytes_per_step": 2 * 4 * B * (L - K + 1),
+                "path": "sliding_window_mean/max on pinned numpy input -> numpy output "
+                        "(sc_pool1d_f32_host chunked H2D/kernel/D2H pipeline)"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_main()
+    if world == 1 and not args.no_extras:
+        line["per_config"] = per_config(torch, sc, hbm_peak, args, traffic)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-extras", action="store_true", help="skip the per-config table")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,326 @@
+// 2-D single-channel valid convolution (and batched 1-D as a 1 x k filter).
+//
+// Replaces _accumulate_taps (reference.py:15-23) behind conv2d_reference,
+// conv2d_slide_generic / _compound, conv2d_custom3 / 5 and conv1d_slide
+// (kernels.py:220-275).
+//
+// conv2d_tma_kernel<KH, KW> -- the filter-size-specialised path, the GPU form
+// of the paper's custom kernels (kernels.py:185-206: each input row's slid
+// vectors are built once and reused for every output row that touches it).
+//   * A CTA owns a column strip of TW = 32*NW output columns and RC output
+//     rows.  A producer warp streams the strip's input rows (TW + KW - 1
+//     columns, RS rows per stage) into an NST-deep shared-memory ring with
+//     cp.async.bulk.tensor (TMA) and mbarrier complete_tx.
+//   * Each consumer warp owns 32 output columns (lane-striped, so every
+//     global store is one coalesced 128-byte line -- output rows are not
+//     16-byte aligned, SURVEY 7 hard part 1).  Walking input rows once, a lane
+//     reads its KW taps of the row from shared memory and folds them into KH
+//     register-resident rolling accumulators (output rows t-KH+1 .. t).
+//   * Taps live in the launch parameters (constant bank), so FFMA / FMUL read
+//     them as constant operands; KH x KW is fully unrolled.
+//   * kExact: __fmul_rn + __fadd_rn in ascending (j, i) order from 0 ->
+//     bit-identical to the reference; otherwise one FFMA per tap.
+// conv2d_generic_kernel<T> -- runtime (kh, kw), float or double (the latter
+// backs oracle_conv2d, reference.py:42-47); direct, L1-cached loads.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace sc {
+namespace {
+
+template <int KH, int KW>
+struct Taps {
+  float f[KH * KW];
+};
+
+constexpr int kConsumerWarps = 4;
+constexpr int kColsPerCta = 32 * kConsumerWarps;  // 128 output columns
+constexpr int kStages = 4;
+
+template <int KH>
+struct RowsPerStage {
+  // a multiple of KH so the rolling-accumulator phase is static per stage
+  static constexpr int value = KH == 1 ? 8 : (KH == 3 ? 12 : (KH == 5 ? 10 : 14));
+};
+
+__host__ __device__ constexpr int box_cols(int kw) { return ((kColsPerCta + kw - 1) + 3) / 4 * 4; }
+__host__ __device__ constexpr int stage_floats(int rs, int bw) { return (rs * bw + 31) / 32 * 32; }
+
+template <int KH, int KW, bool kExact>
+__global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
+    conv2d_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
+                      int64_t oh, int64_t ow, int rows_per_cta, const Taps<KH, KW> taps) {
+  constexpr int RS = RowsPerStage<KH>::value;
+  constexpr int BW = box_cols(KW);
+  constexpr int kStageFloats = stage_floats(RS, BW);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  // TMA destinations must be 128-byte aligned: align the dynamic base and
+  // round every stage up to a multiple of 32 floats
+  float* smem = reinterpret_cast<float*>(
+      smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * kColsPerCta;
+  const int r0 = blockIdx.y * rows_per_cta;
+  const int b = blockIdx.z;
+  const int rc = (int)min((int64_t)rows_per_cta, oh - r0);  // output rows here
+  const int n_in = rc + KH - 1;                              // input rows needed
+  const int n_stage = (n_in + RS - 1) / RS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer: one elected lane issues the TMA ring
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      for (int s = 0; s < n_stage; ++s) {
+        const int slot = s % kStages;
+        if (s >= kStages) mbar_wait(&empty_bar[slot], ((s / kStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full_bar[slot], RS * BW * (uint32_t)sizeof(float));
+        tma_load_3d(smem + slot * kStageFloats, &tmap, &full_bar[slot], c0, r0 + s * RS, b);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  const int col = warp * 32 + lane;  // column within the strip
+  const int64_t gcol = (int64_t)c0 + col;
+  const bool col_ok = gcol < ow;
+  float* yb = y + ((int64_t)b * oh + r0) * ow + gcol;
+
+  float acc[KH];
+#pragma unroll
+  for (int j = 0; j < KH; ++j) acc[j] = 0.0f;
+
+  for (int s = 0; s < n_stage; ++s) {
+    const int slot = s % kStages;
+    mbar_wait(&full_bar[slot], (s / kStages) & 1);
+    const float* buf = smem + slot * kStageFloats + col;
+#pragma unroll 1
+    for (int g = 0; g < RS / KH; ++g) {
+#pragma unroll
+      for (int u = 0; u < KH; ++u) {
+        const int t = s * RS + g * KH + u;  // input row relative to r0
+        const float* rowp = buf + (g * KH + u) * BW;
+        float v[KW];
+#pragma unroll
+        for (int i = 0; i < KW; ++i) v[i] = rowp[i];
+        // output row t - j lives in slot (u - j) mod KH; RS % KH == 0 keeps
+        // (t mod KH) == u, so every index below is a compile-time constant.
+#pragma unroll
+        for (int j = 0; j < KH; ++j) {
+          const int sl = ((u - j) % KH + KH) % KH;
+          float a = (j == 0) ? 0.0f : acc[sl];
+#pragma unroll
+          for (int i = 0; i < KW; ++i) a = mac<kExact>(a, taps.f[j * KW + i], v[i]);
+          acc[sl] = a;
+        }
+        // output row t - KH + 1 is complete
+        const int o = t - (KH - 1);
+        if (o >= 0 && o < rc && col_ok) yb[(int64_t)o * ow] = acc[((u + 1) % KH)];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+  }
+}
+
+// --------------------------------------------------------------- generic
+template <typename T, bool kExact>
+__global__ void conv2d_generic_kernel(const T* __restrict__ x, int64_t batch, int64_t h,
+                                      int64_t w, const T* __restrict__ f, int kh, int kw,
+                                      T* __restrict__ y, int64_t oh, int64_t ow) {
+  const int64_t total = batch * oh * ow;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % ow;
+    const int64_t rb = idx / ow;
+    const int64_t r = rb % oh;
+    const int64_t b = rb / oh;
+    const T* xp = x + (b * h + r) * w + c;
+    T acc = T(0);
+    for (int j = 0; j < kh; ++j) {
+      const T* xr = xp + (int64_t)j * w;
+      const T* fr = f + j * kw;
+      for (int i = 0; i < kw; ++i) acc = mac<kExact>(acc, __ldg(fr + i), __ldg(xr + i));
+    }
+    y[idx] = acc;
+  }
+}
+
+// ---------------------------------------------------------- tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tmap(CUtensorMap* map, const float* x, int64_t batch, int64_t h, int64_t w, int bw,
+              int rs) {
+  auto enc = get_encode();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)w * sizeof(float), (cuuint64_t)(h * w) * sizeof(float)};
+  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)rs, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return SC_OK;
+}
+
+template <int KH, int KW, bool kExact>
+int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, float* y,
+               cudaStream_t st) {
+  constexpr int RS = RowsPerStage<KH>::value;
+  constexpr int BW = box_cols(KW);
+  const int64_t oh = h - KH + 1, ow = w - KW + 1;
+  CUtensorMap map;
+  int rc = make_tmap(&map, x, batch, h, w, BW, RS);
+  if (rc) return rc;
+  Taps<KH, KW> taps;
+  for (int i = 0; i < KH * KW; ++i) taps.f[i] = f[i];
+  // rows per CTA: enough CTAs for >= ~8 waves of 148 SMs, RS-aligned
+  const int64_t strips = (ow + kColsPerCta - 1) / kColsPerCta;
+  const int64_t want_ctas = (int64_t)sm_count() * 48;
+  int64_t segs = std::max<int64_t>(1, want_ctas / std::max<int64_t>(1, strips * batch));
+  int64_t rows = (oh + segs - 1) / segs;
+  rows = std::max<int64_t>(rows, 4 * RS);
+  rows = std::min<int64_t>(rows, oh);
+  segs = (oh + rows - 1) / rows;
+  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
+    return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
+  const size_t smem = (size_t)kStages * stage_floats(RS, BW) * sizeof(float) + 128;
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(conv2d_tma_kernel<KH, KW, kExact>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
+  conv2d_tma_kernel<KH, KW, kExact><<<grid, 32 * (kConsumerWarps + 1), smem, st>>>(
+      map, y, oh, ow, (int)rows, taps);
+  SC_LAUNCH_CHECK("conv2d_tma_kernel");
+  return SC_OK;
+}
+
+template <typename T>
+int launch_generic(const T* x, int64_t batch, int64_t h, int64_t w, const T* f, int64_t kh,
+                   int64_t kw, bool exact, T* y, cudaStream_t st) {
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  T* fd = nullptr;
+  const size_t fb = (size_t)(kh * kw) * sizeof(T);
+  SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&fd), fb, st));
+  SC_CUDA(cudaMemcpyAsync(fd, f, fb, cudaMemcpyHostToDevice, st));
+  const int64_t total = batch * oh * ow;
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 32));
+  if (exact)
+    conv2d_generic_kernel<T, true><<<(unsigned)blocks, 256, 0, st>>>(x, batch, h, w, fd, (int)kh,
+                                                                      (int)kw, y, oh, ow);
+  else
+    conv2d_generic_kernel<T, false><<<(unsigned)blocks, 256, 0, st>>>(x, batch, h, w, fd,
+                                                                       (int)kh, (int)kw, y, oh, ow);
+  SC_LAUNCH_CHECK("conv2d_generic_kernel");
+  SC_CUDA(cudaFreeAsync(fd, st));
+  return SC_OK;
+}
+
+template <int KH, int KW>
+bool tma_ok(const float* x, int64_t h, int64_t w) {
+  return (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (w % 4 == 0) && w >= box_cols(KW) &&
+         h >= RowsPerStage<KH>::value && h * w < (int64_t)1 << 40;
+}
+
+template <int KH, int KW>
+int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, bool exact,
+            float* y, cudaStream_t st, bool* done) {
+  *done = false;
+  if (!tma_ok<KH, KW>(x, h, w)) return SC_OK;
+  *done = true;
+  return exact ? launch_tma<KH, KW, true>(x, batch, h, w, f, y, st)
+               : launch_tma<KH, KW, false>(x, batch, h, w, f, y, st);
+}
+
+}  // namespace
+
+int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
+                        int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st) {
+  bool done = false;
+  int rc = SC_OK;
+  if (kh == 3 && kw == 3) rc = try_tma<3, 3>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 5 && kw == 5) rc = try_tma<5, 5>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 7 && kw == 7) rc = try_tma<7, 7>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 1 && kw == 7) rc = try_tma<1, 7>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 1 && kw == 3) rc = try_tma<1, 3>(x, batch, h, w, f, exact, y, st, &done);
+  if (rc || done) return rc;
+  return launch_generic<float>(x, batch, h, w, f, kh, kw, exact, y, st);
+}
+
+}  // namespace sc
+
+static int check_conv_args(int64_t batch, int64_t h, int64_t w, int64_t kh, int64_t kw,
+                           const void* x, const void* f, const void* y) {
+  using namespace sc;
+  if (batch < 0 || h < 1 || w < 1 || kh < 1 || kw < 1)
+    return fail(SC_ERR_SHAPE, "dims must be positive");
+  if (kh > h || kw > w)
+    return fail(SC_ERR_SHAPE, "filter " + std::to_string(kh) + "x" + std::to_string(kw) +
+                                  " exceeds input " + std::to_string(h) + "x" + std::to_string(w));
+  if (batch > 0 && (!x || !f || !y)) return fail(SC_ERR_ARG, "conv2d: null pointer");
+  return SC_OK;
+}
+
+extern "C" int sc_conv2d_f32(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
+                             int64_t kh, int64_t kw, int mode, float* y, void* stream) {
+  if (mode != SC_MODE_FAST && mode != SC_MODE_EXACT) return sc::fail(SC_ERR_ARG, "bad mode");
+  int rc = check_conv_args(batch, h, w, kh, kw, x, f, y);
+  if (rc || batch == 0) return rc;
+  return sc::conv2d_f32_dispatch(x, batch, h, w, f, kh, kw, mode == SC_MODE_EXACT, y,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sc_conv1d_f32(const float* x, int64_t batch, int64_t length, const float* wt,
+                             int64_t k, int mode, float* y, void* stream) {
+  // batch signals of `length` samples == a (batch, length) image with a 1 x k
+  // filter (bit-identical).
+  if (mode != SC_MODE_FAST && mode != SC_MODE_EXACT) return sc::fail(SC_ERR_ARG, "bad mode");
+  int rc = check_conv_args(1, batch > 0 ? batch : 1, length, 1, k, x, wt, y);
+  if (rc || batch == 0) return rc;
+  return sc::conv2d_f32_dispatch(x, 1, batch, length, wt, 1, k, mode == SC_MODE_EXACT, y,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sc_conv2d_f64(const double* x, int64_t batch, int64_t h, int64_t w,
+                             const double* f, int64_t kh, int64_t kw, double* y, void* stream) {
+  int rc = check_conv_args(batch, h, w, kh, kw, x, f, y);
+  if (rc || batch == 0) return rc;
+  return sc::launch_generic<double>(x, batch, h, w, f, kh, kw, true, y,
+                                    static_cast<cudaStream_t>(stream));
+}

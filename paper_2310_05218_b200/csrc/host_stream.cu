@@ -1,0 +1,279 @@
+// Host-buffer entry points: a chunked H2D -> kernel -> D2H pipeline.
+//
+// The reference's callers pass host (numpy) arrays and get host arrays back
+// (SURVEY 8(b)).  Here x is split into chunks (rows of signals, or row bands
+// of images with a kh-1 row halo -- banded evaluation is bit-identical to
+// whole-image evaluation); chunk c runs on slot c % 3, each
+// slot owning a CUDA stream and device buffers, so the H2D copy of chunk c+1,
+// the kernel of chunk c and the D2H copy of chunk c-1 overlap on the two copy
+// engines and the SMs.  Pinned host buffers are copied directly; pageable
+// ones go through a pinned staging ring filled by parallel host memcpy.
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sc {
+int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
+                        int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st);
+}
+
+extern "C" int sc_pool1d_f32(int op, const float* x, int64_t batch, int64_t length, int64_t k,
+                             int mode, float* y, void* stream);
+
+namespace sc {
+namespace {
+
+constexpr int kSlots = 3;
+constexpr size_t kChunkBytes = size_t(64) << 20;
+
+struct Slot {
+  cudaStream_t stream = nullptr;
+  float* d_in = nullptr;
+  float* d_out = nullptr;
+  size_t in_cap = 0, out_cap = 0;
+  float* h_in = nullptr;   // pinned staging
+  float* h_out = nullptr;
+  size_t h_in_cap = 0, h_out_cap = 0;
+  // pending pageable write-back of the chunk last issued on this slot
+  float* wb_dst = nullptr;
+  size_t wb_bytes = 0;
+};
+
+struct DeviceCtx {
+  std::mutex mu;
+  bool init = false;
+  Slot slot[kSlots];
+};
+
+DeviceCtx& ctx_for(int dev) {
+  static DeviceCtx ctx[64];
+  return ctx[dev & 63];
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = size_t(4) << 20;
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  size_t parts = std::min<size_t>(std::min<size_t>(hw, 8), std::max<size_t>(1, bytes / kMin));
+  if (parts <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t step = (bytes + parts - 1) / parts;
+  for (size_t p = 0; p < parts; ++p) {
+    const size_t off = p * step;
+    if (off >= bytes) break;
+    const size_t n = std::min(step, bytes - off);
+    th.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off, n);
+    });
+  }
+  for (auto& t : th) t.join();
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+int grow_dev(float** p, size_t* cap, size_t need) {
+  if (*cap >= need) return SC_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  SC_CUDA(cudaMalloc(reinterpret_cast<void**>(p), need));
+  *cap = need;
+  return SC_OK;
+}
+
+int grow_host(float** p, size_t* cap, size_t need) {
+  if (*cap >= need) return SC_OK;
+  if (*p) cudaFreeHost(*p);
+  *p = nullptr;
+  *cap = 0;
+  SC_CUDA(cudaHostAlloc(reinterpret_cast<void**>(p), need, cudaHostAllocDefault));
+  *cap = need;
+  return SC_OK;
+}
+
+struct Chunk {
+  const float* in;
+  size_t in_bytes;
+  float* out;
+  size_t out_bytes;
+  std::function<int(const float*, float*, cudaStream_t)> run;
+};
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev_);
+    ok_ = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() { cudaSetDevice(prev_); }
+  bool ok() const { return ok_; }
+
+ private:
+  int prev_ = 0;
+  bool ok_ = false;
+};
+
+int finish_slot(Slot& s) {
+  SC_CUDA(cudaStreamSynchronize(s.stream));
+  if (s.wb_dst) {
+    parallel_memcpy(s.wb_dst, s.h_out, s.wb_bytes);
+    s.wb_dst = nullptr;
+  }
+  return SC_OK;
+}
+
+int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_pinned) {
+  DeviceGuard guard(dev);
+  if (!guard.ok()) return fail(SC_ERR_CUDA, "cudaSetDevice failed");
+  DeviceCtx& ctx = ctx_for(dev);
+  std::lock_guard<std::mutex> lock(ctx.mu);
+  if (!ctx.init) {
+    for (auto& s : ctx.slot) SC_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    ctx.init = true;
+  }
+  size_t max_in = 0, max_out = 0;
+  for (auto& c : chunks) {
+    max_in = std::max(max_in, c.in_bytes);
+    max_out = std::max(max_out, c.out_bytes);
+  }
+  for (auto& s : ctx.slot) {
+    int rc;
+    if ((rc = grow_dev(&s.d_in, &s.in_cap, max_in))) return rc;
+    if ((rc = grow_dev(&s.d_out, &s.out_cap, max_out))) return rc;
+    if (!in_pinned && (rc = grow_host(&s.h_in, &s.h_in_cap, max_in))) return rc;
+    if (!out_pinned && (rc = grow_host(&s.h_out, &s.h_out_cap, max_out))) return rc;
+  }
+  int status = SC_OK;
+  for (size_t i = 0; i < chunks.size() && status == SC_OK; ++i) {
+    Slot& s = ctx.slot[i % kSlots];
+    Chunk& c = chunks[i];
+    if ((status = finish_slot(s))) break;
+    const float* src = c.in;
+    if (!in_pinned) {
+      parallel_memcpy(s.h_in, c.in, c.in_bytes);
+      src = s.h_in;
+    }
+    if (cudaMemcpyAsync(s.d_in, src, c.in_bytes, cudaMemcpyHostToDevice, s.stream) != cudaSuccess) {
+      status = cuda_fail(cudaGetLastError(), "H2D copy");
+      break;
+    }
+    if ((status = c.run(s.d_in, s.d_out, s.stream))) break;
+    float* dst = out_pinned ? c.out : s.h_out;
+    if (cudaMemcpyAsync(dst, s.d_out, c.out_bytes, cudaMemcpyDeviceToHost, s.stream) !=
+        cudaSuccess) {
+      status = cuda_fail(cudaGetLastError(), "D2H copy");
+      break;
+    }
+    if (!out_pinned) {
+      s.wb_dst = c.out;
+      s.wb_bytes = c.out_bytes;
+    }
+  }
+  for (auto& s : ctx.slot) {
+    int rc = finish_slot(s);
+    if (status == SC_OK) status = rc;
+  }
+  return status;
+}
+
+}  // namespace
+}  // namespace sc
+
+extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t length, int64_t k,
+                                  int mode, float* y, int device) {
+  using namespace sc;
+  if (op < SC_POOL_SUM || op > SC_POOL_MAX) return fail(SC_ERR_ARG, "pool1d: bad op");
+  if (batch < 0 || length < 1) return fail(SC_ERR_SHAPE, "pool1d: signal length must be >= 1");
+  if (k < 1 || k > length)
+    return fail(SC_ERR_SHAPE, "window " + std::to_string(k) + " out of range for length " +
+                                  std::to_string(length));
+  if (batch == 0) return SC_OK;
+  if (!x || !y) return fail(SC_ERR_ARG, "pool1d: null pointer");
+  const int64_t out_len = length - k + 1;
+  std::vector<Chunk> chunks;
+  const int64_t row_bytes = length * (int64_t)sizeof(float);
+  if (row_bytes <= (int64_t)kChunkBytes) {
+    const int64_t rows = std::max<int64_t>(1, (int64_t)kChunkBytes / row_bytes);
+    for (int64_t r = 0; r < batch; r += rows) {
+      const int64_t nr = std::min(rows, batch - r);
+      chunks.push_back({x + r * length, (size_t)(nr * length) * sizeof(float), y + r * out_len,
+                        (size_t)(nr * out_len) * sizeof(float),
+                        [=](const float* din, float* dout, cudaStream_t st) {
+                          return sc_pool1d_f32(op, din, nr, length, k, mode, dout, st);
+                        }});
+    }
+  } else {
+    // one signal is larger than a chunk: segments with a k-1 sample overlap
+    const int64_t seg = std::max<int64_t>(1, (int64_t)(kChunkBytes / sizeof(float)) - (k - 1));
+    for (int64_t r = 0; r < batch; ++r)
+      for (int64_t o = 0; o < out_len; o += seg) {
+        const int64_t no = std::min(seg, out_len - o);
+        const int64_t ni = no + k - 1;
+        chunks.push_back({x + r * length + o, (size_t)ni * sizeof(float), y + r * out_len + o,
+                          (size_t)no * sizeof(float),
+                          [=](const float* din, float* dout, cudaStream_t st) {
+                            return sc_pool1d_f32(op, din, 1, ni, k, mode, dout, st);
+                          }});
+      }
+  }
+  return run_pipeline(device, chunks, is_pinned(x), is_pinned(y));
+}
+
+extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int64_t w,
+                                  const float* f, int64_t kh, int64_t kw, int mode, float* y,
+                                  int device) {
+  using namespace sc;
+  if (mode != SC_MODE_FAST && mode != SC_MODE_EXACT) return fail(SC_ERR_ARG, "bad mode");
+  if (batch < 0 || h < 1 || w < 1 || kh < 1 || kw < 1)
+    return fail(SC_ERR_SHAPE, "dims must be positive");
+  if (kh > h || kw > w) return fail(SC_ERR_SHAPE, "filter exceeds input");
+  if (batch == 0) return SC_OK;
+  if (!x || !f || !y) return fail(SC_ERR_ARG, "conv2d: null pointer");
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  const bool exact = mode == SC_MODE_EXACT;
+  std::vector<float> taps(f, f + kh * kw);  // outlives the lambdas below
+  std::vector<Chunk> chunks;
+  const int64_t img_bytes = h * w * (int64_t)sizeof(float);
+  if (img_bytes <= (int64_t)kChunkBytes) {
+    const int64_t imgs = std::max<int64_t>(1, (int64_t)kChunkBytes / img_bytes);
+    for (int64_t b = 0; b < batch; b += imgs) {
+      const int64_t nb = std::min(imgs, batch - b);
+      chunks.push_back({x + b * h * w, (size_t)(nb * h * w) * sizeof(float), y + b * oh * ow,
+                        (size_t)(nb * oh * ow) * sizeof(float),
+                        [=, &taps](const float* din, float* dout, cudaStream_t st) {
+                          return conv2d_f32_dispatch(din, nb, h, w, taps.data(), kh, kw, exact,
+                                                     dout, st);
+                        }});
+    }
+  } else {
+    // row bands with a kh-1 row halo (bit-identical to the whole image)
+    const int64_t band = std::max<int64_t>(1, (int64_t)kChunkBytes / (w * (int64_t)sizeof(float)) -
+                                                  (kh - 1));
+    for (int64_t b = 0; b < batch; ++b)
+      for (int64_t o = 0; o < oh; o += band) {
+        const int64_t no = std::min(band, oh - o);
+        const int64_t ni = no + kh - 1;
+        chunks.push_back({x + (b * h + o) * w, (size_t)(ni * w) * sizeof(float),
+                          y + (b * oh + o) * ow, (size_t)(no * ow) * sizeof(float),
+                          [=, &taps](const float* din, float* dout, cudaStream_t st) {
+                            return conv2d_f32_dispatch(din, 1, ni, w, taps.data(), kh, kw, exact,
+                                                       dout, st);
+                          }});
+      }
+  }
+  return run_pipeline(device, chunks, is_pinned(x), is_pinned(y));
+}

@@ -1,0 +1,222 @@
+// Multi-channel NCHW convolution with zero padding (absent in the reference;
+// SURVEY 8(a) a12, BASELINE config 4: N16 Cin64 Cout64 112x112, 3x3, pad 1).
+//
+// The contraction is Cin*9 = 576 deep per output, AI ~144 flop/B: FP32-pipe
+// bound, not HBM bound.  nchw3x3_kernel is a direct (implicit-GEMM shaped)
+// FFMA kernel:
+//   * CTA tile = 64 output channels x 16x16 output pixels of one image;
+//     256 threads, thread tile = 8 channels x 8 consecutive pixels of a row
+//     (64 accumulators), so each shared-memory input row segment (10 floats)
+//     is reused across the 3 horizontal taps and 8 channels, and each weight
+//     (a warp-uniform broadcast LDS.128) across 8 pixels.
+//   * Cin is streamed in chunks of 4 channels: input tile (4 x 18 x 18, zero
+//     filled outside the image = the padding) and weights (4*9 x 64) staged
+//     in shared memory, double-buffered with cp.async so the next chunk's
+//     loads overlap this chunk's FFMAs.
+// nchw_generic_kernel covers every other shape and the EXACT mode, which
+// reproduces the composed oracle (per (n, co): sum over ci ascending of the
+// reference's single-channel conv of the padded plane, reference.py:15-23).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sc {
+namespace {
+
+constexpr int kCoT = 64;       // output channels per CTA
+constexpr int kTH = 16;        // output rows per CTA
+constexpr int kTW = 16;        // output cols per CTA
+constexpr int kCiT = 4;        // input channels per smem chunk
+constexpr int kXR = kTH + 2;   // staged input rows
+constexpr int kXC = kTW + 2;   // staged input cols
+constexpr int kXS = 20;        // padded row stride of the staged input
+constexpr int kXChunk = kCiT * kXR * kXS;
+constexpr int kWChunk = kCiT * 9 * kCoT;
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool pred) {
+  const int n = pred ? 4 : 0;  // zero-fill when predicated off
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(256, 2)
+    nchw3x3_kernel(const float* __restrict__ x, int cin, int h, int w,
+                   const float* __restrict__ wt, int cout, float* __restrict__ y, int tiles_w) {
+  __shared__ __align__(16) float xs[2][kXChunk];
+  __shared__ __align__(16) float ws[2][kWChunk];
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int tr = blockIdx.x / tiles_w, tc = blockIdx.x - tr * tiles_w;
+  const int r0 = tr * kTH, c0 = tc * kTW;
+  const int co0 = blockIdx.y * kCoT;
+  const int n = blockIdx.z;
+  const float* xn = x + (int64_t)n * cin * h * w;
+
+  auto stage = [&](int buf, int ci0) {
+    // input: kCiT x kXR x kXC, rows/cols offset by the padding of 1
+    for (int idx = tid; idx < kCiT * kXR * kXC; idx += 256) {
+      const int ci = idx / (kXR * kXC);
+      const int rem = idx - ci * (kXR * kXC);
+      const int rr = rem / kXC, cc = rem - rr * kXC;
+      const int gr = r0 - 1 + rr, gc = c0 - 1 + cc;
+      const bool ok = (ci0 + ci < cin) && gr >= 0 && gr < h && gc >= 0 && gc < w;
+      const float* src = ok ? xn + ((int64_t)(ci0 + ci) * h + gr) * w + gc : xn;
+      cp_async4(&xs[buf][(ci * kXR + rr) * kXS + cc], src, ok);
+    }
+    // weights: [ci*9 + tap][co]
+    for (int idx = tid; idx < kWChunk; idx += 256) {
+      const int co = idx % kCoT;
+      const int ct = idx / kCoT;  // ci*9 + tap
+      const int ci = ct / 9, tap = ct - ci * 9;
+      const bool ok = (ci0 + ci < cin) && (co0 + co < cout);
+      const float* src = ok ? wt + ((int64_t)(co0 + co) * cin + ci0 + ci) * 9 + tap : wt;
+      cp_async4(&ws[buf][idx], src, ok);
+    }
+    cp_async_commit();
+  };
+
+  float acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) acc[a][p] = 0.0f;
+
+  const int pr = lane >> 1;        // pixel row within the tile
+  const int pc = (lane & 1) * 8;   // first pixel col within the tile
+  const int cw = warp * 8;         // first channel of this warp
+
+  const int n_chunks = (cin + kCiT - 1) / kCiT;
+  stage(0, 0);
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < n_chunks) {
+      stage(buf ^ 1, (ch + 1) * kCiT);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int ci = 0; ci < kCiT; ++ci) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float* xr = &xs[buf][(ci * kXR + pr + j) * kXS + pc];
+        float xv[10];
+#pragma unroll
+        for (int e = 0; e < 10; ++e) xv[e] = xr[e];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const float4* wp =
+              reinterpret_cast<const float4*>(&ws[buf][(ci * 9 + j * 3 + i) * kCoT + cw]);
+          const float4 wa = wp[0], wb = wp[1];
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int p = 0; p < 8; ++p) acc[a][p] = fmaf(wv[a], xv[p + i], acc[a][p]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  const int orow = r0 + pr;
+  if (orow >= h) return;
+  const bool vec = ((w & 3) == 0) && (c0 + pc + 8 <= w);
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int co = co0 + cw + a;
+    if (co >= cout) break;
+    float* yr = y + (((int64_t)n * cout + co) * h + orow) * w + c0 + pc;
+    if (vec) {
+      reinterpret_cast<float4*>(yr)[0] = make_float4(acc[a][0], acc[a][1], acc[a][2], acc[a][3]);
+      reinterpret_cast<float4*>(yr)[1] = make_float4(acc[a][4], acc[a][5], acc[a][6], acc[a][7]);
+    } else {
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (c0 + pc + p < w) yr[p] = acc[a][p];
+    }
+  }
+}
+
+template <bool kExact>
+__global__ void nchw_generic_kernel(const float* __restrict__ x, int64_t nb, int cin, int h,
+                                    int w, const float* __restrict__ wt, int cout, int kh, int kw,
+                                    int pad, float* __restrict__ y, int oh, int ow) {
+  const int64_t total = nb * cout * (int64_t)oh * ow;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(idx % ow);
+    int64_t t = idx / ow;
+    const int r = (int)(t % oh);
+    t /= oh;
+    const int co = (int)(t % cout);
+    const int64_t n = t / cout;
+    float total_acc = 0.0f;
+    for (int ci = 0; ci < cin; ++ci) {
+      const float* xp = x + ((n * cin + ci) * h) * (int64_t)w;
+      const float* fp = wt + ((int64_t)co * cin + ci) * kh * kw;
+      float p = 0.0f;
+      for (int j = 0; j < kh; ++j) {
+        const int gr = r + j - pad;
+        for (int i = 0; i < kw; ++i) {
+          const int gc = c + i - pad;
+          const float xv =
+              (gr >= 0 && gr < h && gc >= 0 && gc < w) ? __ldg(xp + (int64_t)gr * w + gc) : 0.0f;
+          if constexpr (kExact) {
+            p = mac<true>(p, __ldg(fp + j * kw + i), xv);
+          } else {
+            total_acc = fmaf(__ldg(fp + j * kw + i), xv, total_acc);
+          }
+        }
+      }
+      if constexpr (kExact) total_acc = __fadd_rn(total_acc, p);
+    }
+    y[idx] = total_acc;
+  }
+}
+
+}  // namespace
+}  // namespace sc
+
+extern "C" int sc_conv2d_nchw_f32(const float* x, int64_t n, int64_t cin, int64_t h, int64_t w,
+                                  const float* wt, int64_t cout, int64_t kh, int64_t kw,
+                                  int64_t pad, int mode, float* y, void* stream) {
+  using namespace sc;
+  if (mode != SC_MODE_FAST && mode != SC_MODE_EXACT) return fail(SC_ERR_ARG, "nchw: bad mode");
+  if (n < 0 || cin < 1 || cout < 1 || h < 1 || w < 1 || kh < 1 || kw < 1 || pad < 0)
+    return fail(SC_ERR_SHAPE, "nchw: dims must be positive");
+  const int64_t oh = h + 2 * pad - kh + 1, ow = w + 2 * pad - kw + 1;
+  if (oh < 1 || ow < 1) return fail(SC_ERR_SHAPE, "nchw: filter exceeds padded input");
+  if (h > 0x7fffffff || w > 0x7fffffff || cin > 0x7fffffff || cout > 0x7fffffff)
+    return fail(SC_ERR_UNSUPPORTED, "nchw: dims too large");
+  if (n == 0) return SC_OK;
+  if (!x || !wt || !y) return fail(SC_ERR_ARG, "nchw: null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (mode == SC_MODE_FAST && kh == 3 && kw == 3 && pad == 1) {
+    const int tiles_w = (int)((w + kTW - 1) / kTW);
+    const int tiles_h = (int)((h + kTH - 1) / kTH);
+    dim3 grid((unsigned)(tiles_w * tiles_h), (unsigned)((cout + kCoT - 1) / kCoT), (unsigned)n);
+    if (n > 65535) return fail(SC_ERR_UNSUPPORTED, "nchw: batch too large");
+    nchw3x3_kernel<<<grid, 256, 0, st>>>(x, (int)cin, (int)h, (int)w, wt, (int)cout, y, tiles_w);
+    SC_LAUNCH_CHECK("nchw3x3_kernel");
+    return SC_OK;
+  }
+  const int64_t total = n * cout * oh * ow;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, sm_count() * 32LL));
+  if (mode == SC_MODE_EXACT)
+    nchw_generic_kernel<true><<<(unsigned)blocks, 256, 0, st>>>(
+        x, n, (int)cin, (int)h, (int)w, wt, (int)cout, (int)kh, (int)kw, (int)pad, y, (int)oh, (int)ow);
+  else
+    nchw_generic_kernel<false><<<(unsigned)blocks, 256, 0, st>>>(
+        x, n, (int)cin, (int)h, (int)w, wt, (int)cout, (int)kh, (int)kw, (int)pad, y, (int)oh, (int)ow);
+  SC_LAUNCH_CHECK("nchw_generic_kernel");
+  return SC_OK;
+}

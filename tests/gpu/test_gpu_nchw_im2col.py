@@ -1,0 +1,66 @@
+"""Multi-channel NCHW (config 4) and the im2col + cuBLAS contrast."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2310_05218_b200 as sc
+from oracle import slideconv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config4_full_size_within_tolerance():
+    rng = np.random.default_rng([0x5EED, 4])
+    x = rng.standard_normal((16, 64, 112, 112), dtype=np.float32)
+    w = (rng.standard_normal((64, 64, 3, 3), dtype=np.float32) / np.float32(24.0)).astype(np.float32)
+    got = sc.conv2d_nchw(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), 1).cpu().numpy()
+    want = O.conv2d_nchw_f64(x, w, 1)
+    assert O.normwise_error(got, want) <= O.north_star_tol(3, 64)
+
+
+def test_config4_exact_matches_composed_oracle():
+    rng = np.random.default_rng(41)
+    x = rng.standard_normal((2, 64, 112, 112), dtype=np.float32)
+    w = (rng.standard_normal((8, 64, 3, 3), dtype=np.float32) / np.float32(24.0)).astype(np.float32)
+    got = sc.conv2d_nchw(x, w, 1, exact=True)
+    assert np.array_equal(got, O.conv2d_nchw(x, w, 1))
+
+
+@pytest.mark.parametrize("n,cin,cout,h,w,k,p", [(1, 3, 5, 17, 23, 3, 1), (2, 7, 70, 33, 9, 3, 1),
+                                                 (1, 4, 4, 10, 10, 5, 2), (1, 2, 3, 8, 8, 3, 0)])
+def test_nchw_shapes(n, cin, cout, h, w, k, p):
+    rng = np.random.default_rng(n + cin + cout + h + w)
+    x = rng.standard_normal((n, cin, h, w), dtype=np.float32)
+    wt = rng.standard_normal((cout, cin, k, k), dtype=np.float32)
+    fast = sc.conv2d_nchw(x, wt, p)
+    assert O.normwise_error(fast, O.conv2d_nchw_f64(x, wt, p)) <= O.north_star_tol(k, cin)
+    exact = sc.conv2d_nchw(x, wt, p, exact=True)
+    assert np.array_equal(exact, O.conv2d_nchw(x, wt, p))
+
+
+def test_im2col_exact_and_gemm():
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1, 1, (33, 47)).astype(np.float32)
+    c = sc.CostCounters()
+    cols = sc.im2col_2d(x, 5, 4, c)
+    assert np.array_equal(cols, O.im2col_2d(x, 5, 4))
+    assert c.im2col_elems == cols.size
+    a = rng.uniform(-1, 1, (70, 30)).astype(np.float32)
+    b = rng.uniform(-1, 1, (30, 9)).astype(np.float32)
+    got = sc.gemm(a, b)
+    assert np.allclose(got, a.astype(np.float64) @ b, rtol=0, atol=1e-5)
+    kat = sc.im2col_2d(np.arange(1, 10, dtype=np.float32).reshape(3, 3), 2, 2)
+    assert kat[0].tolist() == [1, 2, 4, 5]
+
+
+def test_conv2d_im2col_matches_direct():
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, (300, 700)).astype(np.float32)
+    f = rng.uniform(-1, 1, (5, 5)).astype(np.float32)
+    c = sc.CostCounters()
+    y = sc.conv2d_im2col(x, f, c)
+    assert sc.relative_error(y, O.oracle_conv2d(x, f)) < 1e-5
+    assert c.im2col_elems == 296 * 696 * 25
+    y2, c2 = sc.run_variant(sc.KernelVariant.IM2COL_GEMM, x, f, sc.VectorModel(16))
+    assert c2.im2col_elems == c.im2col_elems

@@ -1,0 +1,121 @@
+"""Pooling kernels vs the oracle: BASELINE config 2 at full size, every
+dispatch branch (register doubling static/runtime k, float64 tile prefix,
+global passes), ragged shapes, NaN / signed-zero semantics, host pipeline."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2310_05218_b200 as sc
+from oracle import slideconv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FNS = {"sum": sc.sliding_window_sum, "max": sc.sliding_window_max, "avg": sc.sliding_window_mean}
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    rng = np.random.default_rng([0x5EED, 2])
+    x = rng.standard_normal((256, 262144), dtype=np.float32)
+    return x, torch.from_numpy(x).cuda()
+
+
+@pytest.mark.parametrize("k", [16, 3, 64, 255])
+@pytest.mark.parametrize("op", ["max", "sum", "avg"])
+def test_config2_full_size(cfg2, op, k):
+    x, xd = cfg2
+    want = O.pool_batched(x, k, op)
+    fast, st = FNS[op](xd, k)
+    fast = fast.cpu().numpy()
+    assert st == (O.pool_max_stages(k) if op == "max" else O.pool_sum_stages(k))
+    if op == "max":
+        assert np.array_equal(fast, want)
+    else:
+        assert O.normwise_error(fast, want) <= O.north_star_tol(k)
+        if k in (16, 3):                    # register doubling: bit-exact even in fast mode
+            assert np.array_equal(fast, want)
+    exact, _ = FNS[op](xd, k, exact=True)
+    assert np.array_equal(exact.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("k", list(range(1, 40)) + [47, 63, 64, 65, 100, 127, 128, 129, 200, 255,
+                                                     256, 257, 300, 511, 1000, 4097, 9000])
+def test_every_window_branch(k):
+    rng = np.random.default_rng(k)
+    n = 12_345 + k
+    x = rng.standard_normal((3, n), dtype=np.float32)
+    xd = torch.from_numpy(x).cuda()
+    for op in ("sum", "max", "avg"):
+        want = O.pool_batched(x, k, op)
+        got = FNS[op](xd, k)[0].cpu().numpy()
+        got_exact = FNS[op](xd, k, exact=True)[0].cpu().numpy()
+        assert np.array_equal(got_exact, want), (op, k)
+        if op == "max":
+            assert np.array_equal(got, want)
+        else:
+            assert O.normwise_error(got, want) <= O.north_star_tol(k)
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (5, 5), (7, 3), (31, 16), (32, 16), (33, 16),
+                                 (497, 16), (498, 16), (1000, 255), (255, 255)])
+def test_ragged_and_tiny_signals(n, k):
+    rng = np.random.default_rng(n * 1000 + k)
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    for op in ("sum", "max", "avg"):
+        y, _ = FNS[op](x, k, exact=True)
+        assert y.shape == (n - k + 1,)
+        assert np.array_equal(y, O.pool_batched(x[None], k, op)[0])
+
+
+def test_reference_kats():
+    assert sc.sliding_window_sum([1, 2, 3, 4, 5], 3)[0].tolist() == [6, 9, 12]
+    assert sc.sliding_window_max([3, 1, 4, 1, 5], 3)[0].tolist() == [4, 4, 5]
+    x = np.arange(10, dtype=np.float32).reshape(1, 10)
+    y, _ = sc.sliding_window_sum(x, 4)
+    assert y.shape == (1, 7)
+    y, st = sc.sliding_window_sum(np.arange(8, dtype=np.float32), 1)
+    assert np.array_equal(y, np.arange(8, dtype=np.float32)) and st == 0
+
+
+@pytest.mark.parametrize("k", [2, 3, 16, 17, 64, 255, 300])
+def test_max_nan_and_signed_zero_semantics(k):
+    rng = np.random.default_rng(99 + k)
+    x = rng.standard_normal((2, 5000), dtype=np.float32)
+    x[:, ::97] = 0.0
+    x[:, 5::89] = -0.0
+    x[0, 1234] = np.nan
+    x[1, 4000:4003] = np.nan
+    want = O.pool_batched(x, k, "max")
+    got = sc.sliding_window_max(torch.from_numpy(x).cuda(), k)[0].cpu().numpy()
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    m = ~np.isnan(want)
+    assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32))  # +0 vs -0 too
+
+
+def test_host_pipeline_multi_chunk_pageable_and_pinned():
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((80, 262144), dtype=np.float32)     # 84 MB -> 2 chunks
+    want = O.pool_batched(x, 16, "avg")
+    assert np.array_equal(sc.sliding_window_mean(x, 16)[0], want)
+    xp = sc.pinned_empty(x.shape)
+    xp[...] = x
+    assert np.array_equal(sc.sliding_window_mean(xp, 16)[0], want)
+
+
+def test_host_pipeline_single_signal_larger_than_a_chunk():
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal(20_000_000, dtype=np.float32)       # 80 MB, segmented
+    want = O.sliding_window_max(x, 255)[0]
+    assert np.array_equal(sc.sliding_window_max(x, 255)[0], want)
+    want = O.sliding_window_sum(x, 16)[0]
+    assert np.array_equal(sc.sliding_window_sum(x, 16)[0], want)
+
+
+def test_batch_leading_dims_and_empty_batch():
+    x = np.random.default_rng(1).standard_normal((2, 3, 100), dtype=np.float32)
+    y, _ = sc.sliding_window_sum(x, 5)
+    assert y.shape == (2, 3, 96)
+    assert np.array_equal(y.reshape(6, 96), O.pool_batched(x.reshape(6, 100), 5, "sum"))
+    y, _ = sc.sliding_window_sum(np.zeros((0, 10), np.float32), 3)
+    assert y.shape == (0, 8)

@@ -1,0 +1,45 @@
+"""Small fixed workloads for ncu captures (one launch family per name)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_2310_05218_b200 as sc  # noqa: E402
+
+which = sys.argv[1] if len(sys.argv) > 1 else "pool16"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+dev = torch.device("cuda")
+g = torch.Generator(device=dev)
+g.manual_seed(1)
+vm = sc.VectorModel(16)
+if which.startswith("pool"):
+    k = int(which[4:])
+    x = torch.randn((256, 262144), generator=g, device=dev)
+    for _ in range(reps):
+        sc.sliding_window_mean(x, k)
+        sc.sliding_window_max(x, k)
+        sc.sliding_window_sum(x, k)
+elif which in ("conv3", "conv5"):
+    k = int(which[4:])
+    x = torch.rand((32, 4096, 4096), generator=g, device=dev)
+    f = np.random.default_rng(k).standard_normal((k, k), dtype=np.float32) / k
+    for _ in range(reps):
+        sc.conv2d_reference(x, f)
+elif which == "conv1d":
+    x = torch.rand((64, 1 << 20), generator=g, device=dev)
+    f = np.random.default_rng(1).standard_normal((1, 7), dtype=np.float32)
+    for _ in range(reps):
+        sc.conv2d_reference(x, f)
+elif which == "conv7":
+    x = torch.rand((16384, 65536), generator=g, device=dev)
+    f = np.random.default_rng(7).standard_normal((7, 7), dtype=np.float32) / 7
+    for _ in range(reps):
+        sc.conv2d_reference(x, f)
+elif which == "nchw":
+    x = torch.randn((16, 64, 112, 112), generator=g, device=dev)
+    w = torch.randn((64, 64, 3, 3), generator=g, device=dev) / 24
+    for _ in range(reps):
+        sc.conv2d_nchw(x, w, 1)
+torch.cuda.synchronize()
+print("done", which)
