@@ -348,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
     if sampler:
         sampler.start()
         time.sleep(0.2)
-    t_sustain = time.time() + 1.0
+    t_sustain = time.time() + (0.0 if args.no_sustain else 1.0)
     while time.time() < t_sustain:
         for _ in range(20):
             step()
@@ -445,6 +445,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-extras", action="store_true", help="skip the per-config table")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    ap.add_argument("--no-sustain", action="store_true",
+                    help="skip the 1 s pre-load phase (for ncu launch lists)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -37,9 +38,16 @@ template <int KH, int KW>
 struct Taps {
   float f[KH * KW];
 };
+// (f, f) pairs for the packed fp32x2 FMA of the fast path
+template <int KH, int KW>
+struct TapPairs {
+  unsigned long long f[KH * KW];
+};
 
-constexpr int kConsumerWarps = 4;
-constexpr int kColsPerCta = 32 * kConsumerWarps;  // 128 output columns
+constexpr int kConsumerWarps = 2;
+constexpr int kColsPerLane = 2;                                // cols lane and lane + 32
+constexpr int kColsPerWarp = 32 * kColsPerLane;
+constexpr int kColsPerCta = kColsPerWarp * kConsumerWarps;     // 128 output columns
 constexpr int kStages = 4;
 
 template <int KH>
@@ -51,10 +59,31 @@ struct RowsPerStage {
 __host__ __device__ constexpr int box_cols(int kw) { return ((kColsPerCta + kw - 1) + 3) / 4 * 4; }
 __host__ __device__ constexpr int stage_floats(int rs, int bw) { return (rs * bw + 31) / 32 * 32; }
 
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// Fast path: packed FFMA2 over the lane's column pair.  Exact path: scalar
+// __fmul_rn/__fadd_rn (ptxas contracts mul/add.rn.f32x2 into FFMA2, so the
+// packed forms cannot be used for the reference's two-rounding order).
 template <int KH, int KW, bool kExact>
 __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
     conv2d_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
-                      int64_t oh, int64_t ow, int rows_per_cta, const Taps<KH, KW> taps) {
+                      int64_t oh, int64_t ow, int rows_per_cta, const Taps<KH, KW> taps,
+                      const TapPairs<KH, KW> pairs) {
   constexpr int RS = RowsPerStage<KH>::value;
   constexpr int BW = box_cols(KW);
   constexpr int kStageFloats = stage_floats(RS, BW);
@@ -98,15 +127,19 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
     return;
   }
 
-  // ---------------- consumers
-  const int col = warp * 32 + lane;  // column within the strip
+  // ---------------- consumers: lane owns columns col and col + 32
+  const int col = warp * kColsPerWarp + lane;
   const int64_t gcol = (int64_t)c0 + col;
-  const bool col_ok = gcol < ow;
-  float* yb = y + ((int64_t)b * oh + r0) * ow + gcol;
+  const bool ok0 = gcol < ow, ok1 = gcol + 32 < ow;
+  float* yp = y + ((int64_t)b * oh + r0) * ow + gcol;  // output row 0 of this CTA
 
-  float acc[KH];
+  float a0[KH], a1[KH];                 // exact path accumulators
+  unsigned long long ap[KH];            // fast path packed accumulators
 #pragma unroll
-  for (int j = 0; j < KH; ++j) acc[j] = 0.0f;
+  for (int j = 0; j < KH; ++j) {
+    a0[j] = a1[j] = 0.0f;
+    ap[j] = 0ull;
+  }
 
   for (int s = 0; s < n_stage; ++s) {
     const int slot = s % kStages;
@@ -116,24 +149,60 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
     for (int g = 0; g < RS / KH; ++g) {
 #pragma unroll
       for (int u = 0; u < KH; ++u) {
-        const int t = s * RS + g * KH + u;  // input row relative to r0
         const float* rowp = buf + (g * KH + u) * BW;
-        float v[KW];
-#pragma unroll
-        for (int i = 0; i < KW; ++i) v[i] = rowp[i];
         // output row t - j lives in slot (u - j) mod KH; RS % KH == 0 keeps
         // (t mod KH) == u, so every index below is a compile-time constant.
+        if constexpr (kExact) {
+          float v0[KW], v1[KW];
 #pragma unroll
-        for (int j = 0; j < KH; ++j) {
-          const int sl = ((u - j) % KH + KH) % KH;
-          float a = (j == 0) ? 0.0f : acc[sl];
+          for (int i = 0; i < KW; ++i) {
+            v0[i] = rowp[i];
+            v1[i] = rowp[32 + i];
+          }
 #pragma unroll
-          for (int i = 0; i < KW; ++i) a = mac<kExact>(a, taps.f[j * KW + i], v[i]);
-          acc[sl] = a;
+          for (int j = 0; j < KH; ++j) {
+            const int sl = ((u - j) % KH + KH) % KH;
+            float p = (j == 0) ? 0.0f : a0[sl];
+            float q = (j == 0) ? 0.0f : a1[sl];
+#pragma unroll
+            for (int i = 0; i < KW; ++i) {
+              p = mac<true>(p, taps.f[j * KW + i], v0[i]);
+              q = mac<true>(q, taps.f[j * KW + i], v1[i]);
+            }
+            a0[sl] = p;
+            a1[sl] = q;
+          }
+        } else {
+          unsigned long long v[KW];
+#pragma unroll
+          for (int i = 0; i < KW; ++i) v[i] = pack2(rowp[i], rowp[32 + i]);
+#pragma unroll
+          for (int j = 0; j < KH; ++j) {
+            const int sl = ((u - j) % KH + KH) % KH;
+            unsigned long long p = (j == 0) ? 0ull : ap[sl];
+#pragma unroll
+            for (int i = 0; i < KW; ++i) p = ffma2(v[i], pairs.f[j * KW + i], p);
+            ap[sl] = p;
+          }
         }
         // output row t - KH + 1 is complete
+        const int t = s * RS + g * KH + u;  // input row relative to r0
         const int o = t - (KH - 1);
-        if (o >= 0 && o < rc && col_ok) yb[(int64_t)o * ow] = acc[((u + 1) % KH)];
+        if ((unsigned)o < (unsigned)rc) {
+          const int sl = (u + 1) % KH;
+          float r0v, r1v;
+          if constexpr (kExact) {
+            r0v = a0[sl];
+            r1v = a1[sl];
+          } else {
+            const float2 pr = unpack2(ap[sl]);
+            r0v = pr.x;
+            r1v = pr.y;
+          }
+          float* dst = yp + (int64_t)o * ow;
+          if (ok0) dst[0] = r0v;
+          if (ok1) dst[32] = r1v;
+        }
       }
     }
     __syncwarp();
@@ -205,7 +274,13 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   int rc = make_tmap(&map, x, batch, h, w, BW, RS);
   if (rc) return rc;
   Taps<KH, KW> taps;
-  for (int i = 0; i < KH * KW; ++i) taps.f[i] = f[i];
+  TapPairs<KH, KW> pairs;
+  for (int i = 0; i < KH * KW; ++i) {
+    taps.f[i] = f[i];
+    unsigned int bits;
+    std::memcpy(&bits, &f[i], 4);
+    pairs.f[i] = ((unsigned long long)bits << 32) | bits;
+  }
   // rows per CTA: enough CTAs for >= ~8 waves of 148 SMs, RS-aligned
   const int64_t strips = (ow + kColsPerCta - 1) / kColsPerCta;
   const int64_t want_ctas = (int64_t)sm_count() * 48;
@@ -225,7 +300,7 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   }
   dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
   conv2d_tma_kernel<KH, KW, kExact><<<grid, 32 * (kConsumerWarps + 1), smem, st>>>(
-      map, y, oh, ow, (int)rows, taps);
+      map, y, oh, ow, (int)rows, taps, pairs);
   SC_LAUNCH_CHECK("conv2d_tma_kernel");
   return SC_OK;
 }
@@ -269,6 +344,8 @@ int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
 }
 
 }  // namespace
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return get_encode(); }
 
 int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                         int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st) {

@@ -21,6 +21,8 @@
 #include "common.cuh"
 
 namespace sc {
+int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+               cudaStream_t st);
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
@@ -140,10 +142,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   if (gw >= batch * chunks_per_row) return;
   const int kk = kK > 0 ? kK : k;
   const int valid = 32 * T - (kk - 1);
-  const int64_t row = gw / chunks_per_row;
-  const int64_t base = (gw - row * chunks_per_row) * (int64_t)valid;
+  // host guarantees batch * chunks_per_row < 2^32: 32-bit division
+  const unsigned cpr = (unsigned)chunks_per_row;
+  const unsigned row = (unsigned)gw / cpr;
+  const int64_t base = (int64_t)((unsigned)gw - row * cpr) * valid;
   const int64_t out_len = length - kk + 1;
-  const float* xr = x + row * length + base;
+  const float* xr = x + (int64_t)row * length + base;
   const int64_t avail = length - base;  // samples of this row from base on
 
   float s[T];
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
   }
 
   const int64_t lim = min((int64_t)valid, out_len - base);
-  float* yr = y + row * out_len + base;
+  float* yr = y + (int64_t)row * out_len + base;
   const float fk = (float)kk;
 #pragma unroll
   for (int j = 0; j < T; ++j) {
@@ -286,7 +290,8 @@ int launch_reg(const float* x, int64_t batch, int64_t length, int k, float* y,
   const int64_t chunks = (out_len + valid - 1) / valid;
   const int64_t warps = batch * chunks;
   const int64_t blocks = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  if (blocks > 0x7fffffffLL) return fail(SC_ERR_UNSUPPORTED, "pool1d: grid too large");
+  if (blocks > 0x7fffffffLL || warps >= 0xffffffffLL)
+    return fail(SC_ERR_UNSUPPORTED, "pool1d: grid too large");
   pool_reg_kernel<kOp, T, M, kK><<<(unsigned)blocks, 32 * kWarpsPerBlock, 0, st>>>(
       x, batch, length, k, y, chunks);
   SC_LAUNCH_CHECK("pool_reg_kernel");
@@ -413,6 +418,11 @@ template <int kOp>
 int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode, float* y,
              cudaStream_t st) {
   const bool exact = mode == SC_MODE_EXACT;
+  // TMA-staged blocked kernel: bit-exact doubling order, so it serves both modes
+  {
+    const int rc = pool1d_tma(kOp, x, batch, length, k, y, st);
+    if (rc != 1) return rc;
+  }
   // compile-time specialisations for the BASELINE windows
   if (k == 16) return launch_reg<kOp, 16, 1, 16>(x, batch, length, 16, y, st);
   if (k == 3) return launch_reg<kOp, 16, 1, 3>(x, batch, length, 3, y, st);

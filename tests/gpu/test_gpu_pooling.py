@@ -41,9 +41,12 @@ def test_config2_full_size(cfg2, op, k):
 
 @pytest.mark.parametrize("k", list(range(1, 40)) + [47, 63, 64, 65, 100, 127, 128, 129, 200, 255,
                                                      256, 257, 300, 511, 1000, 4097, 9000])
-def test_every_window_branch(k):
+@pytest.mark.parametrize("n", [12_345, 8192, 544])
+def test_every_window_branch(k, n):
     rng = np.random.default_rng(k)
-    n = 12_345 + k
+    n = n + (k if n == 12_345 else 0)          # ragged lengths hit the striped kernel,
+    if k > n:                                   # multiples of 32 the TMA kernel
+        pytest.skip("window longer than the signal")
     x = rng.standard_normal((3, n), dtype=np.float32)
     xd = torch.from_numpy(x).cuda()
     for op in ("sum", "max", "avg"):
@@ -78,14 +81,17 @@ def test_reference_kats():
     assert np.array_equal(y, np.arange(8, dtype=np.float32)) and st == 0
 
 
-@pytest.mark.parametrize("k", [2, 3, 16, 17, 64, 255, 300])
-def test_max_nan_and_signed_zero_semantics(k):
+@pytest.mark.parametrize("n", [5000, 5024])
+@pytest.mark.parametrize("k", [2, 3, 16, 17, 33, 64, 255, 300])
+def test_max_nan_and_signed_zero_semantics(k, n):
     rng = np.random.default_rng(99 + k)
-    x = rng.standard_normal((2, 5000), dtype=np.float32)
+    x = rng.standard_normal((2, n), dtype=np.float32)
     x[:, ::97] = 0.0
     x[:, 5::89] = -0.0
     x[0, 1234] = np.nan
     x[1, 4000:4003] = np.nan
+    x[0, 3000:3100:3] = -0.0                     # dense +0/-0 ties
+    x[0, 3001:3100:3] = 0.0
     want = O.pool_batched(x, k, "max")
     got = sc.sliding_window_max(torch.from_numpy(x).cuda(), k)[0].cpu().numpy()
     assert np.array_equal(np.isnan(got), np.isnan(want))
