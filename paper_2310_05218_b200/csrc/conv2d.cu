@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
   const int col = warp * kColsPerWarp + lane;
   const int64_t gcol = (int64_t)c0 + col;
   const bool ok0 = gcol < ow, ok1 = gcol + 32 < ow;
-  float* yp = y + ((int64_t)b * oh + r0) * ow + gcol;  // output row 0 of this CTA
+  // address of output row (t - KH + 1) for the input row t being consumed
+  float* ynext = y + ((int64_t)b * oh + r0 - (KH - 1)) * ow + gcol;
 
   float a0[KH], a1[KH];                 // exact path accumulators
   unsigned long long ap[KH];            // fast path packed accumulators
@@ -185,10 +186,9 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
             ap[sl] = p;
           }
         }
-        // output row t - KH + 1 is complete
+        // output row t - KH + 1 is complete; ynext tracks its address
         const int t = s * RS + g * KH + u;  // input row relative to r0
-        const int o = t - (KH - 1);
-        if ((unsigned)o < (unsigned)rc) {
+        if ((unsigned)(t - (KH - 1)) < (unsigned)rc) {
           const int sl = (u + 1) % KH;
           float r0v, r1v;
           if constexpr (kExact) {
@@ -199,10 +199,10 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
             r0v = pr.x;
             r1v = pr.y;
           }
-          float* dst = yp + (int64_t)o * ow;
-          if (ok0) dst[0] = r0v;
-          if (ok1) dst[32] = r1v;
+          if (ok0) ynext[0] = r0v;
+          if (ok1) ynext[32] = r1v;
         }
+        ynext += ow;
       }
     }
     __syncwarp();

@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <utility>
 
 #include "common.cuh"
@@ -31,7 +32,7 @@ constexpr int kTmaT = 16;                    // samples per lane
 constexpr int kTmaWin = 32 * kTmaT;          // samples per warp window
 constexpr int kStageStride = kTmaT + 4;      // padded staging row (floats)
 
-__host__ __device__ constexpr int tma_valid(int k) { return kTmaWin - ((k - 1 + 3) / 4) * 4; }
+__host__ __device__ constexpr int tma_valid(int k) { return kTmaWin - ((k - 1 + 31) / 32) * 32; }
 __host__ __device__ constexpr int tma_rows(int k) {
   return ((kTmaWarps - 1) * tma_valid(k) + kTmaWin + 31) / 32;
 }
@@ -41,6 +42,17 @@ __device__ __forceinline__ float max_nan(float a, float b) {
   float d;
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
   return d;
+}
+
+// Correctly rounded a / k from the correctly rounded reciprocal r = RN(1/k):
+// q = RN(a r) is within an ulp of a/k, the FMA residual a - k q is exact, and
+// RN(q + r (a - k q)) is RN(a/k) (Markstein's theorem).  Tiny or non-finite
+// numerators take the IEEE division (underflow voids the theorem).
+__device__ __forceinline__ float div_by_k(float a, float k, float r) {
+  const float q = a * r;
+  const float e = fmaf(-k, q, a);
+  const float q2 = fmaf(e, r, q);
+  return (fabsf(a) < 1e-30f || !(fabsf(a) < 3.0e38f)) ? __fdiv_rn(a, k) : q2;
 }
 
 template <int kOp, bool kExactMax>
@@ -114,45 +126,54 @@ __device__ __forceinline__ void blocked_pool(float (&s)[T]) {
   }
 }
 
-template <int kOp, int K>
-__global__ void __launch_bounds__(32 * kTmaWarps)
+template <int kOp, int K, int NBUF>
+__global__ void __launch_bounds__(32 * (kTmaWarps + 1))
     pool_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                     int64_t out_len, int64_t tiles_per_row, int64_t n_tiles) {
   constexpr int T = kTmaT;
   constexpr int V = tma_valid(K);
   constexpr int BUF = tma_buf_bytes(K);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[2];
+  __shared__ __align__(8) uint64_t full_bar[NBUF];
+  __shared__ __align__(8) uint64_t empty_bar[NBUF];
   unsigned char* base =
       smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);  // swizzle-128B: 1 KiB aligned
-  float* stage_all = reinterpret_cast<float*>(base + 2 * BUF);
+  float* stage_all = reinterpret_cast<float*>(base + NBUF * BUF);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    mbar_init(&full_bar[0], 1);
-    mbar_init(&full_bar[1], 1);
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kTmaWarps);
+    }
     fence_mbar_init();
-    prefetch_tmap(&tmap);
   }
   __syncthreads();
 
   // tile t -> (row, first output); 32-bit math (host guarantees the range)
   const unsigned tpr = (unsigned)tiles_per_row;
-  auto issue = [&](unsigned t, int b) {
-    const unsigned row = t / tpr;
-    const unsigned s0 = (t - row * tpr) * (unsigned)(kTmaWarps * V);
-    mbar_arrive_expect_tx(&full_bar[b], tma_rows(K) * 128);
-    tma_load_3d(base + b * BUF, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
-  };
   const unsigned G = gridDim.x;
   const unsigned nt = (unsigned)n_tiles;
-  if (tid == 0) {
-    if (blockIdx.x < nt) issue(blockIdx.x, 0);
-    if (blockIdx.x + G < nt) issue(blockIdx.x + G, 1);
+
+  if (warp == kTmaWarps) {
+    // ------------- producer warp: one lane streams this CTA's tiles
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      int i = 0;
+      for (unsigned t = blockIdx.x; t < nt; t += G, ++i) {
+        const int b = i % NBUF;
+        if (i >= NBUF) mbar_wait(&empty_bar[b], ((i / NBUF) - 1) & 1);
+        const unsigned row = t / tpr;
+        const unsigned s0 = (t - row * tpr) * (unsigned)(kTmaWarps * V);
+        mbar_arrive_expect_tx(&full_bar[b], tma_rows(K) * 128);
+        tma_load_3d(base + b * BUF, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
+      }
+    }
+    return;
   }
 
-  // this lane's first sample inside the buffer and its swizzled chunk addresses
-  const int p0 = warp * V + T * lane;
+  // ------------- consumer warps
+  const int p0 = warp * V + T * lane;  // this lane's first sample in the buffer
   float* stage = stage_all + warp * (32 * kStageStride);
   const float fk = (float)K;
   const float inv_k = 1.0f / fk;
@@ -160,8 +181,8 @@ __global__ void __launch_bounds__(32 * kTmaWarps)
 
   int it = 0;
   for (unsigned t = blockIdx.x; t < nt; t += G, ++it) {
-    const int b = it & 1;
-    mbar_wait(&full_bar[b], (it >> 1) & 1);
+    const int b = it % NBUF;
+    mbar_wait(&full_bar[b], (it / NBUF) & 1);
     const unsigned char* buf = base + b * BUF;
     float s[T];
     auto load = [&]() {
@@ -177,21 +198,30 @@ __global__ void __launch_bounds__(32 * kTmaWarps)
         s[4 * q + 3] = v.w;
       }
     };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[b]);
+    };
     load();
+    release();  // the window is in registers: hand the buffer back at once
     if constexpr (kOp == SC_POOL_MAX) {
+      float s_in[T];
+#pragma unroll
+      for (int j = 0; j < T; ++j) s_in[j] = s[j];
       blocked_pool<T, kOp, false, K>(s);
       bool zero = false;
 #pragma unroll
       for (int j = 0; j < T; ++j) zero |= (s[j] == 0.0f) && (T * lane + j < V);
       if (__any_sync(0xffffffffu, zero)) {  // rare: redo with np.maximum's order
-        load();
+#pragma unroll
+        for (int j = 0; j < T; ++j) s[j] = s_in[j];
         blocked_pool<T, kOp, true, K>(s);
       }
     } else {
       blocked_pool<T, kOp, false, K>(s);
       if constexpr (kOp == SC_POOL_AVG) {
 #pragma unroll
-        for (int j = 0; j < T; ++j) s[j] = kPow2 ? s[j] * inv_k : __fdiv_rn(s[j], fk);
+        for (int j = 0; j < T; ++j) s[j] = kPow2 ? s[j] * inv_k : div_by_k(s[j], fk, inv_k);
       }
     }
     // stage (padded rows, conflict-free STS.128) -> coalesced 32-bit stores
@@ -216,14 +246,12 @@ __global__ void __launch_bounds__(32 * kTmaWarps)
       for (int m = 0; m < (V + 31) / 32; ++m)
         if (32 * m + lane < lim) yr[32 * m] = sp[(32 / T) * m * kStageStride];
     }
-    __syncthreads();  // buffer b and the staging slab are free again
-    if (tid == 0 && t + 2 * G < nt) issue(t + 2 * G, b);
+    __syncwarp();  // staging slab reused by the next tile
   }
 }
 
-
-template <int kOp, int K>
-int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
+template <int kOp, int K, int NBUF>
+int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
@@ -240,22 +268,40 @@ int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStre
   const int64_t tiles_per_row = (out_len + kTmaWarps * V - 1) / (kTmaWarps * V);
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;  // not applicable: caller falls back
-  const size_t smem = 1024 + 2 * (size_t)tma_buf_bytes(K) +
+  const size_t smem = 1024 + NBUF * (size_t)tma_buf_bytes(K) +
                       (size_t)kTmaWarps * 32 * kStageStride * sizeof(float);
   static bool attr = false;
   if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(pool_tma_kernel<kOp, K>,
+    SC_CUDA(cudaFuncSetAttribute(pool_tma_kernel<kOp, K, NBUF>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   int per_sm = 0;
-  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pool_tma_kernel<kOp, K>,
-                                                        32 * kTmaWarps, smem));
+  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pool_tma_kernel<kOp, K, NBUF>,
+                                                        32 * (kTmaWarps + 1), smem));
   const int64_t grid = std::min<int64_t>(n_tiles, (int64_t)sm_count() * std::max(1, per_sm));
-  pool_tma_kernel<kOp, K><<<(unsigned)grid, 32 * kTmaWarps, smem, st>>>(map, y, out_len,
+  pool_tma_kernel<kOp, K, NBUF><<<(unsigned)grid, 32 * (kTmaWarps + 1), smem, st>>>(map, y, out_len,
                                                                        tiles_per_row, n_tiles);
   SC_LAUNCH_CHECK("pool_tma_kernel");
   return SC_OK;
+}
+
+int env_nbuf() {
+  static int v = [] {
+    const char* e = getenv("SC_POOL_NBUF");
+    int n = e ? atoi(e) : 0;
+    return (n >= 2 && n <= 4) ? n : 4;
+  }();
+  return v;
+}
+
+template <int kOp, int K>
+int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
+  switch (env_nbuf()) {
+    case 2: return launch_nbuf<kOp, K, 2>(x, batch, length, y, st);
+    case 4: return launch_nbuf<kOp, K, 4>(x, batch, length, y, st);
+    default: return launch_nbuf<kOp, K, 3>(x, batch, length, y, st);
+  }
 }
 
 template <int kOp, int... Ks>

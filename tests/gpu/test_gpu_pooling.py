@@ -125,3 +125,14 @@ def test_batch_leading_dims_and_empty_batch():
     assert np.array_equal(y.reshape(6, 96), O.pool_batched(x.reshape(6, 100), 5, "sum"))
     y, _ = sc.sliding_window_sum(np.zeros((0, 10), np.float32), 3)
     assert y.shape == (0, 8)
+
+
+@pytest.mark.parametrize("k", [3, 5, 7, 9, 11, 13, 17, 31, 33])
+def test_average_division_is_ieee(k):
+    # avg = float32(sum) / float32(k); the TMA kernel divides by a reciprocal
+    # plus an FMA correction, which must be bit-identical to IEEE division
+    rng = np.random.default_rng(1000 + k)
+    scale = np.exp(rng.uniform(-60, 60, (8, 1))).astype(np.float32)
+    x = (rng.standard_normal((8, 16384), dtype=np.float32) * scale).astype(np.float32)
+    got = sc.sliding_window_mean(torch.from_numpy(x).cuda(), k)[0].cpu().numpy()
+    assert np.array_equal(got, O.pool_batched(x, k, "avg"))
