@@ -109,15 +109,26 @@ def roofline(alg_bytes, flops, seconds, hbm_peak):
 
 
 def time_launches(torch, fn, reps, warmup, flush=None):
-    """Per-launch device time (CUDA events on the current stream), median."""
+    """Steady-state device time per call (CUDA events on the current stream).
+    Without `flush`, `reps` calls run back to back between two events (inputs
+    are larger than L2); with `flush`, L2 is overwritten before each timed
+    call and the median of per-call event pairs is returned."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
-    times = []
     st = torch.cuda.current_stream()
+    if flush is None:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        b.synchronize()
+        return a.elapsed_time(b) / 1e3 / reps
+    times = []
     for _ in range(reps):
-        if flush is not None:
-            flush()
+        flush()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(st)
@@ -404,7 +415,9 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     dom = max(t_avg, t_max)
-    dom_name = "pool_reg_kernel<AVG,T=16,k=16>" if t_avg >= t_max else "pool_reg_kernel<MAX,T=16,k=16>"
+    nbuf = os.environ.get("SC_POOL_NBUF", "4")
+    dom_name = (f"pool_tma_kernel<1, 16, {nbuf}>" if t_avg >= t_max
+                else f"pool_tma_kernel<2, 16, {nbuf}>")  # <op (1 = AVG, 2 = MAX), k, ring depth>
     achieved = alg_bytes_op / dom / 1e9
     tr = traffic.get(dom_name)
     line = {
