@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -146,20 +147,31 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
     const int slot = s % kStages;
     mbar_wait(&full_bar[slot], (s / kStages) & 1);
     const float* buf = smem + slot * kStageFloats + col;
+    // software pipeline over the stage's rows: the taps of row r+1 are read
+    // from shared memory while row r's FMAs run (hides the LDS latency)
+    float c0v[KW], c1v[KW];
+#pragma unroll
+    for (int i = 0; i < KW; ++i) {
+      c0v[i] = buf[i];
+      c1v[i] = buf[32 + i];
+    }
 #pragma unroll 1
     for (int g = 0; g < RS / KH; ++g) {
 #pragma unroll
       for (int u = 0; u < KH; ++u) {
-        const float* rowp = buf + (g * KH + u) * BW;
+        const int rr = g * KH + u;  // row within the stage
+        float n0v[KW], n1v[KW];
+        if (u < KH - 1 || rr + 1 < RS) {
+          const float* nx = buf + (rr + 1) * BW;
+#pragma unroll
+          for (int i = 0; i < KW; ++i) {
+            n0v[i] = nx[i];
+            n1v[i] = nx[32 + i];
+          }
+        }
         // output row t - j lives in slot (u - j) mod KH; RS % KH == 0 keeps
         // (t mod KH) == u, so every index below is a compile-time constant.
         if constexpr (kExact) {
-          float v0[KW], v1[KW];
-#pragma unroll
-          for (int i = 0; i < KW; ++i) {
-            v0[i] = rowp[i];
-            v1[i] = rowp[32 + i];
-          }
 #pragma unroll
           for (int j = 0; j < KH; ++j) {
             const int sl = ((u - j) % KH + KH) % KH;
@@ -167,8 +179,8 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
             float q = (j == 0) ? 0.0f : a1[sl];
 #pragma unroll
             for (int i = 0; i < KW; ++i) {
-              p = mac<true>(p, taps.f[j * KW + i], v0[i]);
-              q = mac<true>(q, taps.f[j * KW + i], v1[i]);
+              p = mac<true>(p, taps.f[j * KW + i], c0v[i]);
+              q = mac<true>(q, taps.f[j * KW + i], c1v[i]);
             }
             a0[sl] = p;
             a1[sl] = q;
@@ -176,7 +188,7 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
         } else {
           unsigned long long v[KW];
 #pragma unroll
-          for (int i = 0; i < KW; ++i) v[i] = pack2(rowp[i], rowp[32 + i]);
+          for (int i = 0; i < KW; ++i) v[i] = pack2(c0v[i], c1v[i]);
 #pragma unroll
           for (int j = 0; j < KH; ++j) {
             const int sl = ((u - j) % KH + KH) % KH;
@@ -186,8 +198,13 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
             ap[sl] = p;
           }
         }
+#pragma unroll
+        for (int i = 0; i < KW; ++i) {
+          c0v[i] = n0v[i];
+          c1v[i] = n1v[i];
+        }
         // output row t - KH + 1 is complete; ynext tracks its address
-        const int t = s * RS + g * KH + u;  // input row relative to r0
+        const int t = s * RS + rr;  // input row relative to r0
         if ((unsigned)(t - (KH - 1)) < (unsigned)rc) {
           const int sl = (u + 1) % KH;
           float r0v, r1v;
@@ -283,12 +300,23 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   }
   // rows per CTA: enough CTAs for >= ~8 waves of 148 SMs, RS-aligned
   const int64_t strips = (ow + kColsPerCta - 1) / kColsPerCta;
-  const int64_t want_ctas = (int64_t)sm_count() * 48;
-  int64_t segs = std::max<int64_t>(1, want_ctas / std::max<int64_t>(1, strips * batch));
-  int64_t rows = (oh + segs - 1) / segs;
-  rows = std::max<int64_t>(rows, 4 * RS);
+  int64_t rows;
+  static const int env_rows = [] {
+    const char* e = getenv("SC_CONV_ROWS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_rows > 0) {
+    rows = env_rows;
+  } else {
+    // measured on B200 (tools/conv_sweep.py): short row segments keep the
+    // concurrently streamed rows adjacent in HBM for the bandwidth-bound
+    // sizes; the FP32-bound 7x7 prefers long segments (less halo re-work).
+    // Segment length = RS*m - (KH-1) so the last stage carries no waste.
+    const int m = KH >= 7 ? 64 : (KH == 1 ? 7 : (KH == 3 ? 5 : 6));
+    rows = (int64_t)RS * m - (KH - 1);
+  }
   rows = std::min<int64_t>(rows, oh);
-  segs = (oh + rows - 1) / rows;
+  const int64_t segs = (oh + rows - 1) / rows;
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
     return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
   const size_t smem = (size_t)kStages * stage_floats(RS, BW) * sizeof(float) + 128;

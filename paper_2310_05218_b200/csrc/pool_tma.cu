@@ -129,7 +129,7 @@ __device__ __forceinline__ void blocked_pool(float (&s)[T]) {
 template <int kOp, int K, int NBUF>
 __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
     pool_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
-                    int64_t out_len, int64_t tiles_per_row, int64_t n_tiles) {
+                    int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta) {
   constexpr int T = kTmaT;
   constexpr int V = tma_valid(K);
   constexpr int BUF = tma_buf_bytes(K);
@@ -151,16 +151,19 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
   __syncthreads();
 
   // tile t -> (row, first output); 32-bit math (host guarantees the range)
+  // CTA b owns the contiguous tiles [b*tpc, min((b+1)*tpc, n)): the hardware
+  // block scheduler then keeps the in-flight window of memory contiguous
+  // (measured: grid-stride persistent loops lose ~10% HBM bandwidth on B200)
   const unsigned tpr = (unsigned)tiles_per_row;
-  const unsigned G = gridDim.x;
-  const unsigned nt = (unsigned)n_tiles;
+  const unsigned t_begin = blockIdx.x * (unsigned)tiles_per_cta;
+  const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
 
   if (warp == kTmaWarps) {
     // ------------- producer warp: one lane streams this CTA's tiles
     if (lane == 0) {
       prefetch_tmap(&tmap);
       int i = 0;
-      for (unsigned t = blockIdx.x; t < nt; t += G, ++i) {
+      for (unsigned t = t_begin; t < nt; ++t, ++i) {
         const int b = i % NBUF;
         if (i >= NBUF) mbar_wait(&empty_bar[b], ((i / NBUF) - 1) & 1);
         const unsigned row = t / tpr;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
   constexpr bool kPow2 = (K & (K - 1)) == 0;
 
   int it = 0;
-  for (unsigned t = blockIdx.x; t < nt; t += G, ++it) {
+  for (unsigned t = t_begin; t < nt; ++t, ++it) {
     const int b = it % NBUF;
     mbar_wait(&full_bar[b], (it / NBUF) & 1);
     const unsigned char* buf = base + b * BUF;
@@ -250,6 +253,21 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
   }
 }
 
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = getenv(name);
+  const int n = e ? atoi(e) : dflt;
+  return (n >= lo && n <= hi) ? n : dflt;
+}
+
+int env_nbuf() {
+  static int v = [] {
+    const char* e = getenv("SC_POOL_NBUF");
+    int n = e ? atoi(e) : 0;
+    return (n == 1 || n == 2 || n == 4) ? n : 2;
+  }();
+  return v;
+}
+
 template <int kOp, int K, int NBUF>
 int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
   auto enc = tensor_map_encoder();
@@ -276,31 +294,20 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  int per_sm = 0;
-  SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pool_tma_kernel<kOp, K, NBUF>,
-                                                        32 * (kTmaWarps + 1), smem));
-  const int64_t grid = std::min<int64_t>(n_tiles, (int64_t)sm_count() * std::max(1, per_sm));
-  pool_tma_kernel<kOp, K, NBUF><<<(unsigned)grid, 32 * (kTmaWarps + 1), smem, st>>>(map, y, out_len,
-                                                                       tiles_per_row, n_tiles);
+  const int tpc = env_int("SC_POOL_TPC", 4, 1, 64);
+  const int64_t grid = (n_tiles + tpc - 1) / tpc;
+  pool_tma_kernel<kOp, K, NBUF><<<(unsigned)grid, 32 * (kTmaWarps + 1), smem, st>>>(
+      map, y, out_len, tiles_per_row, n_tiles, tpc);
   SC_LAUNCH_CHECK("pool_tma_kernel");
   return SC_OK;
-}
-
-int env_nbuf() {
-  static int v = [] {
-    const char* e = getenv("SC_POOL_NBUF");
-    int n = e ? atoi(e) : 0;
-    return (n >= 2 && n <= 4) ? n : 4;
-  }();
-  return v;
 }
 
 template <int kOp, int K>
 int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
   switch (env_nbuf()) {
-    case 2: return launch_nbuf<kOp, K, 2>(x, batch, length, y, st);
+    case 1: return launch_nbuf<kOp, K, 1>(x, batch, length, y, st);
     case 4: return launch_nbuf<kOp, K, 4>(x, batch, length, y, st);
-    default: return launch_nbuf<kOp, K, 3>(x, batch, length, y, st);
+    default: return launch_nbuf<kOp, K, 2>(x, batch, length, y, st);
   }
 }
 

@@ -1,4 +1,4 @@
-"""Back-to-back timing of the pooling kernels vs a torch copy of the same bytes."""
+"""Back-to-back timing of the pooling kernels vs a device copy of the same bytes."""
 import os
 import sys
 
@@ -9,6 +9,8 @@ import paper_2310_05218_b200 as sc  # noqa: E402
 
 x = torch.randn((256, 262144), device="cuda")
 y = torch.empty_like(x)
+ks = [int(v) for v in os.environ.get("KS", "16,3,64").split(",")]
+ops = os.environ.get("OPS", "avg,max,sum").split(",")
 
 
 def bench(fn, n=50):
@@ -24,16 +26,14 @@ def bench(fn, n=50):
     return a.elapsed_time(b) / n * 1e3
 
 
-nb = 4 * (x.numel() * 2)
-t = bench(lambda: y.copy_(x))
-print(f"torch copy 268MB: {t:.1f} us  {nb / t / 1e3:.0f} GB/s")
-big = torch.empty(1 << 30, dtype=torch.bfloat16, device="cuda")
-big2 = torch.empty_like(big)
-t = bench(lambda: big2.copy_(big), 20)
-print(f"torch copy 2GiB: {t:.1f} us  {4 * (1 << 30) / t / 1e3:.0f} GB/s")
-for k in (16, 3, 64):
-    for name, fn in (("avg", sc.sliding_window_mean), ("max", sc.sliding_window_max),
-                     ("sum", sc.sliding_window_sum)):
-        t = bench(lambda: fn(x, k))
-        print(f"NBUF={os.environ.get('SC_POOL_NBUF', '3')} k={k} {name}: {t:.1f} us  "
-              f"{4 * (x.numel() + 256 * (262144 - k + 1)) / t / 1e3:.0f} GB/s")
+tag = f"NBUF={os.environ.get('SC_POOL_NBUF', '-')} TPC={os.environ.get('SC_POOL_TPC', '-')}"
+if os.environ.get("COPY", "0") == "1":
+    t = bench(lambda: y.copy_(x))
+    print(f"copy 268MB: {t:.1f} us  {4 * x.numel() * 2 / t / 1e3:.0f} GB/s")
+fns = {"avg": sc.sliding_window_mean, "max": sc.sliding_window_max, "sum": sc.sliding_window_sum}
+for k in ks:
+    row = []
+    for name in ops:
+        t = bench(lambda: fns[name](x, k))
+        row.append(f"{name} {t:6.1f}us {4 * (x.numel() + 256 * (262144 - k + 1)) / t / 1e3:5.0f}GB/s")
+    print(f"{tag} k={k}: " + " | ".join(row))
