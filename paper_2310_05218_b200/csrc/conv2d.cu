@@ -374,11 +374,20 @@ int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
 }  // namespace
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return get_encode(); }
+int conv1d_tma(const float* x, int64_t rows, int64_t length, const float* w, int64_t k,
+               bool exact, float* y, cudaStream_t st);
 
 int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                         int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st) {
   bool done = false;
   int rc = SC_OK;
+  if (kh == 1) {
+    // a 1 x k filter over (batch*h) rows == batched 1-D convolution: the TMA
+    // blocked-register kernel shared with pooling (csrc/pool_tma.cu)
+    rc = conv1d_tma(x, batch * h, w, f, kw, exact, y, st);
+    if (rc != 1) return rc;
+    rc = SC_OK;
+  }
   if (kh == 3 && kw == 3) rc = try_tma<3, 3>(x, batch, h, w, f, exact, y, st, &done);
   else if (kh == 5 && kw == 5) rc = try_tma<5, 5>(x, batch, h, w, f, exact, y, st, &done);
   else if (kh == 7 && kw == 7) rc = try_tma<7, 7>(x, batch, h, w, f, exact, y, st, &done);

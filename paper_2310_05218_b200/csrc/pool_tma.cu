@@ -28,6 +28,14 @@ namespace {
 // order whenever one of its outputs is zero (the only case -- a +0/-0 tie --
 // where the two can differ), hence bit-exact maxima.
 constexpr int kTmaWarps = 8;
+// kernel "ops" beyond sc_pool_op: 1-D convolution with K taps (BASELINE config 1)
+constexpr int kConvFast = 3;
+constexpr int kConvExact = 4;
+
+template <int K>
+struct Taps1 {
+  float f[K];
+};
 constexpr int kTmaT = 16;                    // samples per lane
 constexpr int kTmaWin = 32 * kTmaT;          // samples per warp window
 constexpr int kStageStride = kTmaT + 4;      // padded staging row (floats)
@@ -126,10 +134,30 @@ __device__ __forceinline__ void blocked_pool(float (&s)[T]) {
   }
 }
 
+// y[j] = sum_i f[i] x[j + i] on the blocked window: the K-1 samples past the
+// lane's 16 come from the next lane(s) by shuffle; exact = reference order
+// (reference.py:19-22: multiply then add, taps ascending, from 0).
+template <int T, int K, bool kExact>
+__device__ __forceinline__ void blocked_conv(float (&s)[T], const Taps1<K>& taps) {
+  float e[T + K - 1];
+#pragma unroll
+  for (int j = 0; j < T; ++j) e[j] = s[j];
+#pragma unroll
+  for (int i = 0; i < K - 1; ++i) e[T + i] = __shfl_down_sync(0xffffffffu, s[i % T], 1 + i / T);
+#pragma unroll
+  for (int j = 0; j < T; ++j) {
+    float a = 0.0f;
+#pragma unroll
+    for (int i = 0; i < K; ++i) a = mac<kExact>(a, taps.f[i], e[j + i]);
+    s[j] = a;
+  }
+}
+
 template <int kOp, int K, int NBUF>
 __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
     pool_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
-                    int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta) {
+                    int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
+                    const Taps1<K> taps) {
   constexpr int T = kTmaT;
   constexpr int V = tma_valid(K);
   constexpr int BUF = tma_buf_bytes(K);
@@ -220,6 +248,8 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
         for (int j = 0; j < T; ++j) s[j] = s_in[j];
         blocked_pool<T, kOp, true, K>(s);
       }
+    } else if constexpr (kOp >= kConvFast) {
+      blocked_conv<T, K, kOp == kConvExact>(s, taps);
     } else {
       blocked_pool<T, kOp, false, K>(s);
       if constexpr (kOp == SC_POOL_AVG) {
@@ -259,17 +289,10 @@ int env_int(const char* name, int dflt, int lo, int hi) {
   return (n >= lo && n <= hi) ? n : dflt;
 }
 
-int env_nbuf() {
-  static int v = [] {
-    const char* e = getenv("SC_POOL_NBUF");
-    int n = e ? atoi(e) : 0;
-    return (n == 1 || n == 2 || n == 4) ? n : 2;
-  }();
-  return v;
-}
 
 template <int kOp, int K, int NBUF>
-int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
+int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
+                const float* w) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
@@ -296,28 +319,31 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
   }
   const int tpc = env_int("SC_POOL_TPC", 4, 1, 64);
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
+  Taps1<K> taps{};
+  if (w)
+    for (int i = 0; i < K; ++i) taps.f[i] = w[i];
   pool_tma_kernel<kOp, K, NBUF><<<(unsigned)grid, 32 * (kTmaWarps + 1), smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc);
+      map, y, out_len, tiles_per_row, n_tiles, tpc, taps);
   SC_LAUNCH_CHECK("pool_tma_kernel");
   return SC_OK;
 }
 
 template <int kOp, int K>
-int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
-  switch (env_nbuf()) {
-    case 1: return launch_nbuf<kOp, K, 1>(x, batch, length, y, st);
-    case 4: return launch_nbuf<kOp, K, 4>(x, batch, length, y, st);
-    default: return launch_nbuf<kOp, K, 2>(x, batch, length, y, st);
-  }
+int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
+               const float* w) {
+  // ring depth 2 with 4 contiguous tiles per CTA measured best (tools/pool_sweep.py)
+  return launch_nbuf<kOp, K, 2>(x, batch, length, y, st, w);
 }
 
 template <int kOp, int... Ks>
 int launch_switch(int k, const float* x, int64_t batch, int64_t length, float* y,
-                  cudaStream_t st, std::integer_sequence<int, Ks...>) {
+                  cudaStream_t st, std::integer_sequence<int, Ks...>, const float* w = nullptr) {
   int rc = -1000;
-  ((k == Ks ? (rc = launch_one<kOp, Ks>(x, batch, length, y, st), 0) : 0), ...);
+  ((k == Ks ? (rc = launch_one<kOp, Ks>(x, batch, length, y, st, w), 0) : 0), ...);
   return rc;
 }
+
+using ConvTaps = std::integer_sequence<int, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17>;
 
 using Windows = std::integer_sequence<int, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17,
                                       18, 19, 20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32,
@@ -338,6 +364,19 @@ int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k,
     case SC_POOL_AVG: rc = launch_switch<SC_POOL_AVG>((int)k, x, batch, length, y, st, Windows{}); break;
     default: rc = launch_switch<SC_POOL_MAX>((int)k, x, batch, length, y, st, Windows{}); break;
   }
+  return rc == -1000 ? 1 : rc;
+}
+
+// 1-D convolution of `rows` signals of `length` samples with k taps (HOST
+// pointer w); returns 1 when the TMA path does not apply.
+int conv1d_tma(const float* x, int64_t rows, int64_t length, const float* w, int64_t k,
+               bool exact, float* y, cudaStream_t st) {
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || k < 2 || k > 17 ||
+      length < kTmaWin || length / 32 > 0x7fffffff || rows > 0x7fffffff ||
+      rows * length > (int64_t)1 << 40)
+    return 1;
+  const int rc = exact ? launch_switch<kConvExact>((int)k, x, rows, length, y, st, ConvTaps{}, w)
+                       : launch_switch<kConvFast>((int)k, x, rows, length, y, st, ConvTaps{}, w);
   return rc == -1000 ? 1 : rc;
 }
 
