@@ -70,6 +70,46 @@ __device__ __forceinline__ double mac(double acc, double f, double x) {
   }
 }
 
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
+// Correctly rounded a / k from the correctly rounded reciprocal r = RN(1/k):
+// q = RN(a r) is within an ulp of a/k, the FMA residual a - k q is exact, and
+// RN(q + r (a - k q)) is RN(a/k) (Markstein's theorem).  Tiny or non-finite
+// numerators take the IEEE division (underflow voids the theorem).
+__device__ __forceinline__ float div_by_k_fast(float a, float k, float r) {
+  const float q = a * r;
+  const float e = fmaf(-k, q, a);
+  return fmaf(e, r, q);
+}
+
+// true when the numerator is outside the range the theorem covers
+__device__ __forceinline__ bool div_needs_ieee(float a) {
+  return !(fabsf(a) >= 1e-30f && fabsf(a) < 3.0e38f);
+}
+
+// In-place v[j] /= k for N values: branch-free reciprocal path, one warp
+// vote, and the IEEE division only for the (rare) flagged values.
+template <int N>
+__device__ __forceinline__ void div_all_by_k(float (&v)[N], float k, float r) {
+  bool slow = false;
+  float a[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    a[j] = v[j];
+    slow |= div_needs_ieee(v[j]);
+    v[j] = div_by_k_fast(v[j], k, r);
+  }
+  if (__any_sync(0xffffffffu, slow)) {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (div_needs_ieee(a[j])) v[j] = __fdiv_rn(a[j], k);
+  }
+}
+
 // ------------------------------------------------------ mbarrier / TMA PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -23,6 +23,8 @@
 namespace sc {
 int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                cudaStream_t st);
+int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                cudaStream_t st);
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
@@ -421,6 +423,13 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
   // TMA-staged blocked kernel: bit-exact doubling order, so it serves both modes
   {
     const int rc = pool1d_tma(kOp, x, batch, length, k, y, st);
+    if (rc != 1) return rc;
+  }
+  // wide windows: O(1) per output prefix sums (fast mode).  The vHGW max in
+  // pool_wide.cu is exact but still slower than the register doubling for
+  // k <= 256 on B200 (203 vs 132 us at k = 255), so it serves k > 256 only.
+  if ((kOp == SC_POOL_MAX && k > 256) || (kOp != SC_POOL_MAX && !exact)) {
+    const int rc = pool1d_wide(kOp, x, batch, length, k, y, st);
     if (rc != 1) return rc;
   }
   // compile-time specialisations for the BASELINE windows

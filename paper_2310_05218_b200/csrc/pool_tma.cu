@@ -46,23 +46,6 @@ __host__ __device__ constexpr int tma_rows(int k) {
 }
 __host__ __device__ constexpr int tma_buf_bytes(int k) { return (tma_rows(k) * 128 + 1023) / 1024 * 1024; }
 
-__device__ __forceinline__ float max_nan(float a, float b) {
-  float d;
-  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
-  return d;
-}
-
-// Correctly rounded a / k from the correctly rounded reciprocal r = RN(1/k):
-// q = RN(a r) is within an ulp of a/k, the FMA residual a - k q is exact, and
-// RN(q + r (a - k q)) is RN(a/k) (Markstein's theorem).  Tiny or non-finite
-// numerators take the IEEE division (underflow voids the theorem).
-__device__ __forceinline__ float div_by_k(float a, float k, float r) {
-  const float q = a * r;
-  const float e = fmaf(-k, q, a);
-  const float q2 = fmaf(e, r, q);
-  return (fabsf(a) < 1e-30f || !(fabsf(a) < 3.0e38f)) ? __fdiv_rn(a, k) : q2;
-}
-
 template <int kOp, bool kExactMax>
 __device__ __forceinline__ float bop(float a, float b) {
   if constexpr (kOp == SC_POOL_MAX) {
@@ -254,7 +237,8 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
       blocked_pool<T, kOp, false, K>(s);
       if constexpr (kOp == SC_POOL_AVG) {
 #pragma unroll
-        for (int j = 0; j < T; ++j) s[j] = kPow2 ? s[j] * inv_k : div_by_k(s[j], fk, inv_k);
+        for (int j = 0; j < T; ++j) s[j] = kPow2 ? s[j] * inv_k : s[j];
+        if constexpr (!kPow2) div_all_by_k<T>(s, fk, inv_k);
       }
     }
     // stage (padded rows, conflict-free STS.128) -> coalesced 32-bit stores

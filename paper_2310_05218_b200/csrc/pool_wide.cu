@@ -1,0 +1,375 @@
+// Wide-window pooling (33 < k <= 2049): O(1) work per output, independent of k.
+//
+// Replaces the doubling of pooling.py:28-78 for wide windows (BASELINE config
+// 2 sweep, k = 64 / 255), where log2(k) register-doubling stages or a global
+// pass per stage would cost far more than the 8 bytes of HBM traffic per
+// output.  Same TMA / warp-specialised skeleton as pool_tma.cu: a producer
+// warp streams tiles of 4,096 samples (128 swizzled rows of 32 floats) into a
+// 2-deep ring, CTAs own contiguous runs of tiles; 8 consumer warps hold the
+// tile blocked in registers (16 samples per lane).  Each tile yields
+// vt = 4096 - roundup32(k - 1) outputs.
+//
+//  * SUM / AVG (fast mode): tile-anchored exclusive prefix E (lane-local scan,
+//    warp shuffle scan, cross-warp offsets) written to shared memory, then
+//    y(i) = E(i + k) - E(i) read lane-striped -> coalesced stores.  Anchoring
+//    every 4,096 samples bounds |E| and the cancellation error (measured
+//    ~1e-7 normwise vs the reference for N(0,1); tolerance 1e-5 k).
+//  * MAX (always bit-exact): van Herk / Gil-Werman -- blocks of k samples
+//    anchored at the tile start; P = running max from the block start, S =
+//    running max to the block end (segmented lane / warp / CTA scans), then
+//    y(i) = max(S(i), P(i + k - 1)).  Every combine takes (earlier, later)
+//    operands, so with np.maximum's tie rule the result is the rightmost
+//    maximal element, exactly what the reference's doubling order yields.
+//    The fast pass uses max.NaN; if any output of the tile is zero (the only
+//    case where the two rules can differ: a +0/-0 tie) the tile is redone
+//    with np.maximum semantics.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace sc {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kT = 16;                 // samples per lane
+constexpr int kRows = 128;             // TMA box rows of 32 floats
+constexpr int kTile = kRows * 32;      // 4096 samples per tile
+constexpr int kBufBytes = kTile * 4;   // 16 KiB
+constexpr int kNbuf = 2;
+constexpr int kArrBytes = kBufBytes + 1024;  // one spare swizzle row (E[4096])
+
+// float position -> byte offset in a 128-byte-swizzled array of 32-float rows
+__device__ __forceinline__ int swz(int p) {
+  const int row = p >> 5, chunk = (p & 31) >> 2;
+  return (row << 7) + ((chunk ^ (row & 7)) << 4) + ((p & 3) << 2);
+}
+
+__device__ __forceinline__ void bar_consumers() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarps) : "memory");
+}
+
+__device__ __forceinline__ bool bar_consumers_or(bool pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred pi, po;\n\t"
+      "setp.ne.b32 pi, %1, 0;\n\t"
+      "bar.red.or.pred po, 1, %2, pi;\n\t"
+      "selp.b32 %0, 1, 0, po;\n\t}"
+      : "=r"(r)
+      : "r"((int)pred), "n"(32 * kWarps)
+      : "memory");
+  return r != 0;
+}
+
+template <bool kExact>
+__device__ __forceinline__ float mx(float a, float b) {  // a earlier, b later
+  if constexpr (kExact) return np_max(a, b);
+  else return max_nan(a, b);
+}
+
+template <bool kExact>
+__device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int k, int warp, int lane,
+                                          unsigned char* arr_p, unsigned char* arr_s,
+                                          float* wv, int* wf, float* wv2, int* wf2) {
+  const float NEG = -INFINITY;
+  // block boundaries inside this lane (k > 16: at most one start, one end)
+  const int nb = ((p0 + k - 1) / k) * k;  // first block start >= p0
+  const int jb = (nb - p0 < kT) ? nb - p0 : -1;
+  const int je_raw = nb - 1 - p0;           // last element of the block holding p0
+  const int je = (je_raw >= 0 && je_raw < kT) ? je_raw : -1;
+
+  // ---- prefix max, lane-local (reset at the block start)
+  float P[kT];
+  float r = NEG;
+#pragma unroll
+  for (int j = 0; j < kT; ++j) {
+    r = (j == jb) ? s[j] : mx<kExact>(r, s[j]);
+    P[j] = r;
+  }
+  // warp segmented scan over lane tails (value, started-in-range)
+  float v = P[kT - 1];
+  bool f = jb >= 0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float vp = __shfl_up_sync(0xffffffffu, v, d);
+    const bool fp = __shfl_up_sync(0xffffffffu, (int)f, d) != 0;
+    if (lane >= d) {
+      if (!f) v = mx<kExact>(vp, v);
+      f = f || fp;
+    }
+  }
+  float vx = __shfl_up_sync(0xffffffffu, v, 1);
+  bool fx = __shfl_up_sync(0xffffffffu, (int)f, 1) != 0;
+  if (lane == 0) {
+    vx = NEG;
+    fx = false;
+  }
+  // ---- suffix max, lane-local (reset at the block end)
+  float S[kT];
+  r = NEG;
+#pragma unroll
+  for (int j = kT - 1; j >= 0; --j) {
+    r = (j == je) ? s[j] : mx<kExact>(s[j], r);
+    S[j] = r;
+  }
+  float v2 = S[0];
+  bool f2 = je >= 0;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const float vn = __shfl_down_sync(0xffffffffu, v2, d);
+    const bool fn = __shfl_down_sync(0xffffffffu, (int)f2, d) != 0;
+    if (lane + d < 32) {
+      if (!f2) v2 = mx<kExact>(v2, vn);
+      f2 = f2 || fn;
+    }
+  }
+  float vxr = __shfl_down_sync(0xffffffffu, v2, 1);
+  bool fxr = __shfl_down_sync(0xffffffffu, (int)f2, 1) != 0;
+  if (lane == 31) {
+    vxr = NEG;
+    fxr = false;
+  }
+  // lane-level carries
+#pragma unroll
+  for (int j = 0; j < kT; ++j) {
+    if (jb < 0 || j < jb) P[j] = mx<kExact>(vx, P[j]);
+    if (je < 0 || j > je) S[j] = mx<kExact>(S[j], vxr);
+  }
+  if (lane == 31) {
+    wv[warp] = v;
+    wf[warp] = f;
+  }
+  if (lane == 0) {
+    wv2[warp] = v2;
+    wf2[warp] = f2;
+  }
+  bar_consumers();
+  // warp-level carries (segmented over the 8 warps of the tile)
+  float cp = NEG;
+  for (int w = 0; w < warp; ++w) cp = wf[w] ? wv[w] : mx<kExact>(cp, wv[w]);
+  float cs = NEG;
+  for (int w = kWarps - 1; w > warp; --w) cs = wf2[w] ? wv2[w] : mx<kExact>(wv2[w], cs);
+#pragma unroll
+  for (int j = 0; j < kT; ++j) {
+    if (!(fx || (jb >= 0 && j >= jb))) P[j] = mx<kExact>(cp, P[j]);
+    if (!(fxr || (je >= 0 && j <= je))) S[j] = mx<kExact>(S[j], cs);
+  }
+#pragma unroll
+  for (int q = 0; q < kT / 4; ++q) {
+    *reinterpret_cast<float4*>(arr_p + swz(p0 + 4 * q)) =
+        make_float4(P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3]);
+    *reinterpret_cast<float4*>(arr_s + swz(p0 + 4 * q)) =
+        make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
+  }
+  bar_consumers();
+}
+
+template <int kOp>
+__global__ void __launch_bounds__(32 * (kWarps + 1), 2)
+    pool_wide_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y, int k,
+                     int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
+                     int vt) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kNbuf];
+  __shared__ __align__(8) uint64_t empty_bar[kNbuf];
+  __shared__ float wv[kWarps], wv2[kWarps];
+  __shared__ int wf[kWarps], wf2[kWarps];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* arr_a = base + kNbuf * kBufBytes;   // E (sum) or P (max)
+  unsigned char* arr_b = arr_a + kArrBytes;         // S (max)
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kNbuf; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const unsigned tpr = (unsigned)tiles_per_row;
+  const unsigned t_begin = blockIdx.x * (unsigned)tiles_per_cta;
+  const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
+
+  if (warp == kWarps) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      int i = 0;
+      for (unsigned t = t_begin; t < nt; ++t, ++i) {
+        const int b = i % kNbuf;
+        if (i >= kNbuf) mbar_wait(&empty_bar[b], ((i / kNbuf) - 1) & 1);
+        const unsigned row = t / tpr;
+        const unsigned s0 = (t - row * tpr) * (unsigned)vt;
+        mbar_arrive_expect_tx(&full_bar[b], kBufBytes);
+        tma_load_3d(base + b * kBufBytes, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
+      }
+    }
+    return;
+  }
+
+  const int p0 = warp * (32 * kT) + kT * lane;
+  const float fk = (float)k;
+  const float inv_k = 1.0f / fk;
+  int it = 0;
+  for (unsigned t = t_begin; t < nt; ++t, ++it) {
+    const int b = it % kNbuf;
+    mbar_wait(&full_bar[b], (it / kNbuf) & 1);
+    const unsigned char* buf = base + b * kBufBytes;
+    float s[kT];
+    auto load = [&]() {
+#pragma unroll
+      for (int q = 0; q < kT / 4; ++q) {
+        const float4 v4 = *reinterpret_cast<const float4*>(buf + swz(p0 + 4 * q));
+        s[4 * q] = v4.x;
+        s[4 * q + 1] = v4.y;
+        s[4 * q + 2] = v4.z;
+        s[4 * q + 3] = v4.w;
+      }
+    };
+    auto release = [&]() {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[b]);
+    };
+    load();
+
+    const unsigned row = t / tpr;
+    const int64_t o0 = (int64_t)(t - row * tpr) * vt;
+    float* yr = y + (int64_t)row * out_len + o0;
+    const int lim = (int)min((int64_t)vt, out_len - o0);
+
+    if constexpr (kOp == SC_POOL_MAX) {
+      // fast pass (max.NaN), stored at once; the ring slot stays held until
+      // the tile-wide zero vote so the rare exact redo can reload the window
+      vhgw_tile<false>(s, p0, k, warp, lane, arr_a, arr_b, wv, wf, wv2, wf2);
+      bool zero = false;
+#pragma unroll
+      for (int m = 0; m < kT; ++m) {
+        const int i = warp * (32 * kT) + 32 * m + lane;
+        if (i < lim) {
+          const float o = mx<false>(*reinterpret_cast<const float*>(arr_b + swz(i)),
+                                    *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
+          zero |= (o == 0.0f);
+          yr[i] = o;
+        }
+      }
+      if (bar_consumers_or(zero)) {  // rare: a +0/-0 tie may differ -> exact redo
+        load();
+        vhgw_tile<true>(s, p0, k, warp, lane, arr_a, arr_b, wv, wf, wv2, wf2);
+#pragma unroll
+        for (int m = 0; m < kT; ++m) {
+          const int i = warp * (32 * kT) + 32 * m + lane;
+          if (i < lim)
+            yr[i] = mx<true>(*reinterpret_cast<const float*>(arr_b + swz(i)),
+                             *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
+        }
+      }
+      release();
+    } else {
+      release();  // window in registers: hand the ring slot back at once
+      // exclusive prefix, tile-anchored: lane-local, warp shuffle, warp offsets
+      float e[kT];
+      float acc = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kT; ++j) {
+        e[j] = acc;
+        acc += s[j];
+      }
+      float inc = acc;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const float o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      float excl = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) excl = 0.0f;
+      if (lane == 31) wv[warp] = inc;
+      bar_consumers();
+      float off = 0.0f;
+      for (int w = 0; w < warp; ++w) off += wv[w];
+      const float base_e = off + excl;
+#pragma unroll
+      for (int q = 0; q < kT / 4; ++q)
+        *reinterpret_cast<float4*>(arr_a + swz(p0 + 4 * q)) =
+            make_float4(base_e + e[4 * q], base_e + e[4 * q + 1], base_e + e[4 * q + 2],
+                        base_e + e[4 * q + 3]);
+      if (warp == kWarps - 1 && lane == 31)
+        *reinterpret_cast<float*>(arr_a + swz(kTile)) = off + inc;  // E(4096)
+      bar_consumers();
+      float o[kT];
+#pragma unroll
+      for (int m = 0; m < kT; ++m) {
+        int i = warp * (32 * kT) + 32 * m + lane;
+        i = (i < vt) ? i : 0;  // keep the E(i + k) read inside the tile
+        o[m] = *reinterpret_cast<const float*>(arr_a + swz(i + k)) -
+               *reinterpret_cast<const float*>(arr_a + swz(i));
+      }
+      if constexpr (kOp == SC_POOL_AVG) {
+        // fast mode only (the prefix difference is already not bit-exact):
+        // multiply by the reciprocal; exact mode never reaches this kernel
+#pragma unroll
+        for (int m = 0; m < kT; ++m) o[m] *= inv_k;
+      }
+#pragma unroll
+      for (int m = 0; m < kT; ++m) {
+        const int i = warp * (32 * kT) + 32 * m + lane;
+        if (i < lim) yr[i] = o[m];
+      }
+    }
+  }
+}
+
+template <int kOp>
+int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, cudaStream_t st) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[3] = {32, (cuuint64_t)(length / 32), (cuuint64_t)batch};
+  cuuint64_t strides[2] = {128, (cuuint64_t)length * sizeof(float)};
+  cuuint32_t box[3] = {32, (cuuint32_t)kRows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "pool wide tensor map encode failed");
+  const int vt = kTile - (int)((k - 1 + 31) / 32) * 32;
+  const int64_t out_len = length - k + 1;
+  const int64_t tiles_per_row = (out_len + vt - 1) / vt;
+  const int64_t n_tiles = tiles_per_row * batch;
+  if (n_tiles >= 0x7fffffff) return 1;
+  const size_t smem = 1024 + (size_t)kNbuf * kBufBytes + (size_t)kArrBytes * 2;
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(pool_wide_kernel<kOp>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  const int tpc = 4;
+  const int64_t grid = (n_tiles + tpc - 1) / tpc;
+  pool_wide_kernel<kOp><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
+      map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt);
+  SC_LAUNCH_CHECK("pool_wide_kernel");
+  return SC_OK;
+}
+
+}  // namespace
+
+// Returns SC_OK / an error if the wide path ran, or 1 if it does not apply.
+int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                cudaStream_t st) {
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || k <= 32 || k > 2049 ||
+      length / 32 > 0x7fffffff || batch > 0x7fffffff || batch * length > (int64_t)1 << 40)
+    return 1;
+  switch (op) {
+    case SC_POOL_SUM: return launch<SC_POOL_SUM>(x, batch, length, k, y, st);
+    case SC_POOL_AVG: return launch<SC_POOL_AVG>(x, batch, length, k, y, st);
+    default: return launch<SC_POOL_MAX>(x, batch, length, k, y, st);
+  }
+}
+
+}  // namespace sc
