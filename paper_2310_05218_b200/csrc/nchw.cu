@@ -17,10 +17,13 @@
 // reproduces the composed oracle (per (n, co): sum over ci ascending of the
 // reference's single-channel conv of the padded plane, reference.py:15-23).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace sc {
+int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
+               int64_t cout, float* y, cudaStream_t st);
 namespace {
 
 constexpr int kCoT = 64;       // output channels per CTA
@@ -201,6 +204,15 @@ extern "C" int sc_conv2d_nchw_f32(const float* x, int64_t n, int64_t cin, int64_
   if (!x || !wt || !y) return fail(SC_ERR_ARG, "nchw: null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (mode == SC_MODE_FAST && kh == 3 && kw == 3 && pad == 1) {
+    // tensor cores (tcgen05 3xTF32) when the shape fits; CUDA-core FFMA otherwise
+    static const bool no_tc = [] {
+      const char* e = getenv("SC_NCHW_NO_TC");
+      return e && e[0] == '1';
+    }();
+    if (!no_tc) {
+      const int rc = nchw3x3_tc(x, n, cin, h, w, wt, cout, y, st);
+      if (rc != 1) return rc;
+    }
     const int tiles_w = (int)((w + kTW - 1) / kTW);
     const int tiles_h = (int)((h + kTH - 1) / kTH);
     dim3 grid((unsigned)(tiles_w * tiles_h), (unsigned)((cout + kCoT - 1) / kCoT), (unsigned)n);

@@ -1,0 +1,38 @@
+"""Quick correctness + timing check of the tcgen05 NCHW path vs float64."""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_2310_05218_b200 as sc  # noqa: E402
+from oracle import slideconv_oracle as O  # noqa: E402
+
+rng = np.random.default_rng(4)
+for (n, cin, cout, h, w) in [(1, 32, 64, 8, 16), (1, 64, 64, 16, 32), (2, 64, 64, 112, 112),
+                             (1, 32, 128, 20, 24)]:
+    x = rng.standard_normal((n, cin, h, w), dtype=np.float32)
+    wt = (rng.standard_normal((cout, cin, 3, 3), dtype=np.float32) / np.float32(np.sqrt(9 * cin))).astype(np.float32)
+    t0 = time.time()
+    y = sc.conv2d_nchw(x, wt, 1)
+    torch.cuda.synchronize()
+    ref = O.conv2d_nchw_f64(x, wt, 1)
+    err = O.normwise_error(y, ref)
+    print(f"{(n, cin, cout, h, w)} normwise {err:.3e} tol {O.north_star_tol(3, cin):.1e} "
+          f"maxabs {np.max(np.abs(y - ref)):.3e} ({time.time() - t0:.2f}s)", flush=True)
+
+xd = torch.randn((16, 64, 112, 112), device="cuda")
+wd = torch.randn((64, 64, 3, 3), device="cuda") / 24
+for _ in range(3):
+    sc.conv2d_nchw(xd, wd, 1)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+a.record()
+for _ in range(20):
+    sc.conv2d_nchw(xd, wd, 1)
+b.record()
+b.synchronize()
+t = a.elapsed_time(b) / 20
+print(f"config 4 TC: {t * 1e3:.1f} us  {2 * 16 * 64 * 112 * 112 * 64 * 9 / t / 1e9:.1f} TFLOP/s")
