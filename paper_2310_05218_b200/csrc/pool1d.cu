@@ -425,9 +425,10 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
     const int rc = pool1d_tma(kOp, x, batch, length, k, y, st);
     if (rc != 1) return rc;
   }
-  // wide windows: O(1) per output prefix sums (fast mode).  The vHGW max in
-  // pool_wide.cu is exact but still slower than the register doubling for
-  // k <= 256 on B200 (203 vs 132 us at k = 255), so it serves k > 256 only.
+  // wide windows: O(1) per output -- prefix sums (fast mode) or the exact
+  // block-decomposition max.  For 64 < k <= 256 the striped register
+  // doubling is still the faster exact max on B200 (k = 255: 132 us vs
+  // 232 us, tools/pool_sweep.py), so the block kernel serves k > 256.
   if ((kOp == SC_POOL_MAX && k > 256) || (kOp != SC_POOL_MAX && !exact)) {
     const int rc = pool1d_wide(kOp, x, batch, length, k, y, st);
     if (rc != 1) return rc;

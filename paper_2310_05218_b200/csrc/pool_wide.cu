@@ -72,93 +72,27 @@ __device__ __forceinline__ float mx(float a, float b) {  // a earlier, b later
   else return max_nan(a, b);
 }
 
-template <bool kExact>
-__device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int k, int warp, int lane,
-                                          unsigned char* arr_p, unsigned char* arr_s,
-                                          float* wv, int* wf, float* wv2, int* wf2) {
-  const float NEG = -INFINITY;
-  // block boundaries inside this lane (k > 16: at most one start, one end)
-  const int nb = ((p0 + k - 1) / k) * k;  // first block start >= p0
-  const int jb = (nb - p0 < kT) ? nb - p0 : -1;
-  const int je_raw = nb - 1 - p0;           // last element of the block holding p0
-  const int je = (je_raw >= 0 && je_raw < kT) ? je_raw : -1;
+constexpr int kBlocks = kWarps * 32;   // 16-sample blocks per tile (one per lane)
+constexpr int kLevels = 8;              // sparse-table levels over block maxima
 
-  // ---- prefix max, lane-local (reset at the block start)
-  float P[kT];
-  float r = NEG;
+// Block-decomposition max over a tile (exact order): each lane's 16 samples
+// form a block with lane-local prefix P and suffix S maxima; block maxima get
+// a sparse table L[t][b] = max(blocks b .. b + 2^t - 1).  A window [i, e]
+// (e = i + k - 1, k > 16) is S(i) ++ full blocks ++ P(e), the full blocks
+// covered by two overlapping sparse-table entries.  Every combine is
+// (earlier, later), so ties resolve to the rightmost maximal element like the
+// reference's doubling with np.maximum.
+template <bool kExact>
+__device__ __forceinline__ void blocks_tile(const float (&s)[kT], int p0, int levels, int warp,
+                                            int lane, unsigned char* arr_p, unsigned char* arr_s,
+                                            float* table) {
+  float P[kT], S[kT];
+  P[0] = s[0];
 #pragma unroll
-  for (int j = 0; j < kT; ++j) {
-    r = (j == jb) ? s[j] : mx<kExact>(r, s[j]);
-    P[j] = r;
-  }
-  // warp segmented scan over lane tails (value, started-in-range)
-  float v = P[kT - 1];
-  bool f = jb >= 0;
+  for (int j = 1; j < kT; ++j) P[j] = mx<kExact>(P[j - 1], s[j]);
+  S[kT - 1] = s[kT - 1];
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const float vp = __shfl_up_sync(0xffffffffu, v, d);
-    const bool fp = __shfl_up_sync(0xffffffffu, (int)f, d) != 0;
-    if (lane >= d) {
-      if (!f) v = mx<kExact>(vp, v);
-      f = f || fp;
-    }
-  }
-  float vx = __shfl_up_sync(0xffffffffu, v, 1);
-  bool fx = __shfl_up_sync(0xffffffffu, (int)f, 1) != 0;
-  if (lane == 0) {
-    vx = NEG;
-    fx = false;
-  }
-  // ---- suffix max, lane-local (reset at the block end)
-  float S[kT];
-  r = NEG;
-#pragma unroll
-  for (int j = kT - 1; j >= 0; --j) {
-    r = (j == je) ? s[j] : mx<kExact>(s[j], r);
-    S[j] = r;
-  }
-  float v2 = S[0];
-  bool f2 = je >= 0;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const float vn = __shfl_down_sync(0xffffffffu, v2, d);
-    const bool fn = __shfl_down_sync(0xffffffffu, (int)f2, d) != 0;
-    if (lane + d < 32) {
-      if (!f2) v2 = mx<kExact>(v2, vn);
-      f2 = f2 || fn;
-    }
-  }
-  float vxr = __shfl_down_sync(0xffffffffu, v2, 1);
-  bool fxr = __shfl_down_sync(0xffffffffu, (int)f2, 1) != 0;
-  if (lane == 31) {
-    vxr = NEG;
-    fxr = false;
-  }
-  // lane-level carries
-#pragma unroll
-  for (int j = 0; j < kT; ++j) {
-    if (jb < 0 || j < jb) P[j] = mx<kExact>(vx, P[j]);
-    if (je < 0 || j > je) S[j] = mx<kExact>(S[j], vxr);
-  }
-  if (lane == 31) {
-    wv[warp] = v;
-    wf[warp] = f;
-  }
-  if (lane == 0) {
-    wv2[warp] = v2;
-    wf2[warp] = f2;
-  }
-  bar_consumers();
-  // warp-level carries (segmented over the 8 warps of the tile)
-  float cp = NEG;
-  for (int w = 0; w < warp; ++w) cp = wf[w] ? wv[w] : mx<kExact>(cp, wv[w]);
-  float cs = NEG;
-  for (int w = kWarps - 1; w > warp; --w) cs = wf2[w] ? wv2[w] : mx<kExact>(wv2[w], cs);
-#pragma unroll
-  for (int j = 0; j < kT; ++j) {
-    if (!(fx || (jb >= 0 && j >= jb))) P[j] = mx<kExact>(cp, P[j]);
-    if (!(fxr || (je >= 0 && j <= je))) S[j] = mx<kExact>(S[j], cs);
-  }
+  for (int j = kT - 2; j >= 0; --j) S[j] = mx<kExact>(s[j], S[j + 1]);
 #pragma unroll
   for (int q = 0; q < kT / 4; ++q) {
     *reinterpret_cast<float4*>(arr_p + swz(p0 + 4 * q)) =
@@ -166,7 +100,30 @@ __device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int k, i
     *reinterpret_cast<float4*>(arr_s + swz(p0 + 4 * q)) =
         make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
   }
+  const int blk = warp * 32 + lane;
+  table[blk] = P[kT - 1];
   bar_consumers();
+  for (int t = 1; t < levels; ++t) {
+    const int half = 1 << (t - 1);
+    const float* lo = table + (t - 1) * kBlocks;
+    if (blk + half < kBlocks) table[t * kBlocks + blk] = mx<kExact>(lo[blk], lo[blk + half]);
+    bar_consumers();
+  }
+}
+
+template <bool kExact>
+__device__ __forceinline__ float window_max(int i, int k, const unsigned char* arr_p,
+                                            const unsigned char* arr_s, const float* table) {
+  const int e = i + k - 1;
+  const int b0 = i >> 4, b1 = e >> 4;
+  const int c = b1 - b0 - 1;  // full blocks strictly inside the window
+  float y = *reinterpret_cast<const float*>(arr_s + swz(i));
+  if (c > 0) {
+    const int t = 31 - __clz(c);
+    const float* lt = table + t * kBlocks;
+    y = mx<kExact>(y, mx<kExact>(lt[b0 + 1], lt[b1 - (1 << t)]));
+  }
+  return mx<kExact>(y, *reinterpret_cast<const float*>(arr_p + swz(e)));
 }
 
 template <int kOp>
@@ -177,8 +134,8 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kNbuf];
   __shared__ __align__(8) uint64_t empty_bar[kNbuf];
-  __shared__ float wv[kWarps], wv2[kWarps];
-  __shared__ int wf[kWarps], wf2[kWarps];
+  __shared__ float wv[kWarps];
+  __shared__ float table[kLevels * kBlocks];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* arr_a = base + kNbuf * kBufBytes;   // E (sum) or P (max)
   unsigned char* arr_b = arr_a + kArrBytes;         // S (max)
@@ -214,6 +171,10 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
   }
 
   const int p0 = warp * (32 * kT) + kT * lane;
+  // sparse-table levels needed: the widest run of full blocks is (k+14)/16 - 1
+  int levels = 1;
+  while ((1 << levels) <= (k + 14) / 16) ++levels;
+  levels = min(levels, kLevels);
   const float fk = (float)k;
   const float inv_k = 1.0f / fk;
   int it = 0;
@@ -244,32 +205,29 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
     const int lim = (int)min((int64_t)vt, out_len - o0);
 
     if constexpr (kOp == SC_POOL_MAX) {
-      // fast pass (max.NaN), stored at once; the ring slot stays held until
-      // the tile-wide zero vote so the rare exact redo can reload the window
-      vhgw_tile<false>(s, p0, k, warp, lane, arr_a, arr_b, wv, wf, wv2, wf2);
+      release();  // the window stays in registers for a possible exact redo
+      // fast pass (max.NaN), stored at once; if any output of the tile is zero
+      // (a +0/-0 tie may resolve differently) the tile is redone exactly
+      blocks_tile<false>(s, p0, levels, warp, lane, arr_a, arr_b, table);
       bool zero = false;
 #pragma unroll
       for (int m = 0; m < kT; ++m) {
         const int i = warp * (32 * kT) + 32 * m + lane;
         if (i < lim) {
-          const float o = mx<false>(*reinterpret_cast<const float*>(arr_b + swz(i)),
-                                    *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
+          const float o = window_max<false>(i, k, arr_a, arr_b, table);
           zero |= (o == 0.0f);
           yr[i] = o;
         }
       }
-      if (bar_consumers_or(zero)) {  // rare: a +0/-0 tie may differ -> exact redo
-        load();
-        vhgw_tile<true>(s, p0, k, warp, lane, arr_a, arr_b, wv, wf, wv2, wf2);
+      if (bar_consumers_or(zero)) {
+        blocks_tile<true>(s, p0, levels, warp, lane, arr_a, arr_b, table);
 #pragma unroll
         for (int m = 0; m < kT; ++m) {
           const int i = warp * (32 * kT) + 32 * m + lane;
-          if (i < lim)
-            yr[i] = mx<true>(*reinterpret_cast<const float*>(arr_b + swz(i)),
-                             *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
+          if (i < lim) yr[i] = window_max<true>(i, k, arr_a, arr_b, table);
         }
+        bar_consumers();
       }
-      release();
     } else {
       release();  // window in registers: hand the ring slot back at once
       // exclusive prefix, tile-anchored: lane-local, warp shuffle, warp offsets
