@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
       prefetch_tmap(&tmap);
       for (int s = 0; s < n_stage; ++s) {
         const int slot = s % kStages;
-        if (s >= kStages) mbar_wait(&empty_bar[slot], ((s / kStages) - 1) & 1);
+        if (s >= kStages) mbar_wait_sleep(&empty_bar[slot], ((s / kStages) - 1) & 1);
         mbar_arrive_expect_tx(&full_bar[slot], RS * BW * (uint32_t)sizeof(float));
         tma_load_3d(smem + slot * kStageFloats, &tmap, &full_bar[slot], c0, r0 + s * RS, b);
       }

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
       int i = 0;
       for (unsigned t = t_begin; t < nt; ++t, ++i) {
         const int b = i % NBUF;
-        if (i >= NBUF) mbar_wait(&empty_bar[b], ((i / NBUF) - 1) & 1);
+        if (i >= NBUF) mbar_wait_sleep(&empty_bar[b], ((i / NBUF) - 1) & 1);
         const unsigned row = t / tpr;
         const unsigned s0 = (t - row * tpr) * (unsigned)(kTmaWarps * V);
         mbar_arrive_expect_tx(&full_bar[b], tma_rows(K) * 128);

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
       int i = 0;
       for (unsigned t = t_begin; t < nt; ++t, ++i) {
         const int b = i % kNbuf;
-        if (i >= kNbuf) mbar_wait(&empty_bar[b], ((i / kNbuf) - 1) & 1);
+        if (i >= kNbuf) mbar_wait_sleep(&empty_bar[b], ((i / kNbuf) - 1) & 1);
         const unsigned row = t / tpr;
         const unsigned s0 = (t - row * tpr) * (unsigned)vt;
         mbar_arrive_expect_tx(&full_bar[b], kBufBytes);
