@@ -342,6 +342,52 @@ def per_config(torch, sc, hbm_peak, args, traffic):
     return out
 
 
+def rowband_bench(torch, sc, rank, world, hbm_peak, reps=3):
+    """BASELINE config 5 split into `world` row bands (one per rank) with the
+    6-row NCCL halo exchange of paper_2310_05218_b200.rowband; device time,
+    max over ranks (strong scaling of one 65,536^2 image)."""
+    import torch.distributed as dist
+    H = W = 65536
+    plan = sc.plan_row_bands(H, 7, world)[rank]
+    rows = plan.in_stop - plan.in_start
+    dev = torch.device("cuda", torch.cuda.current_device())
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5000 + rank)
+    band = torch.empty((rows, W), device=dev)
+    for r0 in range(0, rows, 8192):
+        band[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
+    f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
+          / np.float32(7)).astype(np.float32)
+    group = dist.group.WORLD if world > 1 else None
+    for _ in range(2):
+        if world > 1:
+            sc.conv2d_rowband(band, f7, group=group)
+        else:
+            sc.conv2d_reference(band, f7)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        y = sc.conv2d_rowband(band, f7, group=group)[0] if world > 1 else sc.conv2d_reference(band, f7)
+    b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3 / reps
+    if world > 1:
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    del band, y
+    torch.cuda.empty_cache()
+    o = H - 6
+    nb = 4 * (H * W + o * o + 49)
+    fl = 2 * o * o * 49
+    return {"ms": round(t * 1e3, 3), "ranks": world, **roofline(nb, fl, t, hbm_peak * world),
+            "halo_bytes_per_pair": 6 * W * 4, "note": "one 65536^2 image, row bands + NCCL halo"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -426,6 +472,9 @@ def run_ours(args, rank, world, local_rank):
         e2e_sec = float(tt.item())
     e2e_val = world * e2e_steps * 2 * alg_bytes_op / e2e_sec / 1e9
 
+    rb = None
+    if world > 1 and not args.no_extras:
+        rb = rowband_bench(torch, sc, rank, world, hbm_peak)
     if rank != 0:
         return
     dom = max(t_avg, t_max)
@@ -461,6 +510,8 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu_baseline_main()
     if world == 1 and not args.no_extras:
         line["per_config"] = per_config(torch, sc, hbm_peak, args, traffic)
+    if rb is not None:
+        line["rowband_cfg5"] = rb
     print(json.dumps(line), flush=True)
 
 
