@@ -1,33 +1,30 @@
 // Multi-channel NCHW 3x3 / pad 1 convolution on the 5th-generation tensor
 // cores (tcgen05, kind::tf32) with 3xTF32 split precision.
 //
-// BASELINE config 4 (N16 Cin64 Cout64 112x112) has ~144 flop/byte: it is
-// FP32-pipe bound on CUDA cores (ncu: nchw3x3_kernel FMA pipe 55 %, 0.45 ms;
-// cuDNN FP32 0.17 ms), so the contraction moves to the tensor cores as an
-// implicit GEMM per filter tap:
+// BASELINE config 4 (N16 Cin64 Cout64 112x112) has ~144 flop/byte: on the
+// CUDA cores it is FP32-pipe bound (nchw3x3_kernel 0.45 ms; cuDNN FP32
+// 0.17 ms), so the contraction runs as an implicit GEMM per filter tap:
 //     out[p, co] += sum_ci  X[ci, p + (j-1, i-1)] * W[co, ci, j, i]
-// * A = shifted input window, M = 128 output pixels (8 rows x 16 cols), K = 32
-//   channels per k-block, loaded straight from the NCHW tensor by a 4-D TMA
-//   box {16 w, 32 c, 8 h, 1 n} whose (w, h) origin is shifted by the tap:
-//   out-of-bounds rows / columns are zero-filled by TMA = the zero padding.
-//   In shared memory this is an MN-major, 64-byte-swizzled UMMA operand.
-// * B = weights of the tap, N = 64 output channels, K-major 128-byte swizzle,
-//   pre-split on the device into tf32 hi / lo parts ([tap][co][ci]).
-// * 3xTF32: D += A_hi B_hi + A_hi B_lo + A_lo B_hi with A_hi = rna_tf32(A),
-//   A_lo = A - A_hi (split in shared memory by 4 worker warps), fp32
-//   accumulation in TMEM (128 lanes x 64 columns).  Error ~2^-21 per product:
-//   far inside 1e-5 * k * sqrt(Cin) (plain TF32 would not be).
+// * Tile = 128 output pixels (8 rows x 16 cols) x 64 output channels; a
+//   persistent kernel (one CTA per SM) walks the tiles.
+// * A (pixels x 32 channels per k-block): one 4-D TMA box {16 w, 32 c, 10 h}
+//   per channel chunk serves all 9 taps (rows h0-1 .. h0+8; TMA zero-fills
+//   rows outside the image = the zero padding), plus two {4 w} halo boxes for
+//   the columns left / right of the tile.  Split warps read the tap's shifted
+//   window from shared memory, split it into tf32 hi / lo (cvt.rna) and store
+//   both to TMEM (tcgen05.st): the MMAs take A from TMEM (TS form).
+// * B = the tap's weights, pre-split on the device into [B_hi | B_lo]
+//   (N = 128 rows, K-major, 128-byte swizzle), streamed by TMA per k-block.
+// * 3xTF32 product per k-step: D[:, 0:128] += A_hi [B_hi | B_lo] and
+//   D[:, 0:64] += A_lo B_hi; the epilogue adds D[:, c] + D[:, 64 + c].
+//   Error ~2^-21 per product: far inside 1e-5 * k * sqrt(Cin) (plain TF32
+//   would not be).
 // * Warp roles: warp 0 TMA producer, warp 1 TMEM owner + single-thread MMA
-//   issuer, warps 2..5 split workers then the epilogue (tcgen05.ld -> NCHW
-//   stores).  A 4-deep TMA ring (A box + B hi/lo) and a 2-deep split ring
-//   (A hi/lo, K-major) with full / split / split_free / empty mbarriers; the
-//   empty barriers are armed by tcgen05.commit so a slot is refilled as soon
-//   as the MMAs that read it retire.
-// * Measured (B200, config 4): 0.20 ms vs 0.455 ms for the FFMA kernel and
-//   0.17 ms for cuDNN's FP32 algorithm.  The kernel is shared-memory-bandwidth
-//   bound: per k-block TMA writes 32 KB, the split moves 48 KB and the 12
-//   MMAs (N = Cout = 64 is small) read 72 KB of operands (~1.2 k cycles at
-//   128 B/clk vs ~0.6 k cycles of MMA issue).
+//   issuer, warps 2..9 split workers, warps 10..13 epilogue (tcgen05.ld ->
+//   NCHW stores).  TMEM (512 columns) holds two 128-column accumulators, so
+//   the epilogue of one tile overlaps the MMAs of the next, and four A hi/lo
+//   stages.  Every hand-off is an mbarrier; the MMA side releases smem / TMEM
+//   stages with tcgen05.commit.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -43,20 +40,30 @@ namespace {
 
 constexpr int kTileH = 8, kTileW = 16;         // M = 128 pixels
 constexpr int kM = kTileH * kTileW;
-constexpr int kN = 64;                          // output channels per CTA
-constexpr int kNC = 2 * kN;                     // MMA N: [B_hi | B_lo] concatenated
-constexpr int kKB = 32;                         // input channels per k-block
-constexpr int kLoadStages = 3;                  // TMA ring: A box + B hi/lo
-constexpr int kSplitStages = 2;                 // split ring: A hi/lo (K-major)
-constexpr int kABytes = kM * kKB * 4;           // 16 KiB
-constexpr int kBBytes = kNC * kKB * 4;          // 16 KiB: rows 0..63 hi, 64..127 lo
-constexpr int kLoadBytes = kABytes + kBBytes;       // [A box (MN-major SW64)][B_hi ; B_lo]
-// A hi / lo live in TMEM (TS-form MMA): per split stage 32 + 32 columns
-constexpr int kTmemD = 0;                        // D: columns [0, 128)
-constexpr int kTmemA = kNC;                      // A stages: columns [128, 256)
-constexpr int kTmemCols = 256;
-constexpr int kSplitWarps = 8;                  // split workers, then epilogue
-constexpr int kThreads = 64 + 32 * kSplitWarps;
+constexpr int kN = 64;                          // output channels per tile
+constexpr int kNC = 2 * kN;                     // [B_hi | B_lo] rows
+constexpr int kBoxH = kTileH + 2;               // A box rows h0-1 .. h0+8
+constexpr int kHaloW = 4;                       // halo box width (16-byte TMA minimum)
+constexpr int kBHalf = kNC * 32 * 4;            // one 32-channel SW128 B box: 16 KiB
+
+// Per k-block channel count KB (64 when Cin allows, else 32): a k-block is
+// (tap, KB channels); each split hand-off then carries 2 * KB / 8 MMAs.
+template <int KB>
+struct TcCfg {
+  static constexpr int kABoxBytes = kBoxH * kTileW * KB * 4;  // MN-major SW64 box
+  static constexpr int kHaloBytes = kBoxH * kHaloW * KB * 4;  // no swizzle
+  static constexpr int kABytes = kABoxBytes + 2 * kHaloBytes; // [box | left | right]
+  static constexpr int kBBytes = kNC * KB * 4;                // KB/32 SW128 boxes
+  static constexpr int kAStages = KB == 64 ? 2 : 3;
+  static constexpr int kBStages = KB == 64 ? 3 : 6;
+  static constexpr int kSplitStages = 256 / (2 * KB);         // TMEM A hi/lo ring
+  static constexpr size_t kSmem = 1024 + (size_t)kAStages * kABytes + (size_t)kBStages * kBBytes;
+};
+constexpr int kTmemCols = 512;                  // D0 [0,128) D1 [128,256) A [256,512)
+constexpr int kTmemA = 256;
+constexpr int kSplitWarps = 8;
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 32 * (2 + kSplitWarps + kEpiWarps);
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo,
                                               uint32_t layout) {
@@ -69,20 +76,23 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, 
   return d;
 }
 
-// kind::tf32, D f32, A K-major, B K-major, M = 128, N = 128 ([B_hi | B_lo]).  (An MN-major
-// tf32 A operand returned all-zero products on sm_100a in
-// tools/micro/umma_probe.cu, so the split workers transpose A to K-major.)
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (0u << 16) |
-                            ((uint32_t)(kNC >> 3) << 17) | ((uint32_t)(kM >> 4) << 24);
+// kind::tf32 instruction descriptor: D f32, A / B tf32, both K-major, M = 128.
+// (An MN-major tf32 A operand in shared memory returned all-zero products on
+// sm_100a, tools/micro/umma_probe.cu; A comes from TMEM instead.)
+constexpr uint32_t idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(kM >> 4) << 24);
+}
 
 // A from TMEM (lane = output pixel, column = k), B from shared memory
+template <int N>
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
                                             uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(db), "r"(kIdesc), "r"(accumulate)
+      "r"(tmem_a), "l"(db), "n"(idesc(N)), "r"(accumulate)
       : "memory");
 }
 
@@ -133,37 +143,66 @@ __device__ __forceinline__ float tf32_hi(float a) {
   return __uint_as_float(r);
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+struct TileCoord {
+  int n, co0, h0, w0;
+};
+
+// tile t -> (output-channel tile fastest, so co-tiles of one pixel tile run
+// concurrently and share the input in L2; then w, h, image)
+__device__ __forceinline__ TileCoord tile_coord(int t, int co_tiles, int wtiles, int htiles) {
+  TileCoord c;
+  c.co0 = (t % co_tiles) * kN;
+  t /= co_tiles;
+  c.w0 = (t % wtiles) * kTileW;
+  t /= wtiles;
+  c.h0 = (t % htiles) * kTileH;
+  c.n = t / htiles;
+  return c;
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kThreads, 1)
     nchw3x3_tc_kernel(const __grid_constant__ CUtensorMap tmx,
-                      const __grid_constant__ CUtensorMap tmw, const float* __restrict__ x,
-                      float* __restrict__ y, int cin, int h, int w, int cout) {
+                      const __grid_constant__ CUtensorMap tmh,
+                      const __grid_constant__ CUtensorMap tmw, float* __restrict__ y, int cin,
+                      int h, int w, int cout, int ntiles) {
+  using C = TcCfg<KB>;
+  constexpr int kAStages = C::kAStages, kBStages = C::kBStages, kSplitStages = C::kSplitStages;
+  constexpr int kABoxBytes = C::kABoxBytes, kHaloBytes = C::kHaloBytes, kABytes = C::kABytes;
+  constexpr int kBBytes = C::kBBytes;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kLoadStages], empty_bar[kLoadStages];
+  __shared__ __align__(8) uint64_t a_full[kAStages], a_empty[kAStages];
+  __shared__ __align__(8) uint64_t b_full[kBStages], b_empty[kBStages];
   __shared__ __align__(8) uint64_t split_bar[kSplitStages], split_free[kSplitStages];
-  __shared__ __align__(8) uint64_t tmem_full;
+  __shared__ __align__(8) uint64_t d_full[2], d_empty[2];
   __shared__ uint32_t tmem_base_sh;
-  unsigned char* load_ring = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* a_ring = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* b_ring = a_ring + kAStages * kABytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w0 = blockIdx.x * kTileW, h0 = blockIdx.y * kTileH;
-  const int co_tiles = cout / kN;
-  const int n = blockIdx.z / co_tiles, co0 = (blockIdx.z % co_tiles) * kN;
-  const int cchunks = cin / kKB;
-  const int kblocks = 9 * cchunks;
+  const int co_tiles = cout / kN, wtiles = w / kTileW, htiles = (h + kTileH - 1) / kTileH;
+  const int cchunks = cin / KB;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kLoadStages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+    for (int s = 0; s < kAStages; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], kSplitWarps);
+    }
+    for (int s = 0; s < kBStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
     }
     for (int s = 0; s < kSplitStages; ++s) {
       mbar_init(&split_bar[s], kSplitWarps);
       mbar_init(&split_free[s], 1);
     }
-    mbar_init(&tmem_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&d_full[s], 1);
+      mbar_init(&d_empty[s], kEpiWarps);
+    }
     fence_mbar_init();
   }
-  if (warp == 1) {  // TMEM: D (128 lanes x 128 fp32 columns) + two A hi/lo stages
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
                  "n"(kTmemCols)
@@ -179,121 +218,171 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       prefetch_tmap(&tmx);
+      prefetch_tmap(&tmh);
       prefetch_tmap(&tmw);
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % kLoadStages;
-        if (kb >= kLoadStages) mbar_wait(&empty_bar[s], ((kb / kLoadStages) - 1) & 1);
-        const int tap = kb / cchunks, ci0 = (kb % cchunks) * kKB;
-        const int dj = tap / 3 - 1;
-        unsigned char* st = load_ring + s * kLoadBytes;
-        mbar_arrive_expect_tx(&full_bar[s], kLoadBytes);
-        // The innermost TMA coordinate must be 16-byte aligned (measured on
-        // sm_100a: an unaligned or negative w origin is an illegal
-        // instruction), so every tap loads the aligned 16-column block at w0;
-        // the split workers apply the tap's column offset and supply the halo
-        // column.  Rows (dim 2) may start at -1: TMA zero-fills them.
-        tma_load_4d(st, &tmx, &full_bar[s], w0, ci0, h0 + dj, n);
-        tma_load_3d(st + kABytes, &tmw, &full_bar[s], ci0, 2 * co0, tap);
+      int ac = 0, bc = 0;  // ring counters across tiles
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileCoord tc = tile_coord(t, co_tiles, wtiles, htiles);
+        // The innermost TMA coordinate must be 16-byte aligned and in range
+        // (measured on sm_100a: otherwise an illegal instruction), so the box
+        // is the aligned 16 columns at w0 and the halo columns come from
+        // {4 w} boxes at w0-4 / w0+16, skipped at the image edge (the split
+        // workers substitute zeros).  Rows start at h0-1: TMA zero-fills.
+        const bool left = tc.w0 > 0, right = tc.w0 + kTileW < w;
+        const uint32_t abytes = kABoxBytes + (left ? kHaloBytes : 0) + (right ? kHaloBytes : 0);
+        for (int chunk = 0; chunk < cchunks; ++chunk, ++ac) {
+          const int sa = ac % kAStages;
+          if (ac >= kAStages) mbar_wait(&a_empty[sa], ((ac / kAStages) - 1) & 1);
+          unsigned char* ab = a_ring + sa * kABytes;
+          mbar_arrive_expect_tx(&a_full[sa], abytes);
+          tma_load_4d(ab, &tmx, &a_full[sa], tc.w0, chunk * KB, tc.h0 - 1, tc.n);
+          if (left)
+            tma_load_4d(ab + kABoxBytes, &tmh, &a_full[sa], tc.w0 - kHaloW, chunk * KB,
+                        tc.h0 - 1, tc.n);
+          if (right)
+            tma_load_4d(ab + kABoxBytes + kHaloBytes, &tmh, &a_full[sa], tc.w0 + kTileW,
+                        chunk * KB, tc.h0 - 1, tc.n);
+          for (int tap = 0; tap < 9; ++tap, ++bc) {
+            const int sb = bc % kBStages;
+            if (bc >= kBStages) mbar_wait(&b_empty[sb], ((bc / kBStages) - 1) & 1);
+            mbar_arrive_expect_tx(&b_full[sb], kBBytes);
+#pragma unroll
+            for (int j = 0; j < KB / 32; ++j)
+              tma_load_3d(b_ring + sb * kBBytes + j * kBHalf, &tmw, &b_full[sb],
+                          chunk * KB + 32 * j, 2 * tc.co0, tap);
+          }
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int ls = kb % kLoadStages, ss = kb % kSplitStages;
-        mbar_wait(&split_bar[ss], (kb / kSplitStages) & 1);  // implies the TMA landed
+      int kc = 0, it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        if (it >= 2) mbar_wait(&d_empty[acc], ((it >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a_hi = tmem + kTmemA + ss * 64;
-        const uint32_t a_lo = a_hi + 32;
-        // B: K-major SW128 (128-byte rows of 32 channels, SBO = 1 KiB between
-        // 8-row groups); a k-step of 8 tf32 advances the start by 32 B
-        const uint64_t dbc = make_desc(smem_u32(load_ring + ls * kLoadBytes) + kABytes, 16, 1024, 2);
+        const uint32_t d = tmem + acc * kNC;
+        for (int kb = 0; kb < 9 * cchunks; ++kb, ++kc) {
+          const int sb = kc % kBStages, ss = kc % kSplitStages;
+          mbar_wait(&split_bar[ss], (kc / kSplitStages) & 1);
+          mbar_wait(&b_full[sb], (kc / kBStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_hi = tmem + kTmemA + ss * 2 * KB, a_lo = a_hi + KB;
+          // B: K-major SW128 boxes of 32 channels (128-byte rows, SBO = 1 KiB
+          // per 8-row group); a k-step of 8 tf32 advances the start by 32 bytes
+          const uint64_t db = make_desc(smem_u32(b_ring + sb * kBBytes), 16, 1024, 2);
 #pragma unroll
-        for (int ks = 0; ks < kKB / 8; ++ks) {
-          // D[:, 0:64] += A * B_hi, D[:, 64:128] += A * B_lo, A = A_lo then A_hi
-          // (4-term split product; the epilogue adds the two halves)
-          mma_tf32_ts(tmem + kTmemD, a_lo + 8 * ks, dbc + 2 * ks, (kb | ks) ? 1u : 0u);
-          mma_tf32_ts(tmem + kTmemD, a_hi + 8 * ks, dbc + 2 * ks, 1u);
+          for (int ks = 0; ks < KB / 8; ++ks) {
+            const uint64_t dbk = db + (uint64_t)((ks >> 2) * (kBHalf >> 4)) + 2 * (ks & 3);
+            mma_tf32_ts<kNC>(d, a_hi + 8 * ks, dbk, (kb | ks) ? 1u : 0u);
+            mma_tf32_ts<kN>(d, a_lo + 8 * ks, dbk, 1u);  // B_hi rows only
+          }
+          umma_commit(&b_empty[sb]);
+          umma_commit(&split_free[ss]);
         }
-        umma_commit(&empty_bar[ls]);    // A box + B slot free once these retire
-        umma_commit(&split_free[ss]);   // TMEM A stage free
+        umma_commit(&d_full[acc]);
       }
-      umma_commit(&tmem_full);
     }
-  } else {
+  } else if (warp < 2 + kSplitWarps) {
     // ------------------------------------------------ split workers (8 warps)
     // warp -> TMEM lane quarter q = warp % 4 (pixels m = 32q + lane) and half
-    // of the 32 channels of a k-block; each thread splits its pixel's 16
-    // channels into tf32 hi / lo and stores them to TMEM (tcgen05.st)
+    // of the KB channels of a k-block; each thread splits its pixel's KB/2
+    // channels into tf32 hi / lo and stores them to the stage's TMEM columns
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int m = 32 * q + lane;
     const int hh = m / kTileW, e = m % kTileW;
-    const int c_lo = 16 * half;
-    float halo_next[16];
-    auto fetch_halo = [&](int kb2, float (&hv)[16]) {
+    int ac = 0, kc = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int w0 = tile_coord(t, co_tiles, wtiles, htiles).w0;
+      const bool left = w0 > 0, right = w0 + kTileW < w;
+      for (int chunk = 0; chunk < cchunks; ++chunk, ++ac) {
+        const int sa = ac % kAStages;
+        mbar_wait(&a_full[sa], (ac / kAStages) & 1);
+        const unsigned char* ab = a_ring + sa * kABytes;
+        for (int tap = 0; tap < 9; ++tap, ++kc) {
+          const int ss = kc % kSplitStages;
+          const int dj = tap / 3, di = tap % 3 - 1;  // box row hh + dj (row 0 = h0-1)
+          if (kc >= kSplitStages) mbar_wait(&split_free[ss], ((kc / kSplitStages) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 2 * KB;
+          // DI = the tap's column offset: pixel e reads column e + DI
+          auto split = [&](auto di_tag) {
+            constexpr int DI = decltype(di_tag)::value;
+            const int ee = e + DI;
+            const bool edge = ee < 0 || ee >= kTileW;
+            const bool zero = edge && (DI < 0 ? !left : !right);
+            const int eec = edge ? 0 : ee;
+            const int chunk16 = eec >> 2;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) hv[c] = 0.0f;
-      if (kb2 >= kblocks) return;
-      const int tap2 = kb2 / cchunks, c2 = (kb2 % cchunks) * kKB;
-      const int dj2 = tap2 / 3 - 1, di2 = tap2 % 3 - 1;
-      if (!((di2 < 0 && e == 0) || (di2 > 0 && e == kTileW - 1))) return;
-      const int gw = di2 < 0 ? w0 - 1 : w0 + kTileW, gh = h0 + dj2 + hh;
-      if (gw < 0 || gw >= w || gh < 0 || gh >= h) return;
-      const float* src = x + (((int64_t)n * cin + c2 + c_lo) * h + gh) * w + gw;
+            for (int g = 0; g < KB / 32; ++g) {
+              const int c_lo = half * (KB / 2) + 16 * g;
+              const int row = (hh + dj) * KB + c_lo;  // (box row, channel) index
+              // box: 64-byte rows (16 columns), SW64 swizzle of the 16-byte
+              // chunks; halo: 16-byte rows, element 3 (left, column w0-1) or
+              // element 0 (right, column w0+16)
+              const unsigned char* hp =
+                  ab + kABoxBytes + (DI > 0 ? kHaloBytes : 0) + row * 16 + (DI < 0 ? 12 : 0);
+              const unsigned char* bp = ab + row * 64 + ((eec & 3) << 2);
+              uint32_t vh[16], vl[16];
 #pragma unroll
-      for (int c = 0; c < 16; ++c) hv[c] = __ldg(src + (int64_t)c * h * w);
-    };
-    fetch_halo(0, halo_next);
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int ls = kb % kLoadStages, ss = kb % kSplitStages;
-      const int tap = kb / cchunks;
-      const int di = tap % 3 - 1;
-      float halo[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) halo[c] = halo_next[c];
-      fetch_halo(kb + 1, halo_next);
-      mbar_wait(&full_bar[ls], (kb / kLoadStages) & 1);
-      if (kb >= kSplitStages) mbar_wait(&split_free[ss], ((kb / kSplitStages) - 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const unsigned char* box = load_ring + ls * kLoadBytes;  // MN-major SW64
-      const int ee = e + di;
-      const bool edge = ee < 0 || ee >= kTileW;
-      const int eec = edge ? 0 : ee;
-      uint32_t vh[16], vl[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int cc = c_lo + c;
-        // box element (hh, cc, eec): 64-byte row (hh, cc), SW64 chunk swizzle
-        const int off = hh * (kKB * 64) + cc * 64 + ((((eec >> 2) ^ ((cc >> 1) & 3))) << 4) +
-                        ((eec & 3) << 2);
-        const float f = edge ? halo[c] : *reinterpret_cast<const float*>(box + off);
-        const float hv = tf32_hi(f);
-        vh[c] = __float_as_uint(hv);
-        vl[c] = __float_as_uint(f - hv);
+              for (int c = 0; c < 16; ++c) {
+                const int sw = ((c_lo + c) >> 1) & 3;
+                const float* src = reinterpret_cast<const float*>(
+                    edge ? hp + c * 16 : bp + c * 64 + ((chunk16 ^ sw) << 4));
+                const float f = zero ? 0.0f : *src;
+                // hi = f with the 13 mantissa bits tf32 drops cleared (exact
+                // lo = f - hi); the MMA reads both operands as tf32
+                const float hv = __uint_as_float(__float_as_uint(f) & 0xffffe000u);
+                vh[c] = __float_as_uint(hv);
+                vl[c] = __float_as_uint(f - hv);
+              }
+              tmem_st16(ta + c_lo, vh);
+              tmem_st16(ta + KB + c_lo, vl);
+            }
+          };
+          if (di < 0) split(std::integral_constant<int, -1>{});
+          else if (di > 0) split(std::integral_constant<int, 1>{});
+          else split(std::integral_constant<int, 0>{});
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&split_bar[ss]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[sa]);  // this warp's box reads are done
       }
-      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 64 + c_lo;
-      tmem_st16(ta, vh);
-      tmem_st16(ta + 32, vl);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  } else {
+    // ------------------------------------------------ epilogue (4 warps)
+    const int q = warp & 3;
+    const int m = 32 * q + lane;
+    const int hh = m / kTileW, e = m % kTileW;
+    const int64_t plane = (int64_t)h * w;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      const TileCoord tc = tile_coord(t, co_tiles, wtiles, htiles);
+      const int acc = it & 1;
+      mbar_wait_sleep(&d_full[acc], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + acc * kNC;
+      const int oh = tc.h0 + hh, ow = tc.w0 + e;
+      float* yp = y + (((int64_t)tc.n * cout + tc.co0) * h + oh) * w + ow;
+#pragma unroll 1
+      for (int ch0 = 0; ch0 < kN; ch0 += 32) {
+        uint32_t r[32], rl[32];
+        tmem_ld32(taddr + ch0, r);
+        tmem_ld32(taddr + kN + ch0, rl);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (oh < h) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
+        }
+      }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&split_bar[ss]);
-    }
-    // ------------------------------------------------ epilogue
-    mbar_wait(&tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int ch0 = half * 32;
-    uint32_t r[32], rl[32];
-    const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + kTmemD + ch0;
-    tmem_ld32(taddr, r);
-    tmem_ld32(taddr + kN, rl);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int oh = h0 + hh, ow = w0 + e;
-    if (oh < h && ow < w) {
-      float* yp = y + (((int64_t)n * cout + co0 + ch0) * h + oh) * w + ow;
-      const int64_t plane = (int64_t)h * w;
-#pragma unroll
-      for (int c = 0; c < 32; ++c) yp[c * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
+      if (lane == 0) mbar_arrive(&d_empty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -323,60 +412,74 @@ __global__ void split_weights_kernel(const float* __restrict__ w, float* __restr
   }
 }
 
-}  // namespace
-
-// Returns SC_OK / an error if the tensor-core path ran, 1 if it does not apply.
-int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
-               int64_t cout, float* y, cudaStream_t st) {
-  if (cin % kKB != 0 || cout % kN != 0 || w % 16 != 0 || (reinterpret_cast<uintptr_t>(x) & 15) ||
-      nb * (cout / kN) > 65535 || h > 65535 * kTileH || cin * h * w >= ((int64_t)1 << 31))
-    return 1;
+template <int KB>
+int launch_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, int64_t cout,
+              float* y, const float* wsplit, cudaStream_t st) {
+  using C = TcCfg<KB>;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  CUtensorMap mx;
+  // dims (w, c, h, n) -- permuted so channels sit between w and h in the box
+  cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)cin, (cuuint64_t)h, (cuuint64_t)nb};
+  cuuint64_t strides[3] = {(cuuint64_t)(h * w * 4), (cuuint64_t)(w * 4),
+                           (cuuint64_t)(cin * h * w * 4)};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMap mx, mh, mw;
   {
-    // dims (w, c, h, n) -- permuted so channels sit between w and h in the box
-    cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)cin, (cuuint64_t)h, (cuuint64_t)nb};
-    cuuint64_t strides[3] = {(cuuint64_t)(h * w * 4), (cuuint64_t)(w * 4),
-                             (cuuint64_t)(cin * h * w * 4)};
-    cuuint32_t box[4] = {kTileW, kKB, kTileH, 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {kTileW, KB, kBoxH, 1};
     CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: x tensor map failed");
   }
+  {
+    cuuint32_t box[4] = {kHaloW, KB, kBoxH, 1};
+    CUresult r = enc(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: halo tensor map failed");
+  }
+  {
+    cuuint64_t wdims[3] = {(cuuint64_t)cin, (cuuint64_t)(2 * cout), 9};
+    cuuint64_t wstrides[2] = {(cuuint64_t)(cin * 4), (cuuint64_t)(2 * cin * cout * 4)};
+    cuuint32_t box[3] = {32, kNC, 1};
+    CUresult r = enc(&mw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(wsplit), wdims,
+                     wstrides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: weight tensor map failed");
+  }
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(nchw3x3_tc_kernel<KB>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
+    attr = true;
+  }
+  const int64_t ntiles = nb * (cout / kN) * (w / kTileW) * ((h + kTileH - 1) / kTileH);
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sm_count());
+  nchw3x3_tc_kernel<KB><<<grid, kThreads, C::kSmem, st>>>(mx, mh, mw, y, (int)cin, (int)h, (int)w,
+                                                         (int)cout, (int)ntiles);
+  SC_LAUNCH_CHECK("nchw3x3_tc_kernel");
+  return SC_OK;
+}
+
+}  // namespace
+
+// Returns SC_OK / an error if the tensor-core path ran, 1 if it does not apply.
+int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
+               int64_t cout, float* y, cudaStream_t st) {
+  if (cin % 32 != 0 || cout % kN != 0 || w % kTileW != 0 ||
+      (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
+      nb * cout * h * w >= ((int64_t)1 << 31))
+    return 1;
   float* wsplit = nullptr;
   const size_t wbytes = (size_t)9 * 2 * cout * cin * sizeof(float);
   SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wsplit), wbytes, st));
   split_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (9 * cout * cin + 255) / 256), 256, 0,
                          st>>>(wt, wsplit, (int)cin, (int)cout);
   SC_LAUNCH_CHECK("split_weights_kernel");
-  CUtensorMap mw;
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)cin, (cuuint64_t)(2 * cout), 9};
-    cuuint64_t strides[2] = {(cuuint64_t)(cin * 4), (cuuint64_t)(2 * cin * cout * 4)};
-    cuuint32_t box[3] = {kKB, kNC, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&mw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, wsplit, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: weight tensor map failed");
-  }
-  const size_t smem = 1024 + (size_t)kLoadStages * kLoadBytes;
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(nchw3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = true;
-  }
-  dim3 grid((unsigned)((w + kTileW - 1) / kTileW), (unsigned)((h + kTileH - 1) / kTileH),
-            (unsigned)(nb * (cout / kN)));
-  nchw3x3_tc_kernel<<<grid, kThreads, smem, st>>>(mx, mw, x, y, (int)cin, (int)h, (int)w,
-                                                   (int)cout);
-  SC_LAUNCH_CHECK("nchw3x3_tc_kernel");
+  const int rc = cin % 64 == 0 ? launch_tc<64>(x, nb, cin, h, w, cout, y, wsplit, st)
+                               : launch_tc<32>(x, nb, cin, h, w, cout, y, wsplit, st);
   SC_CUDA(cudaFreeAsync(wsplit, st));
-  return SC_OK;
+  return rc;
 }
 
 }  // namespace sc

@@ -11,8 +11,10 @@ import paper_2310_05218_b200 as sc  # noqa: E402
 from oracle import slideconv_oracle as O  # noqa: E402
 
 rng = np.random.default_rng(4)
+for_shapes = not os.environ.get("TC_ONLY_TIME")
 for (n, cin, cout, h, w) in [(1, 32, 64, 8, 16), (1, 64, 64, 16, 32), (2, 64, 64, 112, 112),
-                             (1, 32, 128, 20, 24)]:
+                             (1, 32, 128, 20, 24), (3, 64, 128, 13, 48), (1, 96, 64, 9, 32),
+                             (2, 32, 192, 17, 160)]:
     x = rng.standard_normal((n, cin, h, w), dtype=np.float32)
     wt = (rng.standard_normal((cout, cin, 3, 3), dtype=np.float32) / np.float32(np.sqrt(9 * cin))).astype(np.float32)
     t0 = time.time()
@@ -25,14 +27,17 @@ for (n, cin, cout, h, w) in [(1, 32, 64, 8, 16), (1, 64, 64, 16, 32), (2, 64, 64
 
 xd = torch.randn((16, 64, 112, 112), device="cuda")
 wd = torch.randn((64, 64, 3, 3), device="cuda") / 24
-for _ in range(3):
+for _ in range(30):
     sc.conv2d_nchw(xd, wd, 1)
 torch.cuda.synchronize()
-a, b = torch.cuda.Event(True), torch.cuda.Event(True)
-a.record()
-for _ in range(20):
-    sc.conv2d_nchw(xd, wd, 1)
-b.record()
-b.synchronize()
-t = a.elapsed_time(b) / 20
-print(f"config 4 TC: {t * 1e3:.1f} us  {2 * 16 * 64 * 112 * 112 * 64 * 9 / t / 1e9:.1f} TFLOP/s")
+ts = []
+for rep in range(5):
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record()
+    for _ in range(100):
+        sc.conv2d_nchw(xd, wd, 1)
+    b.record()
+    b.synchronize()
+    ts.append(a.elapsed_time(b) / 100)
+t = sorted(ts)[2]
+print(f"config 4 TC: {t * 1e3:.1f} us (min {min(ts)*1e3:.1f} max {max(ts)*1e3:.1f})  {2 * 16 * 64 * 112 * 112 * 64 * 9 / t / 1e9:.1f} TFLOP/s")
