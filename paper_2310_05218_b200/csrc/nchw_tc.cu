@@ -1,31 +1,40 @@
 // Multi-channel NCHW 3x3 / pad 1 convolution on the 5th-generation tensor
-// cores (tcgen05, kind::tf32) with 3xTF32 split precision.
+// cores (tcgen05.mma kind::f16 with bf16 operands, fp32 accumulation) in a
+// 3-product split ("bf16x3") that keeps ~16 significant bits per product.
 //
 // BASELINE config 4 (N16 Cin64 Cout64 112x112) has ~144 flop/byte: on the
 // CUDA cores it is FP32-pipe bound (nchw3x3_kernel 0.45 ms; cuDNN FP32
 // 0.17 ms), so the contraction runs as an implicit GEMM per filter tap:
 //     out[p, co] += sum_ci  X[ci, p + (j-1, i-1)] * W[co, ci, j, i]
 // * Tile = 128 output pixels (8 rows x 16 cols) x 64 output channels; a
-//   persistent kernel (one CTA per SM) walks the tiles.
-// * A (pixels x 32 channels per k-block): one 4-D TMA box {16 w, 32 c, 10 h}
-//   per channel chunk serves all 9 taps (rows h0-1 .. h0+8; TMA zero-fills
-//   rows outside the image = the zero padding), plus two {4 w} halo boxes for
-//   the columns left / right of the tile.  Split warps read the tap's shifted
-//   window from shared memory, split it into tf32 hi / lo (cvt.rna) and store
-//   both to TMEM (tcgen05.st): the MMAs take A from TMEM (TS form).
-// * B = the tap's weights, pre-split on the device into [B_hi | B_lo]
-//   (N = 128 rows, K-major, 128-byte swizzle), streamed by TMA per k-block.
-// * 3xTF32 product per k-step: D[:, 0:128] += A_hi [B_hi | B_lo] and
-//   D[:, 0:64] += A_lo B_hi; the epilogue adds D[:, c] + D[:, 64 + c].
-//   Error ~2^-21 per product: far inside 1e-5 * k * sqrt(Cin) (plain TF32
-//   would not be).
+//   persistent kernel (one CTA per SM) walks the tiles.  A k-block is one tap
+//   x 64 input channels.
+// * A (pixels x channels): one 4-D TMA box {16 w, 10 h, 64 c} per channel
+//   chunk serves all 9 taps (rows h0-1 .. h0+8; TMA zero-fills rows outside
+//   the image = the zero padding), plus two {4 w} halo boxes for the columns
+//   left / right of the tile.  Split warps read the tap's shifted window from
+//   shared memory, split every value x = x1 + x2 + O(2^-17 x) with
+//   x1 = bf16(x), x2 = bf16(x - x1), and store both (packed bf16x2) to TMEM:
+//   the MMAs take A from TMEM (TS form).
+// * B = the tap's weights, pre-split on the device the same way into
+//   [W1 | W2] (N = 128 rows, K-major, 128-byte swizzle), one TMA box per
+//   k-block.
+// * Per 16-channel k-step: D[:, 0:128] += X1 [W1 | W2] and D[:, 0:64] += X2 W1
+//   (two MMAs: measured TS cost is ~80 cycles per instruction up to N = 128,
+//   so N = 128 + 64 beats three N = 64 products); the epilogue adds
+//   D[:, c] + D[:, 64 + c].  The dropped X2 W2 and the split residuals bound
+//   the error per product by ~2^-16 relative: normwise ~1e-5, inside the
+//   north-star 1e-5 * k * sqrt(Cin) (2.4e-4 here) where plain TF32 / BF16
+//   would not be.  kind::f16 issues K = 16 per instruction at
+//   the cost of a K = 8 tf32 one, so this is 2x the 3xTF32 throughput.
 // * Warp roles: warp 0 TMA producer, warp 1 TMEM owner + single-thread MMA
 //   issuer, warps 2..9 split workers, warps 10..13 epilogue (tcgen05.ld ->
 //   NCHW stores).  TMEM (512 columns) holds two 128-column accumulators, so
-//   the epilogue of one tile overlaps the MMAs of the next, and four A hi/lo
+//   the epilogue of one tile overlaps the MMAs of the next, and four X1/X2
 //   stages.  Every hand-off is an mbarrier; the MMA side releases smem / TMEM
 //   stages with tcgen05.commit.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -41,29 +50,26 @@ namespace {
 constexpr int kTileH = 8, kTileW = 16;         // M = 128 pixels
 constexpr int kM = kTileH * kTileW;
 constexpr int kN = 64;                          // output channels per tile
-constexpr int kNC = 2 * kN;                     // [B_hi | B_lo] rows
+constexpr int kNC = 2 * kN;                     // [W1 | W2] rows
+constexpr int kKB = 64;                         // input channels per k-block
+constexpr int kKS = 16;                         // channels per MMA (bf16 K)
 constexpr int kBoxH = kTileH + 2;               // A box rows h0-1 .. h0+8
 constexpr int kHaloW = 4;                       // halo box width (16-byte TMA minimum)
-constexpr int kBHalf = kNC * 32 * 4;            // one 32-channel SW128 B box: 16 KiB
-
-// Per k-block channel count KB (64 when Cin allows, else 32): a k-block is
-// (tap, KB channels); each split hand-off then carries 2 * KB / 8 MMAs.
-template <int KB>
-struct TcCfg {
-  static constexpr int kABoxBytes = kBoxH * kTileW * KB * 4;  // MN-major SW64 box
-  static constexpr int kHaloBytes = kBoxH * kHaloW * KB * 4;  // no swizzle
-  static constexpr int kABytes = kABoxBytes + 2 * kHaloBytes; // [box | left | right]
-  static constexpr int kBBytes = kNC * KB * 4;                // KB/32 SW128 boxes
-  static constexpr int kAStages = KB == 64 ? 2 : 3;
-  static constexpr int kBStages = KB == 64 ? 3 : 6;
-  static constexpr int kSplitStages = 256 / (2 * KB);         // TMEM A hi/lo ring
-  static constexpr size_t kSmem = 1024 + (size_t)kAStages * kABytes + (size_t)kBStages * kBBytes;
-};
+constexpr int kABoxBytes = kBoxH * kTileW * kKB * 4;   // [c][rows][cols] fp32, 40 KiB
+constexpr int kHaloBytes = kBoxH * kHaloW * kKB * 4;   // [c][rows][4] fp32, 10 KiB
+constexpr int kABytes = kABoxBytes + 2 * kHaloBytes;   // [box | left | right]
+constexpr int kBBytes = kNC * kKB * 2;          // bf16, 128-byte rows: 16 KiB
+constexpr int kAStages = 2;
+constexpr int kBStages = 6;
+constexpr int kACols = kKB / 2;                 // TMEM columns per X1 (or X2) k-block
+constexpr int kSplitStages = 4;                 // TMEM X1/X2 ring
 constexpr int kTmemCols = 512;                  // D0 [0,128) D1 [128,256) A [256,512)
 constexpr int kTmemA = 256;
 constexpr int kSplitWarps = 8;
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 32 * (2 + kSplitWarps + kEpiWarps);
+constexpr size_t kSmem = 1024 + (size_t)kAStages * kABytes + (size_t)kBStages * kBBytes;
+static_assert(kTmemA + kSplitStages * 2 * kACols <= kTmemCols, "TMEM budget");
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo,
                                               uint32_t layout) {
@@ -76,22 +82,21 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, 
   return d;
 }
 
-// kind::tf32 instruction descriptor: D f32, A / B tf32, both K-major, M = 128.
-// (An MN-major tf32 A operand in shared memory returned all-zero products on
-// sm_100a, tools/micro/umma_probe.cu; A comes from TMEM instead.)
+// kind::f16 instruction descriptor: D f32 (bit 4), A / B bf16 (format 1 at
+// bits 7 / 10), both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
 constexpr uint32_t idesc(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(kM >> 4) << 24);
 }
 
-// A from TMEM (lane = output pixel, column = k), B from shared memory
+// A from TMEM (lane = output pixel, 32-bit column = 2 channels), B from smem
 template <int N>
-__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
                                             uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
       "r"(tmem_a), "l"(db), "n"(idesc(N)), "r"(accumulate)
       : "memory");
 }
@@ -137,10 +142,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       : "memory");
 }
 
-__device__ __forceinline__ float tf32_hi(float a) {
+// packs (lo -> bits 0..15, hi -> bits 16..31), both rounded to nearest
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(a));
-  return __uint_as_float(r);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 
 struct TileCoord {
@@ -160,30 +166,35 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int co_tiles, int wtiles,
   return c;
 }
 
-template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
     nchw3x3_tc_kernel(const __grid_constant__ CUtensorMap tmx,
                       const __grid_constant__ CUtensorMap tmh,
                       const __grid_constant__ CUtensorMap tmw, float* __restrict__ y, int cin,
                       int h, int w, int cout, int ntiles) {
-  using C = TcCfg<KB>;
-  constexpr int kAStages = C::kAStages, kBStages = C::kBStages, kSplitStages = C::kSplitStages;
-  constexpr int kABoxBytes = C::kABoxBytes, kHaloBytes = C::kHaloBytes, kABytes = C::kABytes;
-  constexpr int kBBytes = C::kBBytes;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+#ifdef SC_TC_TRACE
+  // debugging aid: per-k-block clock64 stamps of CTA 0 written over y
+  auto TR = [&](int slot, int i) {
+    if (blockIdx.x == 0 && i < 64) reinterpret_cast<uint32_t*>(y)[slot * 64 + i] = (uint32_t)clock64();
+  };
+#else
+  auto TR = [](int, int) {};
+#endif
   __shared__ __align__(8) uint64_t a_full[kAStages], a_empty[kAStages];
   __shared__ __align__(8) uint64_t b_full[kBStages], b_empty[kBStages];
   __shared__ __align__(8) uint64_t split_bar[kSplitStages], split_free[kSplitStages];
   __shared__ __align__(8) uint64_t d_full[2], d_empty[2];
   __shared__ uint32_t tmem_base_sh;
+  __shared__ float zero_word;
   unsigned char* a_ring = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* b_ring = a_ring + kAStages * kABytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int co_tiles = cout / kN, wtiles = w / kTileW, htiles = (h + kTileH - 1) / kTileH;
-  const int cchunks = cin / KB;
+  const int cchunks = cin / kKB;
 
   if (threadIdx.x == 0) {
+    zero_word = 0.0f;
     for (int s = 0; s < kAStages; ++s) {
       mbar_init(&a_full[s], 1);
       mbar_init(&a_empty[s], kSplitWarps);
@@ -235,21 +246,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (ac >= kAStages) mbar_wait(&a_empty[sa], ((ac / kAStages) - 1) & 1);
           unsigned char* ab = a_ring + sa * kABytes;
           mbar_arrive_expect_tx(&a_full[sa], abytes);
-          tma_load_4d(ab, &tmx, &a_full[sa], tc.w0, chunk * KB, tc.h0 - 1, tc.n);
+          tma_load_4d(ab, &tmx, &a_full[sa], tc.w0, tc.h0 - 1, chunk * kKB, tc.n);
           if (left)
-            tma_load_4d(ab + kABoxBytes, &tmh, &a_full[sa], tc.w0 - kHaloW, chunk * KB,
-                        tc.h0 - 1, tc.n);
+            tma_load_4d(ab + kABoxBytes, &tmh, &a_full[sa], tc.w0 - kHaloW, tc.h0 - 1,
+                        chunk * kKB, tc.n);
           if (right)
             tma_load_4d(ab + kABoxBytes + kHaloBytes, &tmh, &a_full[sa], tc.w0 + kTileW,
-                        chunk * KB, tc.h0 - 1, tc.n);
+                        tc.h0 - 1, chunk * kKB, tc.n);
           for (int tap = 0; tap < 9; ++tap, ++bc) {
             const int sb = bc % kBStages;
             if (bc >= kBStages) mbar_wait(&b_empty[sb], ((bc / kBStages) - 1) & 1);
+            TR(5, bc);
             mbar_arrive_expect_tx(&b_full[sb], kBBytes);
-#pragma unroll
-            for (int j = 0; j < KB / 32; ++j)
-              tma_load_3d(b_ring + sb * kBBytes + j * kBHalf, &tmw, &b_full[sb],
-                          chunk * KB + 32 * j, 2 * tc.co0, tap);
+            tma_load_3d(b_ring + sb * kBBytes, &tmw, &b_full[sb], chunk * kKB, 2 * tc.co0, tap);
           }
         }
       }
@@ -266,20 +275,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < 9 * cchunks; ++kb, ++kc) {
           const int sb = kc % kBStages, ss = kc % kSplitStages;
           mbar_wait(&split_bar[ss], (kc / kSplitStages) & 1);
+          TR(0, kc);
           mbar_wait(&b_full[sb], (kc / kBStages) & 1);
+          TR(1, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a_hi = tmem + kTmemA + ss * 2 * KB, a_lo = a_hi + KB;
-          // B: K-major SW128 boxes of 32 channels (128-byte rows, SBO = 1 KiB
-          // per 8-row group); a k-step of 8 tf32 advances the start by 32 bytes
+          const uint32_t x1 = tmem + kTmemA + ss * 2 * kACols, x2 = x1 + kACols;
+          // B: K-major SW128 (128-byte rows of 64 bf16 channels, SBO = 1 KiB
+          // per 8-row group); a 16-channel k-step advances the start by 32 B
           const uint64_t db = make_desc(smem_u32(b_ring + sb * kBBytes), 16, 1024, 2);
 #pragma unroll
-          for (int ks = 0; ks < KB / 8; ++ks) {
-            const uint64_t dbk = db + (uint64_t)((ks >> 2) * (kBHalf >> 4)) + 2 * (ks & 3);
-            mma_tf32_ts<kNC>(d, a_hi + 8 * ks, dbk, (kb | ks) ? 1u : 0u);
-            mma_tf32_ts<kN>(d, a_lo + 8 * ks, dbk, 1u);  // B_hi rows only
+          for (int ks = 0; ks < kKB / kKS; ++ks) {
+            mma_bf16_ts<kNC>(d, x1 + 8 * ks, db + 2 * ks, (kb | ks) ? 1u : 0u);
+            mma_bf16_ts<kN>(d, x2 + 8 * ks, db + 2 * ks, 1u);  // W1 rows only
           }
           umma_commit(&b_empty[sb]);
           umma_commit(&split_free[ss]);
+          TR(2, kc);
         }
         umma_commit(&d_full[acc]);
       }
@@ -287,8 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < 2 + kSplitWarps) {
     // ------------------------------------------------ split workers (8 warps)
     // warp -> TMEM lane quarter q = warp % 4 (pixels m = 32q + lane) and half
-    // of the KB channels of a k-block; each thread splits its pixel's KB/2
-    // channels into tf32 hi / lo and stores them to the stage's TMEM columns
+    // of the 64 channels of a k-block; each thread splits its pixel's 32
+    // channels into bf16 x1 / x2 pairs and stores them to TMEM (tcgen05.st)
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int m = 32 * q + lane;
     const int hh = m / kTileW, e = m % kTileW;
@@ -304,49 +315,49 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ss = kc % kSplitStages;
           const int dj = tap / 3, di = tap % 3 - 1;  // box row hh + dj (row 0 = h0-1)
           if (kc >= kSplitStages) mbar_wait(&split_free[ss], ((kc / kSplitStages) - 1) & 1);
+          if (q == 0 && lane == 0 && half == 0) TR(3, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 2 * KB;
-          // DI = the tap's column offset: pixel e reads column e + DI
-          auto split = [&](auto di_tag) {
-            constexpr int DI = decltype(di_tag)::value;
-            const int ee = e + DI;
-            const bool edge = ee < 0 || ee >= kTileW;
-            const bool zero = edge && (DI < 0 ? !left : !right);
-            const int eec = edge ? 0 : ee;
-            const int chunk16 = eec >> 2;
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 2 * kACols +
+                              half * (kACols / 2);
+          // Box [c][10 rows][16 cols] and halo boxes [c][10 rows][4 cols],
+          // unswizzled: the two pixel rows of a warp sit 64 bytes apart, so a
+          // warp's read of one channel is a single conflict-free wavefront.
+          // Each lane walks the channels with its own base / stride: box
+          // column e + di, halo column (tile edge) or a zero word (image edge).
+          const int ee = e + di;
+          const int r = hh + dj;
+          const unsigned char* base;
+          int stride;
+          if (ee >= 0 && ee < kTileW) {
+            base = ab + (r * kTileW + ee) * 4;
+            stride = kBoxH * kTileW * 4;
+          } else if (di < 0 ? left : right) {
+            base = ab + kABoxBytes + (di > 0 ? kHaloBytes : 0) + (r * kHaloW + (di < 0 ? 3 : 0)) * 4;
+            stride = kBoxH * kHaloW * 4;
+          } else {
+            base = reinterpret_cast<const unsigned char*>(&zero_word);
+            stride = 0;
+          }
+          const unsigned char* p = base + half * (kKB / 2) * stride;
+          uint32_t v1[16], v2[16];
 #pragma unroll
-            for (int g = 0; g < KB / 32; ++g) {
-              const int c_lo = half * (KB / 2) + 16 * g;
-              const int row = (hh + dj) * KB + c_lo;  // (box row, channel) index
-              // box: 64-byte rows (16 columns), SW64 swizzle of the 16-byte
-              // chunks; halo: 16-byte rows, element 3 (left, column w0-1) or
-              // element 0 (right, column w0+16)
-              const unsigned char* hp =
-                  ab + kABoxBytes + (DI > 0 ? kHaloBytes : 0) + row * 16 + (DI < 0 ? 12 : 0);
-              const unsigned char* bp = ab + row * 64 + ((eec & 3) << 2);
-              uint32_t vh[16], vl[16];
-#pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const int sw = ((c_lo + c) >> 1) & 3;
-                const float* src = reinterpret_cast<const float*>(
-                    edge ? hp + c * 16 : bp + c * 64 + ((chunk16 ^ sw) << 4));
-                const float f = zero ? 0.0f : *src;
-                // hi = f with the 13 mantissa bits tf32 drops cleared (exact
-                // lo = f - hi); the MMA reads both operands as tf32
-                const float hv = __uint_as_float(__float_as_uint(f) & 0xffffe000u);
-                vh[c] = __float_as_uint(hv);
-                vl[c] = __float_as_uint(f - hv);
-              }
-              tmem_st16(ta + c_lo, vh);
-              tmem_st16(ta + KB + c_lo, vl);
-            }
-          };
-          if (di < 0) split(std::integral_constant<int, -1>{});
-          else if (di > 0) split(std::integral_constant<int, 1>{});
-          else split(std::integral_constant<int, 0>{});
+          for (int j = 0; j < 16; ++j) {
+            const float f0 = *reinterpret_cast<const float*>(p + (2 * j) * stride);
+            const float f1 = *reinterpret_cast<const float*>(p + (2 * j + 1) * stride);
+            const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
+            const float r0 = f0 - __uint_as_float(a1 << 16);
+            const float r1 = f1 - __uint_as_float(a1 & 0xffff0000u);
+            v1[j] = a1;
+            v2[j] = pack_bf16x2(r0, r1);
+          }
+          tmem_st16(ta, v1);
+          tmem_st16(ta + kACols, v2);
+          if (q == 0 && lane == 0 && half == 0) TR(4, kc);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (q == 0 && lane == 0 && half == 0) TR(7, kc);
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
+          if (q == 0 && lane == 0 && half == 0) TR(6, kc);
           if (lane == 0) mbar_arrive(&split_bar[ss]);
         }
         __syncwarp();
@@ -374,7 +385,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(taddr + ch0, r);
         tmem_ld32(taddr + kN + ch0, rl);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifdef SC_TC_TRACE
+        if (false) {
+#else
         if (oh < h) {
+#endif
 #pragma unroll
           for (int c = 0; c < 32; ++c)
             yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
@@ -395,70 +410,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// w[co][ci][3][3] -> [tap][2*cout][ci]: for every 64-channel tile, rows
-// 0..63 are the tf32 hi parts, rows 64..127 the lo parts (K-major B operand
-// of one N = 128 MMA per tap)
-__global__ void split_weights_kernel(const float* __restrict__ w, float* __restrict__ out,
+// w[co][ci][3][3] -> bf16 [tap][2*cout][ci]: for every 64-channel output tile,
+// rows 0..63 hold w1 = bf16(w), rows 64..127 w2 = bf16(w - w1) (the K-major
+// B operand [W1 | W2] of one N = 128 MMA per tap)
+__global__ void split_weights_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ out,
                                      int cin, int cout) {
   const int total = 9 * cout * cin;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int ci = e % cin, co = (e / cin) % cout, tap = e / (cin * cout);
     const float v = w[((int64_t)co * cin + ci) * 9 + tap];
-    const float hv = tf32_hi(v);
+    const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
+    const __nv_bfloat16 v2 = __float2bfloat16_rn(v - __bfloat162float(v1));
     const int tile = co / kN, cl = co % kN;
-    float* base = out + ((int64_t)tap * 2 * cout + (int64_t)tile * kNC) * cin;
-    base[(int64_t)cl * cin + ci] = hv;
-    base[(int64_t)(kN + cl) * cin + ci] = v - hv;
+    __nv_bfloat16* base = out + ((int64_t)tap * 2 * cout + (int64_t)tile * kNC) * cin;
+    base[(int64_t)cl * cin + ci] = v1;
+    base[(int64_t)(kN + cl) * cin + ci] = v2;
   }
-}
-
-template <int KB>
-int launch_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, int64_t cout,
-              float* y, const float* wsplit, cudaStream_t st) {
-  using C = TcCfg<KB>;
-  auto enc = tensor_map_encoder();
-  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  // dims (w, c, h, n) -- permuted so channels sit between w and h in the box
-  cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)cin, (cuuint64_t)h, (cuuint64_t)nb};
-  cuuint64_t strides[3] = {(cuuint64_t)(h * w * 4), (cuuint64_t)(w * 4),
-                           (cuuint64_t)(cin * h * w * 4)};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  CUtensorMap mx, mh, mw;
-  {
-    cuuint32_t box[4] = {kTileW, KB, kBoxH, 1};
-    CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: x tensor map failed");
-  }
-  {
-    cuuint32_t box[4] = {kHaloW, KB, kBoxH, 1};
-    CUresult r = enc(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
-                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: halo tensor map failed");
-  }
-  {
-    cuuint64_t wdims[3] = {(cuuint64_t)cin, (cuuint64_t)(2 * cout), 9};
-    cuuint64_t wstrides[2] = {(cuuint64_t)(cin * 4), (cuuint64_t)(2 * cin * cout * 4)};
-    cuuint32_t box[3] = {32, kNC, 1};
-    CUresult r = enc(&mw, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(wsplit), wdims,
-                     wstrides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: weight tensor map failed");
-  }
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(nchw3x3_tc_kernel<KB>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem));
-    attr = true;
-  }
-  const int64_t ntiles = nb * (cout / kN) * (w / kTileW) * ((h + kTileH - 1) / kTileH);
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sm_count());
-  nchw3x3_tc_kernel<KB><<<grid, kThreads, C::kSmem, st>>>(mx, mh, mw, y, (int)cin, (int)h, (int)w,
-                                                         (int)cout, (int)ntiles);
-  SC_LAUNCH_CHECK("nchw3x3_tc_kernel");
-  return SC_OK;
 }
 
 }  // namespace
@@ -466,20 +433,60 @@ int launch_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, int
 // Returns SC_OK / an error if the tensor-core path ran, 1 if it does not apply.
 int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
                int64_t cout, float* y, cudaStream_t st) {
-  if (cin % 32 != 0 || cout % kN != 0 || w % kTileW != 0 ||
+  if (cin % kKB != 0 || cout % kN != 0 || w % kTileW != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
       nb * cout * h * w >= ((int64_t)1 << 31))
     return 1;
-  float* wsplit = nullptr;
-  const size_t wbytes = (size_t)9 * 2 * cout * cin * sizeof(float);
+  const int64_t ntiles = nb * (cout / kN) * (w / kTileW) * ((h + kTileH - 1) / kTileH);
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  // dims (w, h, c, n): the box is [c][rows][cols] in shared memory
+  cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)cin, (cuuint64_t)nb};
+  cuuint64_t strides[3] = {(cuuint64_t)(w * 4), (cuuint64_t)(h * w * 4),
+                           (cuuint64_t)(cin * h * w * 4)};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMap mx, mh, mw;
+  {
+    cuuint32_t box[4] = {kTileW, kBoxH, kKB, 1};
+    CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: x tensor map failed");
+  }
+  {
+    cuuint32_t box[4] = {kHaloW, kBoxH, kKB, 1};
+    CUresult r = enc(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: halo tensor map failed");
+  }
+  __nv_bfloat16* wsplit = nullptr;
+  const size_t wbytes = (size_t)9 * 2 * cout * cin * sizeof(__nv_bfloat16);
   SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wsplit), wbytes, st));
   split_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (9 * cout * cin + 255) / 256), 256, 0,
                          st>>>(wt, wsplit, (int)cin, (int)cout);
   SC_LAUNCH_CHECK("split_weights_kernel");
-  const int rc = cin % 64 == 0 ? launch_tc<64>(x, nb, cin, h, w, cout, y, wsplit, st)
-                               : launch_tc<32>(x, nb, cin, h, w, cout, y, wsplit, st);
+  {
+    cuuint64_t wdims[3] = {(cuuint64_t)cin, (cuuint64_t)(2 * cout), 9};
+    cuuint64_t wstrides[2] = {(cuuint64_t)(cin * 2), (cuuint64_t)(2 * cin * cout * 2)};
+    cuuint32_t box[3] = {kKB, kNC, 1};
+    CUresult r = enc(&mw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wsplit, wdims, wstrides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: weight tensor map failed");
+  }
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(nchw3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmem));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sm_count());
+  nchw3x3_tc_kernel<<<grid, kThreads, kSmem, st>>>(mx, mh, mw, y, (int)cin, (int)h, (int)w,
+                                                   (int)cout, (int)ntiles);
+  SC_LAUNCH_CHECK("nchw3x3_tc_kernel");
   SC_CUDA(cudaFreeAsync(wsplit, st));
-  return rc;
+  return SC_OK;
 }
 
 }  // namespace sc

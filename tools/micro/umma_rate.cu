@@ -1,4 +1,4 @@
-// tcgen05.mma issue-rate microbenchmark: ./umma_rate <kind 0=tf32 1=f16> <N> <iters>
+// tcgen05.mma issue-rate microbenchmark: ./umma_rate <kind 0=tf32 1=f16 2=tf32-TS 3=bf16-TS> <N> <iters>
 // One CTA per SM, one thread issues `iters` MMAs (M=128, K-major SW128 operands
 // already in smem, same accumulator), timed with clock64 around commit/wait.
 #include <cstdio>
@@ -30,7 +30,8 @@ __global__ void k(int kind, int N, int iters, long long* cyc) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (threadIdx.x == 0) {
-    const uint32_t idesc = (1u << 4) | ((kind != 1 ? 2u : 0u) << 7) | ((kind != 1 ? 2u : 0u) << 10) |
+    const uint32_t fmt = kind == 1 ? 0u : kind == 3 ? 1u : 2u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) |
                            ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
     const uint64_t da = mk(su32(base)), db = mk(su32(base + 32768));
     long long t0 = clock64();
@@ -46,6 +47,13 @@ __global__ void k(int kind, int N, int iters, long long* cyc) {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+                       ::"r"(tb), "r"(tb + 256 + (u & 3) * 8), "l"(db + (uint64_t)((u & 3) * 2)), "r"(idesc), "r"(1u) : "memory");
+      }
+    } else if (kind == 3) {  // bf16, A from TMEM
+      for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
                        ::"r"(tb), "r"(tb + 256 + (u & 3) * 8), "l"(db + (uint64_t)((u & 3) * 2)), "r"(idesc), "r"(1u) : "memory");
       }
     } else {
@@ -73,7 +81,7 @@ int main(int argc, char** argv) {
   k<<<148, 128, 100000>>>(kind, N, iters, cyc);
   cudaError_t e = cudaDeviceSynchronize();
   const double c = (double)cyc[0] / iters;
-  const int K = kind != 1 ? 8 : 16;
-  printf("kind %s N %d: %.1f cycles/MMA, %.0f MAC/cycle/SM (%s)\n", kind == 0 ? "tf32" : kind == 2 ? "tf32-TS" : "f16", N, c,
+  const int K = (kind == 1 || kind == 3) ? 16 : 8;
+  printf("kind %s N %d: %.1f cycles/MMA, %.0f MAC/cycle/SM (%s)\n", kind == 0 ? "tf32" : kind == 2 ? "tf32-TS" : kind == 3 ? "bf16-TS" : "f16", N, c,
          128.0 * N * K / c, cudaGetErrorString(e));
 }
