@@ -59,17 +59,19 @@ constexpr int kABoxBytes = kBoxH * kTileW * kKB * 4;   // [c][rows][cols] fp32, 
 constexpr int kHaloBytes = kBoxH * kHaloW * kKB * 4;   // [c][rows][4] fp32, 10 KiB
 constexpr int kABytes = kABoxBytes + 2 * kHaloBytes;   // [box | left | right]
 constexpr int kBBytes = kNC * kKB * 2;          // bf16, 128-byte rows: 16 KiB
-constexpr int kAStages = 2;
-constexpr int kBStages = 6;
+constexpr int kAStages = 2;                     // A box ring (one per channel chunk)
+constexpr int kStages = 4;                      // k-block ring: B slot + TMEM X1/X2 stage
 constexpr int kACols = kKB / 2;                 // TMEM columns per X1 (or X2) k-block
-constexpr int kSplitStages = 4;                 // TMEM X1/X2 ring
 constexpr int kTmemCols = 512;                  // D0 [0,128) D1 [128,256) A [256,512)
 constexpr int kTmemA = 256;
-constexpr int kSplitWarps = 8;
+constexpr int kSplitWarps = 8;                 // 2 per TMEM lane quarter
+constexpr int kSplitParts = kSplitWarps / 4;    // channel slices of a k-block
+constexpr int kPairs = kKB / kSplitParts / 2;   // packed bf16x2 columns per thread
 constexpr int kEpiWarps = 4;
-constexpr int kThreads = 32 * (2 + kSplitWarps + kEpiWarps);
-constexpr size_t kSmem = 1024 + (size_t)kAStages * kABytes + (size_t)kBStages * kBBytes;
-static_assert(kTmemA + kSplitStages * 2 * kACols <= kTmemCols, "TMEM budget");
+constexpr int kIssuer2 = 2 + kSplitWarps + kEpiWarps;   // warp of the second MMA issuer
+constexpr int kThreads = 32 * (kIssuer2 + 1);
+constexpr size_t kSmem = 1024 + (size_t)kAStages * kABytes + (size_t)kStages * kBBytes;
+static_assert(kTmemA + kStages * 2 * kACols <= kTmemCols, "TMEM budget");
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo,
                                               uint32_t layout) {
@@ -142,6 +144,37 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+                   taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 // packs (lo -> bits 0..15, hi -> bits 16..31), both rounded to nearest
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
@@ -175,14 +208,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef SC_TC_TRACE
   // debugging aid: per-k-block clock64 stamps of CTA 0 written over y
   auto TR = [&](int slot, int i) {
-    if (blockIdx.x == 0 && i < 64) reinterpret_cast<uint32_t*>(y)[slot * 64 + i] = (uint32_t)clock64();
+    if (blockIdx.x == 0 && i < 128) reinterpret_cast<uint32_t*>(y)[slot * 128 + i] = (uint32_t)clock64();
   };
+  auto GT = [&](int which) {
+    uint64_t g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    reinterpret_cast<uint64_t*>(y)[1024 + blockIdx.x * 4 + which] = g;
+  };
+  if (threadIdx.x == 0) GT(0);
 #else
   auto TR = [](int, int) {};
 #endif
   __shared__ __align__(8) uint64_t a_full[kAStages], a_empty[kAStages];
-  __shared__ __align__(8) uint64_t b_full[kBStages], b_empty[kBStages];
-  __shared__ __align__(8) uint64_t split_bar[kSplitStages], split_free[kSplitStages];
+  // kb_full[s]: B landed (tx) + 8 split warps stored X1/X2; kb_free[s]: both
+  // issuers' MMAs of the k-block retired (commit); d_full / d_empty: the
+  // accumulator handshake with the epilogue (which re-zeroes D after reading)
+  __shared__ __align__(8) uint64_t kb_full[kStages], kb_free[kStages];
   __shared__ __align__(8) uint64_t d_full[2], d_empty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ float zero_word;
@@ -199,16 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&a_full[s], 1);
       mbar_init(&a_empty[s], kSplitWarps);
     }
-    for (int s = 0; s < kBStages; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
-    }
-    for (int s = 0; s < kSplitStages; ++s) {
-      mbar_init(&split_bar[s], kSplitWarps);
-      mbar_init(&split_free[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&kb_full[s], kSplitWarps + 1);
+      mbar_init(&kb_free[s], 2);
     }
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&d_full[s], 1);
+      mbar_init(&d_full[s], 2);
       mbar_init(&d_empty[s], kEpiWarps);
     }
     fence_mbar_init();
@@ -224,6 +261,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
+  if (warp >= 2 + kSplitWarps && warp < kIssuer2) {
+    // both accumulators start at zero: every MMA accumulates, so the two
+    // issuers need no ordering between them
+    uint32_t z[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) z[i] = 0u;
+#pragma unroll
+    for (int c = 0; c < 2 * kNC; c += 32) tmem_st32(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + c, z);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -254,18 +304,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_4d(ab + kABoxBytes + kHaloBytes, &tmh, &a_full[sa], tc.w0 + kTileW,
                         tc.h0 - 1, chunk * kKB, tc.n);
           for (int tap = 0; tap < 9; ++tap, ++bc) {
-            const int sb = bc % kBStages;
-            if (bc >= kBStages) mbar_wait(&b_empty[sb], ((bc / kBStages) - 1) & 1);
+            const int sb = bc % kStages;
+            if (bc >= kStages) mbar_wait(&kb_free[sb], ((bc / kStages) - 1) & 1);
             TR(5, bc);
-            mbar_arrive_expect_tx(&b_full[sb], kBBytes);
-            tma_load_3d(b_ring + sb * kBBytes, &tmw, &b_full[sb], chunk * kKB, 2 * tc.co0, tap);
+            mbar_arrive_expect_tx(&kb_full[sb], kBBytes);
+            tma_load_3d(b_ring + sb * kBBytes, &tmw, &kb_full[sb], chunk * kKB, 2 * tc.co0, tap);
           }
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
+  } else if (warp == 1 || warp == kIssuer2) {
+    // ------------------------------------------------ MMA issuers
+    // A TS-form MMA costs its issuing thread ~80 cycles (the A fetch from
+    // TMEM) whatever N is, so one thread cannot keep the tensor pipe busy;
+    // two issuers split the products of every k-step into the same
+    // accumulator (tools/micro/umma_queue.cu, umma_shared_acc.cu):
+    //   warp 1:   D[:, 0:128] += X1 [W1 | W2]     (N = 128)
+    //   issuer 2: D[:, 0:64]  += X2 W1            (N = 64)
     if (lane == 0) {
+      const bool first = warp == 1;
       int kc = 0, it = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
@@ -273,34 +330,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + acc * kNC;
         for (int kb = 0; kb < 9 * cchunks; ++kb, ++kc) {
-          const int sb = kc % kBStages, ss = kc % kSplitStages;
-          mbar_wait(&split_bar[ss], (kc / kSplitStages) & 1);
-          TR(0, kc);
-          mbar_wait(&b_full[sb], (kc / kBStages) & 1);
-          TR(1, kc);
+          const int s = kc % kStages;
+          mbar_wait(&kb_full[s], (kc / kStages) & 1);
+          if (first) TR(0, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t x1 = tmem + kTmemA + ss * 2 * kACols, x2 = x1 + kACols;
           // B: K-major SW128 (128-byte rows of 64 bf16 channels, SBO = 1 KiB
           // per 8-row group); a 16-channel k-step advances the start by 32 B
-          const uint64_t db = make_desc(smem_u32(b_ring + sb * kBBytes), 16, 1024, 2);
+          const uint64_t db = make_desc(smem_u32(b_ring + s * kBBytes), 16, 1024, 2);
+          const uint32_t xa = tmem + kTmemA + s * 2 * kACols + (first ? 0 : kACols);
+          if (first) {
 #pragma unroll
-          for (int ks = 0; ks < kKB / kKS; ++ks) {
-            mma_bf16_ts<kNC>(d, x1 + 8 * ks, db + 2 * ks, (kb | ks) ? 1u : 0u);
-            mma_bf16_ts<kN>(d, x2 + 8 * ks, db + 2 * ks, 1u);  // W1 rows only
+            for (int ks = 0; ks < kKB / kKS; ++ks) mma_bf16_ts<kNC>(d, xa + 8 * ks, db + 2 * ks, 1u);
+          } else {
+#pragma unroll
+            for (int ks = 0; ks < kKB / kKS; ++ks) mma_bf16_ts<kN>(d, xa + 8 * ks, db + 2 * ks, 1u);
           }
-          umma_commit(&b_empty[sb]);
-          umma_commit(&split_free[ss]);
-          TR(2, kc);
+          if (first) TR(8, kc);
+          umma_commit(&kb_free[s]);
+          if (first) TR(2, kc);
         }
         umma_commit(&d_full[acc]);
       }
     }
   } else if (warp < 2 + kSplitWarps) {
     // ------------------------------------------------ split workers (8 warps)
-    // warp -> TMEM lane quarter q = warp % 4 (pixels m = 32q + lane) and half
-    // of the 64 channels of a k-block; each thread splits its pixel's 32
+    // warp -> TMEM lane quarter q = warp % 4 (pixels m = 32q + lane) and a
+    // 16-channel slice of the k-block; each thread splits its pixel's 16
     // channels into bf16 x1 / x2 pairs and stores them to TMEM (tcgen05.st)
-    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int q = warp & 3, half = (warp - 2) >> 2;  // half = slice index
     const int m = 32 * q + lane;
     const int hh = m / kTileW, e = m % kTileW;
     int ac = 0, kc = 0;
@@ -312,13 +369,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&a_full[sa], (ac / kAStages) & 1);
         const unsigned char* ab = a_ring + sa * kABytes;
         for (int tap = 0; tap < 9; ++tap, ++kc) {
-          const int ss = kc % kSplitStages;
+          const int ss = kc % kStages;
           const int dj = tap / 3, di = tap % 3 - 1;  // box row hh + dj (row 0 = h0-1)
-          if (kc >= kSplitStages) mbar_wait(&split_free[ss], ((kc / kSplitStages) - 1) & 1);
+          if (kc >= kStages) mbar_wait(&kb_free[ss], ((kc / kStages) - 1) & 1);
           if (q == 0 && lane == 0 && half == 0) TR(3, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 2 * kACols +
-                              half * (kACols / 2);
+                              half * kPairs;
           // Box [c][10 rows][16 cols] and halo boxes [c][10 rows][4 cols],
           // unswizzled: the two pixel rows of a warp sit 64 bytes apart, so a
           // warp's read of one channel is a single conflict-free wavefront.
@@ -338,10 +395,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             base = reinterpret_cast<const unsigned char*>(&zero_word);
             stride = 0;
           }
-          const unsigned char* p = base + half * (kKB / 2) * stride;
-          uint32_t v1[16], v2[16];
+          const unsigned char* p = base + half * (2 * kPairs) * stride;
+          uint32_t v1[kPairs], v2[kPairs];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < kPairs; ++j) {
             const float f0 = *reinterpret_cast<const float*>(p + (2 * j) * stride);
             const float f1 = *reinterpret_cast<const float*>(p + (2 * j + 1) * stride);
             const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
@@ -350,26 +407,34 @@ __global__ void __launch_bounds__(kThreads, 1)
             v1[j] = a1;
             v2[j] = pack_bf16x2(r0, r1);
           }
-          tmem_st16(ta, v1);
-          tmem_st16(ta + kACols, v2);
+          if constexpr (kPairs == 16) {
+            tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(v1));
+            tmem_st16(ta + kACols, *reinterpret_cast<const uint32_t(*)[16]>(v2));
+          } else {
+            tmem_st8(ta, *reinterpret_cast<const uint32_t(*)[8]>(v1));
+            tmem_st8(ta + kACols, *reinterpret_cast<const uint32_t(*)[8]>(v2));
+          }
           if (q == 0 && lane == 0 && half == 0) TR(4, kc);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           if (q == 0 && lane == 0 && half == 0) TR(7, kc);
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (q == 0 && lane == 0 && half == 0) TR(6, kc);
-          if (lane == 0) mbar_arrive(&split_bar[ss]);
+          if (lane == 0) mbar_arrive(&kb_full[ss]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_empty[sa]);  // this warp's box reads are done
       }
     }
-  } else {
+  } else if (warp < kIssuer2) {
     // ------------------------------------------------ epilogue (4 warps)
     const int q = warp & 3;
     const int m = 32 * q + lane;
     const int hh = m / kTileW, e = m % kTileW;
     const int64_t plane = (int64_t)h * w;
+    uint32_t zero16[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) zero16[i] = 0u;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
       const TileCoord tc = tile_coord(t, co_tiles, wtiles, htiles);
@@ -380,28 +445,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int oh = tc.h0 + hh, ow = tc.w0 + e;
       float* yp = y + (((int64_t)tc.n * cout + tc.co0) * h + oh) * w + ow;
 #pragma unroll 1
-      for (int ch0 = 0; ch0 < kN; ch0 += 32) {
-        uint32_t r[32], rl[32];
-        tmem_ld32(taddr + ch0, r);
-        tmem_ld32(taddr + kN + ch0, rl);
+      for (int ch0 = 0; ch0 < kN; ch0 += 16) {
+        uint32_t r[16], rl[16];
+        tmem_ld16(taddr + ch0, r);
+        tmem_ld16(taddr + kN + ch0, rl);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        tmem_st16(taddr + ch0, zero16);  // re-arm the accumulator for tile it + 2
+        tmem_st16(taddr + kN + ch0, zero16);
 #ifdef SC_TC_TRACE
         if (false) {
 #else
         if (oh < h) {
 #endif
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
+          for (int c = 0; c < 16; ++c)
             yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
         }
       }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&d_empty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#ifdef SC_TC_TRACE
+  if (warp == 1 && lane == 0) GT(2);
+#endif
   __syncthreads();
+#ifdef SC_TC_TRACE
+  if (threadIdx.x == 0) GT(3);
+#endif
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
