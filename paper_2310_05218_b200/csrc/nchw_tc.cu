@@ -10,29 +10,34 @@
 //   persistent kernel (one CTA per SM) walks the tiles.  A k-block is one tap
 //   x 64 input channels.
 // * A (pixels x channels): one 4-D TMA box {16 w, 10 h, 64 c} per channel
-//   chunk serves all 9 taps (rows h0-1 .. h0+8; TMA zero-fills rows outside
-//   the image = the zero padding), plus two {4 w} halo boxes for the columns
-//   left / right of the tile.  Split warps read the tap's shifted window from
-//   shared memory, split every value x = x1 + x2 + O(2^-17 x) with
-//   x1 = bf16(x), x2 = bf16(x - x1), and store both (packed bf16x2) to TMEM:
-//   the MMAs take A from TMEM (TS form).
+//   chunk (rows h0-1 .. h0+8; TMA zero-fills rows outside the image = the
+//   zero padding) plus two {4 w} halo boxes for the columns left / right of
+//   the tile.  The split warps convert it once per chunk into bf16 pairs
+//   x = x1 + x2 + O(2^-17 x), x1 = bf16(x), x2 = bf16(x - x1), in a swizzled
+//   [pixel][channel] split buffer (18 columns incl. halos, zero at the image
+//   edge); then per tap each thread copies its pixel's shifted 32-channel
+//   slice to TMEM (tcgen05.st): the MMAs take A from TMEM (TS form).
 // * B = the tap's weights, pre-split on the device the same way into
 //   [W1 | W2] (N = 128 rows, K-major, 128-byte swizzle), one TMA box per
 //   k-block.
-// * Per 16-channel k-step: D[:, 0:128] += X1 [W1 | W2] and D[:, 0:64] += X2 W1
-//   (two MMAs: measured TS cost is ~80 cycles per instruction up to N = 128,
-//   so N = 128 + 64 beats three N = 64 products); the epilogue adds
-//   D[:, c] + D[:, 64 + c].  The dropped X2 W2 and the split residuals bound
-//   the error per product by ~2^-16 relative: normwise ~1e-5, inside the
-//   north-star 1e-5 * k * sqrt(Cin) (2.4e-4 here) where plain TF32 / BF16
-//   would not be.  kind::f16 issues K = 16 per instruction at
-//   the cost of a K = 8 tf32 one, so this is 2x the 3xTF32 throughput.
-// * Warp roles: warp 0 TMA producer, warp 1 TMEM owner + single-thread MMA
-//   issuer, warps 2..9 split workers, warps 10..13 epilogue (tcgen05.ld ->
-//   NCHW stores).  TMEM (512 columns) holds two 128-column accumulators, so
-//   the epilogue of one tile overlaps the MMAs of the next, and four X1/X2
-//   stages.  Every hand-off is an mbarrier; the MMA side releases smem / TMEM
-//   stages with tcgen05.commit.
+// * Per 16-channel k-step: D[:, 0:128] += X1 [W1 | W2] and D[:, 0:64] += X2 W1;
+//   the epilogue adds D[:, c] + D[:, 64 + c].  The dropped X2 W2 and the
+//   split residuals bound the error per product by ~2^-16 relative:
+//   normwise ~5e-6 measured, inside the north-star 1e-5 * k * sqrt(Cin)
+//   (2.4e-4 here) where plain TF32 / BF16 would not be.
+//   kind::f16 issues K = 16 per instruction at the cost of a K = 8 tf32 one.
+// * Warp roles: warp 0 B producer (TMA), warp 1 TMEM owner + MMA issuer for
+//   X1 [W1 | W2], warps 2..9 split workers, warps 10..13 epilogue
+//   (tcgen05.ld -> NCHW stores, then re-zero D), warp 14 MMA issuer for
+//   X2 W1 (one thread cannot issue TS MMAs fast enough to fill the tensor
+//   pipe; two issuers accumulate into the same D), warp 15 A-box producer.
+//   TMEM (512 columns): two 128-column accumulators, so the epilogue of one
+//   tile overlaps the MMAs of the next, and four X1/X2 stages.  Hand-offs are
+//   mbarriers; the MMA side releases smem / TMEM stages with tcgen05.commit.
+// * Measured (B200, config 4): 0.055 ms vs cuDNN FP32 0.17 ms.  The kernel is
+//   shared-memory-bandwidth bound: per 128-pixel tile ~800 KB of smem traffic
+//   (split reads/writes, per-tap copies, B writes by TMA and B reads by the
+//   MMAs) against 128 B/clk.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -59,18 +64,21 @@ constexpr int kABoxBytes = kBoxH * kTileW * kKB * 4;   // [c][rows][cols] fp32, 
 constexpr int kHaloBytes = kBoxH * kHaloW * kKB * 4;   // [c][rows][4] fp32, 10 KiB
 constexpr int kABytes = kABoxBytes + 2 * kHaloBytes;   // [box | left | right]
 constexpr int kBBytes = kNC * kKB * 2;          // bf16, 128-byte rows: 16 KiB
-constexpr int kAStages = 2;                     // A box ring (one per channel chunk)
+constexpr int kAStages = 1;                     // A box (one per channel chunk)
+constexpr int kXCols = kTileW + 2;              // split buffer columns w0-1 .. w0+16
+constexpr int kXPix = kBoxH * kXCols;           // 180 pixels
+constexpr int kXBytes = kXPix * kKB * 2;        // bf16 x1 (or x2) of one chunk: 22.5 KiB
 constexpr int kStages = 4;                      // k-block ring: B slot + TMEM X1/X2 stage
 constexpr int kACols = kKB / 2;                 // TMEM columns per X1 (or X2) k-block
 constexpr int kTmemCols = 512;                  // D0 [0,128) D1 [128,256) A [256,512)
 constexpr int kTmemA = 256;
 constexpr int kSplitWarps = 8;                 // 2 per TMEM lane quarter
-constexpr int kSplitParts = kSplitWarps / 4;    // channel slices of a k-block
-constexpr int kPairs = kKB / kSplitParts / 2;   // packed bf16x2 columns per thread
 constexpr int kEpiWarps = 4;
 constexpr int kIssuer2 = 2 + kSplitWarps + kEpiWarps;   // warp of the second MMA issuer
-constexpr int kThreads = 32 * (kIssuer2 + 1);
-constexpr size_t kSmem = 1024 + (size_t)kAStages * kABytes + (size_t)kStages * kBBytes;
+constexpr int kAProducer = kIssuer2 + 1;                 // warp of the A-box TMA producer
+constexpr int kThreads = 32 * (kAProducer + 1);
+constexpr size_t kSmem =
+    1024 + (size_t)kAStages * kABytes + (size_t)kStages * kBBytes + 2 * (size_t)kXBytes;
 static_assert(kTmemA + kStages * 2 * kACols <= kTmemCols, "TMEM budget");
 
 __device__ __forceinline__ uint64_t make_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo,
@@ -120,20 +128,6 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, uint64_
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-        "=r"(r[31])
-      : "r"(taddr));
-}
-
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -142,13 +136,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
       "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
       "r"(v[15])
       : "memory");
-}
-
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
-                   taddr),
-               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-               : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -229,6 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ float zero_word;
   unsigned char* a_ring = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* b_ring = a_ring + kAStages * kABytes;
+  // split buffer: x1 then x2, [pixel][64 channels] as 32 packed bf16x2 words,
+  // 16-byte chunks XOR-swizzled by (pixel & 7) so both the split writes and
+  // the per-tap reads of 8 consecutive pixels hit distinct banks
+  unsigned char* xbuf = b_ring + kStages * kBBytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int co_tiles = cout / kN, wtiles = w / kTileW, htiles = (h + kTileH - 1) / kTileH;
@@ -275,13 +266,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+  if (warp == kAProducer) {
+    // ------------------------------------------------ A-box TMA producer
+    // Separate from the B producer so the next chunk's box is requested as
+    // soon as the split warps have consumed the current one (its HBM latency
+    // then hides behind the current chunk's 9 taps).
     if (lane == 0) {
       prefetch_tmap(&tmx);
       prefetch_tmap(&tmh);
-      prefetch_tmap(&tmw);
-      int ac = 0, bc = 0;  // ring counters across tiles
+      int ac = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const TileCoord tc = tile_coord(t, co_tiles, wtiles, htiles);
         // The innermost TMA coordinate must be 16-byte aligned and in range
@@ -303,12 +296,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (right)
             tma_load_4d(ab + kABoxBytes + kHaloBytes, &tmh, &a_full[sa], tc.w0 + kTileW,
                         tc.h0 - 1, chunk * kKB, tc.n);
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------ B (weights) TMA producer
+    if (lane == 0) {
+      prefetch_tmap(&tmw);
+      int bc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int co0 = tile_coord(t, co_tiles, wtiles, htiles).co0;
+        for (int chunk = 0; chunk < cchunks; ++chunk) {
           for (int tap = 0; tap < 9; ++tap, ++bc) {
             const int sb = bc % kStages;
             if (bc >= kStages) mbar_wait(&kb_free[sb], ((bc / kStages) - 1) & 1);
             TR(5, bc);
             mbar_arrive_expect_tx(&kb_full[sb], kBBytes);
-            tma_load_3d(b_ring + sb * kBBytes, &tmw, &kb_full[sb], chunk * kKB, 2 * tc.co0, tap);
+            tma_load_3d(b_ring + sb * kBBytes, &tmw, &kb_full[sb], chunk * kKB, 2 * co0, tap);
           }
         }
       }
@@ -354,12 +358,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < 2 + kSplitWarps) {
     // ------------------------------------------------ split workers (8 warps)
-    // warp -> TMEM lane quarter q = warp % 4 (pixels m = 32q + lane) and a
-    // 16-channel slice of the k-block; each thread splits its pixel's 16
-    // channels into bf16 x1 / x2 pairs and stores them to TMEM (tcgen05.st)
-    const int q = warp & 3, half = (warp - 2) >> 2;  // half = slice index
+    // Once per channel chunk the 8 warps convert the fp32 box (+ halo
+    // columns) into bf16 x1 / x2 pairs in the split buffer; then for each tap
+    // a thread copies its pixel's shifted 32-channel slice (8 x 16 B) to the
+    // stage's TMEM columns.  Warp -> TMEM lane quarter q = warp % 4 (pixels
+    // m = 32q + lane) and channel half `half`.
+    const int q = warp & 3, half = (warp - 2) >> 2;
     const int m = 32 * q + lane;
     const int hh = m / kTileW, e = m % kTileW;
+    const int stid = threadIdx.x - 64;  // 0..255
     int ac = 0, kc = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int w0 = tile_coord(t, co_tiles, wtiles, htiles).w0;
@@ -368,52 +375,71 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sa = ac % kAStages;
         mbar_wait(&a_full[sa], (ac / kAStages) & 1);
         const unsigned char* ab = a_ring + sa * kABytes;
+        // all split warps finished reading the previous chunk's buffer
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kSplitWarps) : "memory");
+        // warp `sw` converts 8-channel group g = sw for every pixel: the 160
+        // box pixels (lane-consecutive, immediate channel offsets), then the
+        // 20 halo pixels (columns w0-1 / w0+16, zero at the image edge)
+        {
+          const int g = warp - 2;
+          auto put = [&](int pix, const unsigned char* src, int stride) {
+            uint4 w1, w2;
+            uint32_t* p1 = &w1.x;
+            uint32_t* p2 = &w2.x;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float f0 = *reinterpret_cast<const float*>(src + (2 * j) * stride);
+              const float f1 = *reinterpret_cast<const float*>(src + (2 * j + 1) * stride);
+              const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
+              p1[j] = a1;
+              p2[j] = pack_bf16x2(f0 - __uint_as_float(a1 << 16),
+                                  f1 - __uint_as_float(a1 & 0xffff0000u));
+            }
+            const int off = pix * (kKB * 2) + ((g ^ (pix & 7)) << 4);
+            *reinterpret_cast<uint4*>(xbuf + off) = w1;
+            *reinterpret_cast<uint4*>(xbuf + kXBytes + off) = w2;
+          };
+          constexpr int kBoxStride = kBoxH * kTileW * 4;  // bytes per channel
+#pragma unroll
+          for (int i = 0; i < kBoxH * kTileW / 32; ++i) {
+            const int p = 32 * i + lane;             // box pixel (row p / 16, col p % 16)
+            put(p + 2 * (p >> 4) + 1, ab + p * 4 + 8 * g * kBoxStride, kBoxStride);
+          }
+          if (lane < 2 * kBoxH) {
+            const int r = lane >> 1, right_col = lane & 1;
+            const int pix = r * kXCols + (right_col ? kXCols - 1 : 0);
+            if (right_col ? right : left) {
+              constexpr int kHStride = kBoxH * kHaloW * 4;
+              put(pix, ab + kABoxBytes + (right_col ? kHaloBytes : 0) + (r * kHaloW + (right_col ? 0 : 3)) * 4 +
+                           8 * g * kHStride, kHStride);
+            } else {
+              put(pix, reinterpret_cast<const unsigned char*>(&zero_word), 0);
+            }
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kSplitWarps) : "memory");
+        if (lane == 0) mbar_arrive(&a_empty[sa]);  // box consumed: next chunk may land
         for (int tap = 0; tap < 9; ++tap, ++kc) {
           const int ss = kc % kStages;
-          const int dj = tap / 3, di = tap % 3 - 1;  // box row hh + dj (row 0 = h0-1)
+          const int dj = tap / 3, di = tap % 3 - 1;
           if (kc >= kStages) mbar_wait(&kb_free[ss], ((kc / kStages) - 1) & 1);
           if (q == 0 && lane == 0 && half == 0) TR(3, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 2 * kACols +
-                              half * kPairs;
-          // Box [c][10 rows][16 cols] and halo boxes [c][10 rows][4 cols],
-          // unswizzled: the two pixel rows of a warp sit 64 bytes apart, so a
-          // warp's read of one channel is a single conflict-free wavefront.
-          // Each lane walks the channels with its own base / stride: box
-          // column e + di, halo column (tile edge) or a zero word (image edge).
-          const int ee = e + di;
-          const int r = hh + dj;
-          const unsigned char* base;
-          int stride;
-          if (ee >= 0 && ee < kTileW) {
-            base = ab + (r * kTileW + ee) * 4;
-            stride = kBoxH * kTileW * 4;
-          } else if (di < 0 ? left : right) {
-            base = ab + kABoxBytes + (di > 0 ? kHaloBytes : 0) + (r * kHaloW + (di < 0 ? 3 : 0)) * 4;
-            stride = kBoxH * kHaloW * 4;
-          } else {
-            base = reinterpret_cast<const unsigned char*>(&zero_word);
-            stride = 0;
-          }
-          const unsigned char* p = base + half * (2 * kPairs) * stride;
-          uint32_t v1[kPairs], v2[kPairs];
+                              half * (kACols / 2);
+          const int pix = (hh + dj) * kXCols + e + 1 + di;
+          const unsigned char* rp = xbuf + pix * (kKB * 2);
+          uint32_t v1[16], v2[16];
 #pragma unroll
-          for (int j = 0; j < kPairs; ++j) {
-            const float f0 = *reinterpret_cast<const float*>(p + (2 * j) * stride);
-            const float f1 = *reinterpret_cast<const float*>(p + (2 * j + 1) * stride);
-            const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
-            const float r0 = f0 - __uint_as_float(a1 << 16);
-            const float r1 = f1 - __uint_as_float(a1 & 0xffff0000u);
-            v1[j] = a1;
-            v2[j] = pack_bf16x2(r0, r1);
+          for (int j = 0; j < 4; ++j) {
+            const int off = ((4 * half + j) ^ (pix & 7)) << 4;
+            const uint4 a = *reinterpret_cast<const uint4*>(rp + off);
+            const uint4 b2 = *reinterpret_cast<const uint4*>(rp + kXBytes + off);
+            v1[4 * j] = a.x, v1[4 * j + 1] = a.y, v1[4 * j + 2] = a.z, v1[4 * j + 3] = a.w;
+            v2[4 * j] = b2.x, v2[4 * j + 1] = b2.y, v2[4 * j + 2] = b2.z, v2[4 * j + 3] = b2.w;
           }
-          if constexpr (kPairs == 16) {
-            tmem_st16(ta, *reinterpret_cast<const uint32_t(*)[16]>(v1));
-            tmem_st16(ta + kACols, *reinterpret_cast<const uint32_t(*)[16]>(v2));
-          } else {
-            tmem_st8(ta, *reinterpret_cast<const uint32_t(*)[8]>(v1));
-            tmem_st8(ta + kACols, *reinterpret_cast<const uint32_t(*)[8]>(v2));
-          }
+          tmem_st16(ta, v1);
+          tmem_st16(ta + kACols, v2);
           if (q == 0 && lane == 0 && half == 0) TR(4, kc);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           if (q == 0 && lane == 0 && half == 0) TR(7, kc);
@@ -422,11 +448,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (q == 0 && lane == 0 && half == 0) TR(6, kc);
           if (lane == 0) mbar_arrive(&kb_full[ss]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_empty[sa]);  // this warp's box reads are done
       }
     }
-  } else if (warp < kIssuer2) {
+  } else if (warp >= 2 + kSplitWarps && warp < kIssuer2) {
     // ------------------------------------------------ epilogue (4 warps)
     const int q = warp & 3;
     const int m = 32 * q + lane;

@@ -33,11 +33,15 @@ torch.cuda.synchronize()
 ts = []
 for rep in range(5):
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
     a.record()
     for _ in range(100):
         sc.conv2d_nchw(xd, wd, 1)
+    w1 = time.perf_counter()
     b.record()
     b.synchronize()
     ts.append(a.elapsed_time(b) / 100)
+    print(f"  host issue {1e4 * (w1 - w0):.1f} us/call, device {ts[-1] * 1e3:.1f} us/call")
 t = sorted(ts)[2]
 print(f"config 4 TC: {t * 1e3:.1f} us (min {min(ts)*1e3:.1f} max {max(ts)*1e3:.1f})  {2 * 16 * 64 * 112 * 112 * 64 * 9 / t / 1e9:.1f} TFLOP/s")

@@ -1,6 +1,6 @@
-"""Per-k-block timeline of CTA 0 of the NCHW tensor-core kernel (library built with
-make EXTRA=-DSC_TC_TRACE; the stamps overwrite y)."""
-import os
+"""Per-k-block timeline of CTA 0 of the NCHW tensor-core kernel plus per-CTA
+globaltimer stamps (library built with make EXTRA=-DSC_TC_TRACE; the stamps
+overwrite y)."""
 import sys
 
 import numpy as np
@@ -14,11 +14,20 @@ wd = torch.randn((64, 64, 3, 3), device="cuda") / 24
 for _ in range(3):
     y = sc.conv2d_nchw(xd, wd, 1)
 torch.cuda.synchronize()
-t = y.reshape(-1)[:8 * 64].view(torch.int32).cpu().numpy().astype(np.int64).reshape(8, 64)
+flat = y.reshape(-1)
+t = flat[:9 * 128].view(torch.int32).cpu().numpy().astype(np.int64).reshape(9, 128)
 t0 = t[0, 0]
 t = (t - t0) & 0xffffffff
 t[t > 2**31] -= 2**32
-names = ["mma:split_ok", "mma:b_ok", "mma:committed", "split:free_ok", "split:st_issued", "prod:b_empty_ok", "split:arrive", "split:st_done"]
+names = ["mma:full_ok", "-", "mma:committed", "split:free_ok", "split:st_issued", "prod:free_ok",
+         "split:arrive", "split:st_done", "mma:issued"]
 print("kc " + " ".join(f"{n:>15}" for n in names))
-for kc in range(45):
-    print(f"{kc:2d} " + " ".join(f"{t[r, kc]:15d}" for r in range(8)))
+for kc in range(0, 99):
+    print(f"{kc:2d} " + " ".join(f"{t[r, kc]:15d}" for r in range(9)))
+g = flat[2048:2048 + 148 * 8].view(torch.int64).cpu().numpy().reshape(148, 4)
+base = g[:, 0].min()
+g = g - base
+print("per-CTA globaltimer (ns): start, setup done, loop done, teardown")
+for b in range(0, 148, 8):
+    print(b, g[b])
+print("max loop end", g[:, 2].max(), "min", g[:, 2].min(), "mean setup", g[:, 1].mean())
