@@ -366,7 +366,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int m = 32 * q + lane;
     const int hh = m / kTileW, e = m % kTileW;
-    const int stid = threadIdx.x - 64;  // 0..255
     int ac = 0, kc = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int w0 = tile_coord(t, co_tiles, wtiles, htiles).w0;

@@ -29,9 +29,13 @@ def test_config4_exact_matches_composed_oracle():
 
 @pytest.mark.parametrize("n,cin,cout,h,w,k,p", [(1, 3, 5, 17, 23, 3, 1), (2, 7, 70, 33, 9, 3, 1),
                                                  (1, 4, 4, 10, 10, 5, 2), (1, 2, 3, 8, 8, 3, 0),
-                                                 # tcgen05 3xTF32 path (Cin % 32, Cout % 64, W % 16)
-                                                 (2, 32, 64, 16, 32, 3, 1), (1, 64, 128, 21, 48, 3, 1),
-                                                 (3, 96, 64, 9, 16, 3, 1), (1, 32, 64, 1, 16, 3, 1)])
+                                                 # tcgen05 bf16x3 path (Cin % 64, Cout % 64, W % 16):
+                                                 # edge tiles, ragged H, several chunks / co-tiles
+                                                 (2, 64, 64, 16, 32, 3, 1), (1, 64, 128, 21, 48, 3, 1),
+                                                 (3, 128, 64, 9, 16, 3, 1), (1, 64, 64, 1, 16, 3, 1),
+                                                 (2, 192, 128, 7, 48, 3, 1),
+                                                 # Cin % 64 != 0 -> CUDA-core kernel
+                                                 (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1)])
 def test_nchw_shapes(n, cin, cout, h, w, k, p):
     rng = np.random.default_rng(n + cin + cout + h + w)
     x = rng.standard_normal((n, cin, h, w), dtype=np.float32)
