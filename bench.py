@@ -315,7 +315,18 @@ def per_config(torch, sc, hbm_peak, args, traffic):
     tc = time_launches(torch, contrast4, 5, 2, flush=flush)
     tcd = time_launches(torch, lambda: F.conv2d(xn, wn, padding=1), 5, 2, flush=flush)
     torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = prev
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            bf16_peak, bf16_src = float(json.load(fh)["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops"
+    except (OSError, KeyError, ValueError):
+        bf16_peak, bf16_src = 2250.0, "fallback nominal dense bf16 (B200_PROFILING.md)"
+    # nchw3x3_tc_kernel runs 3 bf16 products per useful MAC (x1 w1, x1 w2, x2 w1)
+    tensor = {"kernel": "nchw3x3_tc_kernel (tcgen05 kind::f16, bf16x3 split)",
+              "executed_bf16_tflops": round(3 * fl / t / 1e12, 1), "peak": bf16_peak,
+              "peak_source": bf16_src, "frac": round(3 * fl / t / 1e12 / bf16_peak, 4),
+              "fp32_equiv_tflops": round(fl / t / 1e12, 1)}
     out["cfg4_nchw_3x3"] = {"ms": round(t * 1e3, 4), **roofline(nb, fl, t, hbm_peak),
+                            "tensor_roofline": tensor,
                             "im2col_cublas_ms": round(tc * 1e3, 3),
                             "cudnn_fp32_ms": round(tcd * 1e3, 3),
                             "cpu": cpu_rate("nchw", {"cfg": 4, "cin": 64, "cout": 64, "h": 112,
@@ -478,7 +489,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     dom = max(t_avg, t_max)
-    nbuf = os.environ.get("SC_POOL_NBUF", "4")
+    nbuf = "2"  # pool_tma.cu launch_nbuf<..., 2> (double-buffered TMA ring)
     dom_name = (f"pool_tma_kernel<1, 16, {nbuf}>" if t_avg >= t_max
                 else f"pool_tma_kernel<2, 16, {nbuf}>")  # <op (1 = AVG, 2 = MAX), k, ring depth>
     achieved = alg_bytes_op / dom / 1e9
