@@ -10,7 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
     python bench.py --steps 5 --warmup 3 --no-extras --no-cpu --no-sustain > $OUT/ncu_launch.log 2>&1
 for w in ${WORKLOADS:-pool16 conv3 conv5 conv7 conv1d nchw pool64 pool255}; do
   timeout 120 python $P $w 1 > $OUT/plain_$w.log 2>&1 &&
-  timeout 900 ncu --set full --clock-control none --import-source on \
+  timeout 900 ncu -f --set full --clock-control none --import-source on \
       -k regex:"pool_|conv2d_|nchw|tc_" -c ${NCU_COUNT:-3} -o /tmp/prof_$w python $P $w 1 > $OUT/ncu_$w.log 2>&1
   if [ -f /tmp/prof_$w.ncu-rep ]; then
     ncu -i /tmp/prof_$w.ncu-rep --page raw --csv > $OUT/raw_$w.csv 2>/dev/null
