@@ -147,3 +147,9 @@ def test_no_cpu_fallback_without_gpu():
         sc.conv2d_reference(np.ones((4, 4), np.float32), np.ones((2, 2), np.float32))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         sc.sliding_window_sum(np.ones(8, np.float32), 3)
+
+
+def test_verify_suite_rejects_zero_trials():
+    import paper_2310_05218_b200 as sc
+    with pytest.raises(ValueError):
+        sc.verify_suite(trials=0)
