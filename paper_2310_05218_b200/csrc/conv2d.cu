@@ -376,6 +376,8 @@ int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return get_encode(); }
 int conv1d_tma(const float* x, int64_t rows, int64_t length, const float* w, int64_t k,
                bool exact, float* y, cudaStream_t st);
+int conv2d_big(const float* x, int64_t batch, int64_t h, int64_t w, const float* f_host,
+               int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st);
 
 int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                         int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st) {
@@ -394,6 +396,9 @@ int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, con
   else if (kh == 1 && kw == 7) rc = try_tma<1, 7>(x, batch, h, w, f, exact, y, st, &done);
   else if (kh == 1 && kw == 3) rc = try_tma<1, 3>(x, batch, h, w, f, exact, y, st, &done);
   if (rc || done) return rc;
+  // runtime (kh, kw) up to 64 x 64: the register-blocked kernel (conv2d_big.cu)
+  rc = conv2d_big(x, batch, h, w, f, kh, kw, exact, y, st);
+  if (rc != 1) return rc;
   return launch_generic<float>(x, batch, h, w, f, kh, kw, exact, y, st);
 }
 

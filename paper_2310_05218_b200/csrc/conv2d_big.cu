@@ -1,0 +1,214 @@
+// 2-D single-channel valid convolution for runtime filter sizes (the paper's
+// 11..51 sweep, reference bench.py:20; conv2d_slide_compound / _generic /
+// conv2d_reference with any kh x kw up to 64 x 64, kernels.py:235-255).
+//
+// The filter-size-specialised TMA kernels (conv2d.cu) fully unroll KH x KW
+// with the taps as constant operands; that does not scale to 51 x 51 = 2,601
+// taps.  Here the taps sit in shared memory and the work is register-blocked
+// so each shared-memory load feeds many FMAs:
+//   * a CTA owns 64 output rows x 128 output columns of one image and stages
+//     the (64 + kh - 1) x (128 + kw - 1 (+pad)) input tile and the taps in
+//     shared memory;
+//   * a thread owns R = 8 output rows x 4 consecutive columns (32 register
+//     accumulators); warp w (of 8) owns rows 8w .. 8w+7, lane l columns 4l .. 4l+3,
+//     so a warp's LDS.128 of 4 consecutive inputs per lane is 512 contiguous
+//     bytes (conflict-free);
+//   * the thread walks the input rows q of its band once (rolling
+//     accumulators, the custom kernels' reuse, kernels.py:185-206): input row
+//     q feeds output rows r with j = q - r in [0, kh).  Along the row it
+//     slides an 8-value register window in steps of 4 taps: one LDS.128 of
+//     inputs and, per live output row, one broadcast LDS.128 of 4 taps for
+//     16 FMAs -- ~14 FMAs per shared-memory load, so the FP32 pipe, not
+//     shared memory, is the limit.
+//   * kExact: __fmul_rn + __fadd_rn, and every output still accumulates in
+//     the reference's order (j ascending as q ascends, i ascending within a
+//     row, from 0): bit-identical to _accumulate_taps (reference.py:15-23).
+#include <algorithm>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace sc {
+namespace {
+
+constexpr int kR = 8;                 // output rows per thread
+constexpr int kC = 4;                 // output columns per thread
+constexpr int kTileCols = 32 * kC;                // 128
+constexpr int kMaxK = 64;
+
+__host__ __device__ constexpr int tile_rows(int warps) { return kR * warps; }
+__host__ __device__ constexpr int pad4(int v) { return (v + 3) & ~3; }
+// tile row pitch: columns read up to 124 + 3 + (pad4(kw) - 4) + 4
+__host__ __device__ constexpr int tile_pitch(int kw) { return kTileCols + pad4(kw) + 4; }
+
+template <bool kExact>
+__device__ __forceinline__ void mac4(float (&acc)[kC], float t, const float (&xw)[12], int off) {
+#pragma unroll
+  for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t, xw[c + off]);
+}
+
+// the filter travels in the launch parameters (16 KiB < the 32 KiB limit):
+// no per-call allocation or pageable copy
+struct BigTaps {
+  float f[kMaxK * kMaxK];
+};
+
+// kWarps = 8 (64-row tiles, less halo, more warps per SM) for big grids;
+// 4 when a single image would leave SMs idle
+template <bool kExact, int kWarps>
+__global__ void __launch_bounds__(32 * kWarps)
+    conv2d_big_kernel(const float* __restrict__ x, int h, int w,
+                      const __grid_constant__ BigTaps ft, int kh, int kw, float* __restrict__ y,
+                      int oh, int ow) {
+  constexpr int kTileRows = tile_rows(kWarps);
+  const float* f = ft.f;
+  extern __shared__ __align__(16) float smem[];
+  const int kwp = pad4(kw);
+  const int pitch = tile_pitch(kw);
+  float* taps = smem;                        // [kh][kwp], zero padded
+  float* tile = smem + kh * kwp;             // [kTileRows + kh - 1][pitch]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.y * kTileRows, c0 = blockIdx.x * kTileCols;
+  const float* xi = x + (int64_t)blockIdx.z * h * w;
+  float* yi = y + (int64_t)blockIdx.z * oh * ow;
+
+  for (int e = threadIdx.x; e < kh * kwp; e += blockDim.x) {
+    const int j = e / kwp, i = e - j * kwp;
+    taps[e] = i < kw ? f[j * kw + i] : 0.0f;
+  }
+  const int rows = kTileRows + kh - 1;
+  for (int rr = warp; rr < rows; rr += kWarps) {
+    const int gr = r0 + rr;
+    float* dst = tile + rr * pitch;
+    const float* src = xi + (int64_t)gr * w;
+    for (int cc = lane; cc < pitch; cc += 32) {
+      const int gc = c0 + cc;
+      dst[cc] = (gr < h && gc < w) ? __ldg(src + gc) : 0.0f;
+    }
+  }
+  __syncthreads();
+
+  float acc[kR][kC];
+#pragma unroll
+  for (int r = 0; r < kR; ++r)
+#pragma unroll
+    for (int c = 0; c < kC; ++c) acc[r][c] = 0.0f;
+
+  const int kfull = kw & ~3, krem = kw & 3;
+  const float* band = tile + warp * kR * pitch + kC * lane;
+  // One input row: ALL = every output row of the band is live (kR-1 <= q <=
+  // kh-1), so the r loop has no branches and the 8 tap loads can be hoisted
+  // ahead of the 128 FMAs; otherwise rows outside [rlo, rhi] are skipped.
+  auto row = [&](auto all_tag, int q) {
+    constexpr bool ALL = decltype(all_tag)::value;
+    const int rlo = max(0, q - kh + 1), rhi = min(kR - 1, q);
+    const float* xr = band + q * pitch;
+    const float* tq = taps + q * kwp;  // row j = q - r at tq - r * kwp
+    float xw[12];
+    *reinterpret_cast<float4*>(&xw[0]) = *reinterpret_cast<const float4*>(xr);
+    // one 4-tap block against the window starting at xw[base]
+    auto block = [&](int i0, auto base_tag) {
+      constexpr int B = decltype(base_tag)::value;
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        if (!ALL && (r < rlo || r > rhi)) continue;  // warp-uniform
+        const float4 t = *reinterpret_cast<const float4*>(tq - r * kwp + i0);
+        mac4<kExact>(acc[r], t.x, xw, B + 0);
+        mac4<kExact>(acc[r], t.y, xw, B + 1);
+        mac4<kExact>(acc[r], t.z, xw, B + 2);
+        mac4<kExact>(acc[r], t.w, xw, B + 3);
+      }
+    };
+    int i0 = 0;
+    // two blocks per trip: windows xw[0..7] then xw[4..11], then one shift
+    for (; i0 + 8 <= kfull; i0 += 8) {
+      *reinterpret_cast<float4*>(&xw[4]) = *reinterpret_cast<const float4*>(xr + i0 + 4);
+      *reinterpret_cast<float4*>(&xw[8]) = *reinterpret_cast<const float4*>(xr + i0 + 8);
+      block(i0, std::integral_constant<int, 0>{});
+      block(i0 + 4, std::integral_constant<int, 4>{});
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xw[v] = xw[v + 8];
+    }
+    if (i0 < kfull) {
+      *reinterpret_cast<float4*>(&xw[4]) = *reinterpret_cast<const float4*>(xr + i0 + 4);
+      block(i0, std::integral_constant<int, 0>{});
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xw[v] = xw[v + 4];
+      i0 += 4;
+    }
+    if (krem) {  // last partial block: only the real taps (a zero tap times
+                 // an inf/NaN input would poison the result)
+      *reinterpret_cast<float4*>(&xw[4]) = *reinterpret_cast<const float4*>(xr + i0 + 4);
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        if (!ALL && (r < rlo || r > rhi)) continue;
+        const float4 t = *reinterpret_cast<const float4*>(tq - r * kwp + i0);
+        mac4<kExact>(acc[r], t.x, xw, 0);
+        if (krem > 1) mac4<kExact>(acc[r], t.y, xw, 1);
+        if (krem > 2) mac4<kExact>(acc[r], t.z, xw, 2);
+      }
+    }
+  };
+  const int q_end = kR + kh - 1;
+  const int s_lo = kR - 1, s_hi = kh - 1;  // steady range (empty when kh < kR)
+  for (int q = 0; q < q_end; ++q) {
+    if (q >= s_lo && q <= s_hi) row(std::true_type{}, q);
+    else row(std::false_type{}, q);
+  }
+
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int gr = r0 + warp * kR + r;
+    if (gr >= oh) break;
+    float* yr = yi + (int64_t)gr * ow;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) {
+      const int gc = c0 + kC * lane + c;
+      if (gc < ow) yr[gc] = acc[r][c];
+    }
+  }
+}
+
+template <bool kExact, int kWarps>
+int launch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigTaps& taps,
+               int64_t kh, int64_t kw, float* y, cudaStream_t st) {
+  constexpr int kTileRows = tile_rows(kWarps);
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  const int64_t gx = (ow + kTileCols - 1) / kTileCols, gy = (oh + kTileRows - 1) / kTileRows;
+  if (gy > 65535) return 1;
+  const size_t smem =
+      ((size_t)kh * pad4((int)kw) + (size_t)(kTileRows + kh - 1) * tile_pitch((int)kw)) * 4;
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(conv2d_big_kernel<kExact, kWarps>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(((size_t)kMaxK * pad4(kMaxK) +
+                                        (size_t)(kTileRows + kMaxK - 1) * tile_pitch(kMaxK)) * 4)));
+    attr = true;
+  }
+  conv2d_big_kernel<kExact, kWarps>
+      <<<dim3((unsigned)gx, (unsigned)gy, (unsigned)batch), 32 * kWarps, smem, st>>>(
+          x, (int)h, (int)w, taps, (int)kh, (int)kw, y, (int)oh, (int)ow);
+  SC_LAUNCH_CHECK("conv2d_big_kernel");
+  return SC_OK;
+}
+
+}  // namespace
+
+// Returns SC_OK / an error if it ran, 1 if the shape is outside its range.
+int conv2d_big(const float* x, int64_t batch, int64_t h, int64_t w, const float* f_host,
+               int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st) {
+  if (kh > kMaxK || kw > kMaxK || batch > 65535 || h * w >= ((int64_t)1 << 31)) return 1;
+  static thread_local BigTaps taps;
+  std::copy(f_host, f_host + kh * kw, taps.f);
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  const int64_t ctas8 = batch * ((ow + kTileCols - 1) / kTileCols) * ((oh + 63) / 64);
+  const bool small = ctas8 < 2 * sm_count();
+  if (exact)
+    return small ? launch_big<true, 4>(x, batch, h, w, taps, kh, kw, y, st)
+                 : launch_big<true, 8>(x, batch, h, w, taps, kh, kw, y, st);
+  return small ? launch_big<false, 4>(x, batch, h, w, taps, kh, kw, y, st)
+               : launch_big<false, 8>(x, batch, h, w, taps, kh, kw, y, st);
+}
+
+}  // namespace sc

@@ -36,6 +36,36 @@ def test_shapes_exact_and_fast(kh, kw, h, w):
     assert sc.relative_error(fast, ref64) <= 1e-5 * max(1, kh * kw / 64)
 
 
+@pytest.mark.parametrize("kh,kw", [(51, 51), (64, 64), (2, 64), (64, 3), (21, 13), (37, 29)])
+@pytest.mark.parametrize("n,h,w", [(1, 200, 300), (3, 70, 133), (40, 64, 64)])
+def test_runtime_k_register_blocked_kernel(kh, kw, n, h, w):
+    # conv2d_big.cu: the paper's large-filter sweep (11..51) and up to 64 x 64,
+    # 4- and 8-warp tiles (small and large grids), exact and fast modes
+    if kh > h or kw > w:
+        pytest.skip("filter larger than input")
+    x = rand(kh * 1000 + kw + n, (n, h, w))
+    f = rand(kh + 77 * kw, (kh, kw))
+    xd = torch.from_numpy(x).cuda()
+    got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
+    assert np.array_equal(got, O.conv2d_batched(x, f))
+    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    ref64 = np.stack([O.oracle_conv2d(img, f) for img in x])
+    assert O.normwise_error(fast, ref64) <= O.north_star_tol(max(kh, kw))
+
+
+def test_runtime_k_nonfinite_inputs_match_reference():
+    # a zero-padded tap must never multiply an inf beyond the filter width
+    x = rand(5, (1, 90, 140))
+    x[0, 10, 60] = np.inf
+    x[0, 50, 20] = np.nan
+    f = rand(6, (19, 23))
+    got = sc.conv2d_reference(torch.from_numpy(x).cuda(), f, exact=True).cpu().numpy()
+    want = O.conv2d_batched(x, f)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    m = ~np.isnan(want)
+    assert np.array_equal(got[m], want[m])
+
+
 def test_config3_one_image_full_size_both_filters():
     rng = np.random.default_rng([0x5EED, 3])
     img = rng.uniform(0, 1, (1, 4096, 4096)).astype(np.float32)

@@ -153,3 +153,11 @@ def test_verify_suite_rejects_zero_trials():
     import paper_2310_05218_b200 as sc
     with pytest.raises(ValueError):
         sc.verify_suite(trials=0)
+
+
+@pytest.mark.parametrize("kw", [dict(reps=2), dict(warmup=-1), dict(filter_sizes=()),
+                                dict(filter_sizes=(512,)), dict(in_n=0)])
+def test_harness_config_validation(kw):
+    from paper_2310_05218_b200 import harness
+    with pytest.raises(ValueError):
+        harness.BenchConfig(**kw).validate()
