@@ -9,6 +9,7 @@
 // engines and the SMs.  Pinned host buffers are copied directly; pageable
 // ones go through a pinned staging ring filled by parallel host memcpy.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -29,7 +30,17 @@ namespace sc {
 namespace {
 
 constexpr int kSlots = 3;
-constexpr size_t kChunkBytes = size_t(64) << 20;
+constexpr size_t kMaxChunkBytes = size_t(64) << 20;
+
+// Chunk size: ~1/16 of the transfer (so the unoverlapped first H2D and last
+// D2H are short), between 8 and 64 MiB (SC_HOST_CHUNK_MB overrides).
+size_t chunk_bytes(size_t total) {
+  if (const char* e = getenv("SC_HOST_CHUNK_MB")) {
+    const long mb = atol(e);
+    if (mb >= 1 && mb <= 1024) return size_t(mb) << 20;
+  }
+  return std::min(kMaxChunkBytes, std::max(size_t(8) << 20, total / 16));
+}
 
 struct Slot {
   cudaStream_t stream = nullptr;
@@ -206,6 +217,7 @@ extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t
   const int64_t out_len = length - k + 1;
   std::vector<Chunk> chunks;
   const int64_t row_bytes = length * (int64_t)sizeof(float);
+  const size_t kChunkBytes = chunk_bytes((size_t)(batch * row_bytes));
   if (row_bytes <= (int64_t)kChunkBytes) {
     const int64_t rows = std::max<int64_t>(1, (int64_t)kChunkBytes / row_bytes);
     for (int64_t r = 0; r < batch; r += rows) {
@@ -248,6 +260,7 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
   std::vector<float> taps(f, f + kh * kw);  // outlives the lambdas below
   std::vector<Chunk> chunks;
   const int64_t img_bytes = h * w * (int64_t)sizeof(float);
+  const size_t kChunkBytes = chunk_bytes((size_t)(batch * img_bytes));
   if (img_bytes <= (int64_t)kChunkBytes) {
     const int64_t imgs = std::max<int64_t>(1, (int64_t)kChunkBytes / img_bytes);
     for (int64_t b = 0; b < batch; b += imgs) {
