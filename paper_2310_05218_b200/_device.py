@@ -39,17 +39,48 @@ def torch_mod():
     return torch
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
-    torch = torch_mod()
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2310_05218_b200 computes on a CUDA device (sm_100a); none is "
-                           "visible and there is no CPU fallback")
+    global _CUDA_OK
+    if not _CUDA_OK:
+        torch = torch_mod()
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2310_05218_b200 computes on a CUDA device (sm_100a); none "
+                               "is visible and there is no CPU fallback")
+        _CUDA_OK = True
     return _lib.load()
 
 
 def stream_of(t) -> int:
+    """Raw handle of the current stream on t's device (the call enqueues there)."""
     torch = torch_mod()
-    return torch.cuda.current_stream(t.device).cuda_stream
+    return torch._C._cuda_getCurrentRawStream(t.get_device())
+
+
+class on_device:
+    """Make t's device current for the C call; free when it already is
+    (the common case -- torch.cuda.device() costs microseconds per call)."""
+
+    __slots__ = ("dev", "prev")
+
+    def __init__(self, t):
+        self.dev = t.get_device()
+        self.prev = -1
+
+    def __enter__(self):
+        torch = torch_mod()
+        cur = torch._C._cuda_getDevice()
+        if cur != self.dev:
+            self.prev = cur
+            torch._C._cuda_setDevice(self.dev)
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev >= 0:
+            torch_mod()._C._cuda_setDevice(self.prev)
+        return False
 
 
 def pinned_empty(shape, dtype=np.float32) -> np.ndarray:

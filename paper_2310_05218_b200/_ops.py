@@ -9,8 +9,8 @@ from __future__ import annotations
 import numpy as np
 
 from . import _lib
-from ._device import (device_index, host_output, mode_flag, ptr, require_cuda, stream_of,
-                      to_device, torch_mod)
+from ._device import (device_index, host_output, mode_flag, on_device, ptr, require_cuda,
+                      stream_of, to_device, torch_mod)
 from .tensor import is_cuda_tensor
 
 
@@ -29,7 +29,7 @@ def conv2d(x, f: np.ndarray, exact=None, shape_error=None):
     if is_cuda_tensor(x):
         torch = torch_mod()
         y = torch.empty((b, oh, ow), dtype=torch.float32, device=x.device)
-        with torch.cuda.device(x.device):
+        with on_device(x):
             _lib.check(lib.sc_conv2d_f32(ptr(x), b, h, w, f.ctypes.data, kh, kw, mode, ptr(y),
                                          stream_of(x)), shape_error)
         return y
@@ -50,7 +50,7 @@ def conv2d_into(x, f: np.ndarray, y, exact=None):
     if tuple(y.shape[-2:]) != (h - kh + 1, w - kw + 1) or not y.is_contiguous():
         raise ValueError("conv2d_into: output view has the wrong shape or is not contiguous")
     f = _f32(f)
-    with torch.cuda.device(xb.device):
+    with on_device(xb):
         _lib.check(lib.sc_conv2d_f32(ptr(xb), b, h, w, f.ctypes.data, kh, kw, mode_flag(exact),
                                      ptr(y), stream_of(xb)))
     return y
@@ -66,7 +66,7 @@ def conv1d(x, f: np.ndarray, exact=None):
     if is_cuda_tensor(x):
         torch = torch_mod()
         y = torch.empty((b, n - k + 1), dtype=torch.float32, device=x.device)
-        with torch.cuda.device(x.device):
+        with on_device(x):
             _lib.check(lib.sc_conv1d_f32(ptr(x), b, n, f.ctypes.data, k, mode, ptr(y),
                                          stream_of(x)))
         return y
@@ -86,7 +86,7 @@ def conv2d_f64(x, f: np.ndarray):
     kh, kw = (int(d) for d in f.shape)
     f = np.ascontiguousarray(f, dtype=np.float64)
     y = torch.empty((b, h - kh + 1, w - kw + 1), dtype=torch.float64, device=xd.device)
-    with torch.cuda.device(xd.device):
+    with on_device(xd):
         _lib.check(lib.sc_conv2d_f64(ptr(xd), b, h, w, f.ctypes.data, kh, kw, ptr(y),
                                      stream_of(xd)))
     return y if on_dev else y.cpu().numpy()
@@ -100,7 +100,7 @@ def pool1d(op: int, x, k: int, exact=None):
     if is_cuda_tensor(x):
         torch = torch_mod()
         y = torch.empty((b, n - k + 1), dtype=torch.float32, device=x.device)
-        with torch.cuda.device(x.device):
+        with on_device(x):
             _lib.check(lib.sc_pool1d_f32(op, ptr(x), b, n, k, mode, ptr(y), stream_of(x)))
         return y
     y = host_output((b, n - k + 1))
@@ -123,7 +123,7 @@ def conv2d_nchw(x, wt, pad: int, exact=None):
     cout, cin2, kh, kw = (int(d) for d in wd.shape)
     oh, ow = h + 2 * pad - kh + 1, w + 2 * pad - kw + 1
     y = torch.empty((n, cout, oh, ow), dtype=torch.float32, device=xd.device)
-    with torch.cuda.device(xd.device):
+    with on_device(xd):
         _lib.check(lib.sc_conv2d_nchw_f32(ptr(xd), n, cin, h, w, ptr(wd), cout, kh, kw, pad,
                                           mode_flag(exact), ptr(y), stream_of(xd)))
     return y if on_dev else y.cpu().numpy()
@@ -138,7 +138,7 @@ def im2col(x, kh: int, kw: int):
     h, w = (int(d) for d in xd.shape)
     oh, ow = h - kh + 1, w - kw + 1
     cols = torch.empty((oh * ow, kh * kw), dtype=torch.float32, device=xd.device)
-    with torch.cuda.device(xd.device):
+    with on_device(xd):
         _lib.check(lib.sc_im2col_f32(ptr(xd), h, w, kh, kw, 0, oh, ptr(cols), stream_of(xd)))
     return cols if on_dev else cols.cpu().numpy()
 
@@ -152,7 +152,7 @@ def gemm(a, b):
     m, k = (int(d) for d in ad.shape)
     n = int(bd.shape[1])
     c = torch.empty((m, n), dtype=torch.float32, device=ad.device)
-    with torch.cuda.device(ad.device):
+    with on_device(ad):
         _lib.check(lib.sc_gemm_f32(ptr(ad), ptr(bd), ptr(c), m, n, k, stream_of(ad)))
     return c if on_dev else c.cpu().numpy()
 
@@ -172,7 +172,7 @@ def conv2d_im2col(x, f: np.ndarray, max_cols_bytes: int = 8 << 30):
     chunk = max(1, min(oh, max_cols_bytes // max(1, row_bytes)))
     cols = torch.empty((chunk * ow * kh * kw,), dtype=torch.float32, device=xd.device)
     y = torch.empty((oh, ow), dtype=torch.float32, device=xd.device)
-    with torch.cuda.device(xd.device):
+    with on_device(xd):
         _lib.check(lib.sc_conv2d_im2col_f32(ptr(xd), h, w, ptr(fd), kh, kw, ptr(cols), chunk,
                                             ptr(y), stream_of(xd)))
     return y if on_dev else y.cpu().numpy()

@@ -34,3 +34,23 @@ for _ in range(200):
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(14)
+
+# raw C-ABI call cost (no Python wrapper): pooling and conv on device pointers
+import ctypes  # noqa: E402
+from paper_2310_05218_b200 import _lib  # noqa: E402
+
+lib = _lib.load()
+y = torch.empty((256, 262144 - 15), device="cuda")
+stream = torch.cuda.current_stream().cuda_stream
+for name, call in (("sc_pool1d_f32 avg", lambda: lib.sc_pool1d_f32(1, x.data_ptr(), 256, 262144, 16, 0, y.data_ptr(), stream)),
+                   ("sc_pool1d_stages", lambda: lib.sc_pool1d_stages(1, 16)),
+                   ("sc_version", lambda: lib.sc_version())):
+    call()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(int(4e8))
+    t0 = time.perf_counter()
+    for _ in range(200):
+        call()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"{name}: {1e6 * (t1 - t0) / 200:.2f} us per raw call", flush=True)
