@@ -22,6 +22,8 @@
 #include "common.cuh"
 
 namespace sc {
+int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
+               int64_t cout, float* y, cudaStream_t st);
 int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
                int64_t cout, float* y, cudaStream_t st);
 namespace {
@@ -210,7 +212,14 @@ extern "C" int sc_conv2d_nchw_f32(const float* x, int64_t n, int64_t cin, int64_
       return e && e[0] == '1';
     }();
     if (!no_tc) {
-      const int rc = nchw3x3_tc(x, n, cin, h, w, wt, cout, y, st);
+      // weights-stationary (Cin <= 64) first, then the pixel-stationary form
+      static const bool no_ws = [] {
+        const char* e = getenv("SC_NCHW_NO_WS");
+        return e && e[0] == '1';
+      }();
+      int rc = no_ws ? 1 : nchw3x3_ws(x, n, cin, h, w, wt, cout, y, st);
+      if (rc != 1) return rc;
+      rc = nchw3x3_tc(x, n, cin, h, w, wt, cout, y, st);
       if (rc != 1) return rc;
     }
     const int tiles_w = (int)((w + kTW - 1) / kTW);

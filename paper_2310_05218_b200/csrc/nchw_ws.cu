@@ -1,0 +1,458 @@
+// Multi-channel NCHW 3x3 / pad 1 convolution, weights-stationary form, for
+// Cin <= 64 (BASELINE config 4: N16 Cin64 Cout64 112x112).
+//
+// The pixel-stationary kernel (nchw_tc.cu) streams the weights through shared
+// memory for every 128-pixel tile and copies the shifted pixel window into
+// TMEM for every tap; both cost shared-memory bandwidth, which is what bounds
+// it.  Here the roles flip:
+//   * A (M = 128 TMEM lanes) = the 64 output channels' weights, split
+//     w = w1 + w2 (bf16, as in nchw_tc.cu) and interleaved by lane
+//     (lane 2c = w1[c], lane 2c+1 = w2[c]), K = 9 taps x Cin in TMEM columns
+//     -- loaded ONCE per CTA and resident for all its rows (288 columns).
+//   * B (N = a row segment of Wt <= 112 pixels) = the input, split
+//     x = x1 + x2, read by the MMA straight from shared memory: each input
+//     row is converted once into a 128-byte-swizzled K-major [pixel][channel]
+//     slot (the canonical UMMA layout, 8-pixel core groups 1024 B apart), and
+//     the tap (dj, di) is just a descriptor at slot(r+dj) + (1+di) pixels.
+//   * D[m, p] += A x B for B = x1 and B = x2 (two issuer warps, one per
+//     product, same accumulator), so lanes 2c / 2c+1 hold w1.x and w2.x; the
+//     epilogue adds them with one shuffle: out = w1 x1 + w1 x2 + w2 x1 + w2 x2,
+//     error ~2^-16 per product as in nchw_tc.cu.
+//   * A CTA walks a segment of output rows of one image with a rolling window
+//     of four split input-row slots: row r needs input rows r-1, r, r+1, and
+//     row r+2 is converted while row r's MMAs run.  TMA brings each input row
+//     (+ 4-column halo boxes when the tile is not the whole width) into a
+//     2-deep fp32 staging ring.
+// Warp roles: 0 TMA producer; 1 TMEM owner + x1 issuer; 2-9 split; 10-13
+// epilogue (+ the one-time A load); 14 x2 issuer.  TMEM: D0 [0,112),
+// D1 [112,224), A [224,512).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace sc {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+namespace {
+using namespace tc;
+
+constexpr int kCo = 64;                       // output channels per CTA (M = 2 x 64)
+constexpr int kMaxCin = 64;
+constexpr int kMaxWt = 112;                   // pixels per row segment (N)
+constexpr int kDStride = 112;                 // TMEM columns per accumulator
+constexpr int kTmemA = 2 * kDStride;          // 224
+constexpr int kTmemCols = 512;
+constexpr int kSlots = 4;                     // split input-row ring
+constexpr int kStages = 2;                    // fp32 staging ring
+constexpr int kPixBytes = 128;                // one pixel's 64 bf16 channels
+constexpr int kXRegion = ((kMaxWt + 2) * kPixBytes + 1023) / 1024 * 1024;  // 15 KiB
+constexpr int kSlotBytes = 2 * kXRegion;                                     // x1 | x2
+constexpr int kHaloW = 4;
+constexpr int kStageBoxBytes = kMaxWt * kMaxCin * 4;                         // 28 KiB
+constexpr int kStageBytes = kStageBoxBytes + 2 * kHaloW * kMaxCin * 4;      // + halos
+constexpr size_t kSmem = 1024 + (size_t)kSlots * kSlotBytes + (size_t)kStages * kStageBytes;
+constexpr int kSplitWarps = 8, kEpiWarps = 4;
+constexpr int kIssuer2 = 2 + kSplitWarps + kEpiWarps;   // 14
+constexpr int kThreads = 32 * (kIssuer2 + 1);
+static_assert(kTmemA + 9 * kMaxCin / 2 <= kTmemCols, "TMEM budget");
+
+struct WsArgs {
+  int nb, cin, h, w, cout;
+  int wt, col_tiles, seg_rows, segs;   // row segments of seg_rows rows per (image, column tile)
+  int items_per_co, ctas_per_co;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    nchw3x3_ws_kernel(const __grid_constant__ CUtensorMap tmx,
+                      const __grid_constant__ CUtensorMap tmh, const uint32_t* __restrict__ apack,
+                      float* __restrict__ y, const WsArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t stage_full[kStages], stage_empty[kStages];
+  __shared__ __align__(8) uint64_t slot_full[kSlots], slot_free[kSlots];
+  __shared__ __align__(8) uint64_t d_full[2], d_empty[2];
+  __shared__ __align__(8) uint64_t a_ready;  // weights + zeroed D in TMEM
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float zero_word;
+  unsigned char* slots = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* stages = slots + kSlots * kSlotBytes;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cin = args.cin, h = args.h, w = args.w, wt = args.wt;
+  const int co_tile = blockIdx.x % (args.cout / kCo);
+  const int cta_in_co = blockIdx.x / (args.cout / kCo);
+  const int a_cols = 9 * cin / 2;
+  const int ksteps = cin / 16;
+  const uint32_t idesc = idesc_bf16(128, wt);
+
+  // item -> (image, column tile, first row, row count)
+  auto item_of = [&](int it, int& n, int& w0, int& r0, int& nr) {
+    const int seg = it % args.segs;
+    const int rest = it / args.segs;
+    w0 = (rest % args.col_tiles) * wt;
+    n = rest / args.col_tiles;
+    r0 = seg * args.seg_rows;
+    nr = min(args.seg_rows, h - r0);
+  };
+
+  if (threadIdx.x == 0) {
+    zero_word = 0.0f;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&stage_full[s], 1);
+      mbar_init(&stage_empty[s], kSplitWarps);
+    }
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&slot_full[s], kSplitWarps);
+      mbar_init(&slot_free[s], 2);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&d_full[s], 2);
+      mbar_init(&d_empty[s], kEpiWarps);
+    }
+    mbar_init(&a_ready, kSplitWarps + kEpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "n"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  if (warp >= 2 && warp < kIssuer2) {
+    // one-time setup by the 12 split + epilogue warps (3 per TMEM lane
+    // quarter q = warp % 4): zero both accumulators and load this CTA's
+    // weights (A) into TMEM.  Each warp owns a third of the A columns and
+    // issues all its 16-byte loads before storing (one L2 round trip).
+    const int q = warp & 3, third = (warp - 2) >> 2;  // 0..2
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+    if (third == 0) {
+      uint32_t z[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) z[i] = 0u;
+      for (int c = 0; c < kTmemA; c += 16) tmem_st16(lane_base + c, z);
+    }
+    const int chunks = a_cols / 16;                // 18 for Cin 64, 9 for Cin 32
+    const int per = (chunks + 2) / 3;
+    const int c_lo = third * per, c_hi = min(chunks, c_lo + per);
+    const uint4* arow = reinterpret_cast<const uint4*>(
+        apack + ((size_t)co_tile * 128 + 32 * q + lane) * a_cols);
+    uint4 buf[6][4];
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (c_lo + k < c_hi)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) buf[k][v] = __ldg(arow + (c_lo + k) * 4 + v);
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (c_lo + k < c_hi) tmem_st16(lane_base + kTmemA + (c_lo + k) * 16,
+                                     *reinterpret_cast<const uint32_t(*)[16]>(&buf[k][0]));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&a_ready);
+  }
+  // no CTA-wide barrier here: the producer and split warps start on the
+  // first input rows while the A load is in flight; only the issuers wait
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer: input rows
+    if (lane == 0) {
+      prefetch_tmap(&tmx);
+      prefetch_tmap(&tmh);
+      int s = 0;
+      for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
+        int n, w0, r0, nr;
+        item_of(it, n, w0, r0, nr);
+        // innermost TMA coordinates must be 16-byte aligned and in range, so
+        // halo columns come from 4-wide boxes, skipped at the image edge
+        const bool left = w0 > 0, right = w0 + wt < w;
+        const uint32_t bytes = (uint32_t)(wt * cin * 4) + (left ? kHaloW * cin * 4 : 0) +
+                               (right ? kHaloW * cin * 4 : 0);
+        for (int rho = r0 - 1; rho <= r0 + nr; ++rho, ++s) {
+          const int st = s % kStages;
+          if (s >= kStages) mbar_wait(&stage_empty[st], ((s / kStages) - 1) & 1);
+          unsigned char* dst = stages + st * kStageBytes;
+          mbar_arrive_expect_tx(&stage_full[st], bytes);
+          // rows -1 and h are outside the image: TMA zero-fills them (padding)
+          tma_load_4d(dst, &tmx, &stage_full[st], w0, rho, 0, n);
+          if (left)
+            tma_load_4d(dst + kStageBoxBytes, &tmh, &stage_full[st], w0 - kHaloW, rho, 0, n);
+          if (right)
+            tma_load_4d(dst + kStageBoxBytes + kHaloW * cin * 4, &tmh, &stage_full[st], w0 + wt,
+                        rho, 0, n);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == kIssuer2) {
+    // ------------------------------------------------ MMA issuers (x1 / x2)
+    if (lane == 0) {
+      const int part = warp == 1 ? 0 : 1;  // which split product this thread issues
+      mbar_wait(&a_ready, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      int s = 0, o = 0;
+      for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
+        int n, w0, r0, nr;
+        item_of(it, n, w0, r0, nr);
+        const int base = s;  // seq of input row r0 - 1
+        for (int rr = 0; rr < nr; ++rr, ++o) {
+          const int acc = o & 1;
+          if (o >= 2) mbar_wait(&d_empty[acc], ((o >> 1) - 1) & 1);
+#pragma unroll
+          for (int dj = 0; dj < 3; ++dj) {
+            const int sq = base + rr + dj;
+            mbar_wait(&slot_full[sq % kSlots], (sq / kSlots) & 1);
+          }
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tmem + acc * kDStride;
+#pragma unroll 1
+          for (int dj = 0; dj < 3; ++dj) {
+            const unsigned char* xs =
+                slots + ((base + rr + dj) % kSlots) * kSlotBytes + part * kXRegion;
+#pragma unroll
+            for (int di = 0; di < 3; ++di) {
+              const uint32_t a0 = tmem + kTmemA + (dj * 3 + di) * (cin / 2);
+              // tap column offset di: the window starts at slot pixel 1 + di.
+              // Measured on sm_100a (tools/ws_debug.py): with this 128-byte
+              // swizzled K-major B operand the MMA's first row is the one
+              // after the descriptor start, so the start is one pixel earlier.
+              const uint32_t b0 = smem_u32(xs) + di * kPixBytes;
+              for (int kk = 0; kk < ksteps; ++kk) {
+                const uint64_t db = make_desc(b0 + kk * 32, 16, 1024, 2);
+                mma_bf16_ts_rt(d, a0 + kk * 8, db, idesc, 1u);
+              }
+            }
+          }
+          umma_commit(&d_full[acc]);
+          // input row r-1 is not read by any later output row of this item
+          umma_commit(&slot_free[(base + rr) % kSlots]);
+          if (rr == nr - 1) {
+            umma_commit(&slot_free[(base + rr + 1) % kSlots]);
+            umma_commit(&slot_free[(base + rr + 2) % kSlots]);
+          }
+        }
+        s = base + nr + 2;
+      }
+    }
+  } else if (warp < 2 + kSplitWarps) {
+    // ------------------------------------------------ split warps
+    const int tid = threadIdx.x - 64;  // 0 .. 255
+    int s = 0;
+    for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
+      int n, w0, r0, nr;
+      item_of(it, n, w0, r0, nr);
+      const bool left = w0 > 0, right = w0 + wt < w;
+      for (int rho = r0 - 1; rho <= r0 + nr; ++rho, ++s) {
+        const int st = s % kStages, sl = s % kSlots;
+        mbar_wait(&stage_full[st], (s / kStages) & 1);
+        if (s >= kSlots) mbar_wait(&slot_free[sl], ((s / kSlots) - 1) & 1);
+        const unsigned char* src_box = stages + st * kStageBytes;
+        unsigned char* xs = slots + sl * kSlotBytes;
+        const int groups = cin / 8, pix = wt + 2;
+        // unit = (8-channel group g, slot pixel p): p = 0 is column w0-1,
+        // p = wt+1 is column w0+wt (halo or zero padding)
+        for (int u = tid; u < groups * pix; u += 32 * kSplitWarps) {
+          const int g = u / pix, p = u - g * pix;
+          const unsigned char* src;
+          int stride;
+          if (p >= 1 && p <= wt) {
+            src = src_box + (p - 1) * 4;
+            stride = wt * 4;
+          } else if (p == 0 ? left : right) {
+            src = src_box + kStageBoxBytes + (p == 0 ? 3 * 4 : kHaloW * cin * 4);
+            stride = kHaloW * 4;
+          } else {
+            src = reinterpret_cast<const unsigned char*>(&zero_word);
+            stride = 0;
+          }
+          src += 8 * g * stride;
+          uint4 w1, w2;
+          uint32_t* p1 = &w1.x;
+          uint32_t* p2 = &w2.x;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float f0 = *reinterpret_cast<const float*>(src + (2 * j) * stride);
+            const float f1 = *reinterpret_cast<const float*>(src + (2 * j + 1) * stride);
+            const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
+            p1[j] = a1;
+            p2[j] = pack_bf16x2(f0 - __uint_as_float(a1 << 16),
+                                f1 - __uint_as_float(a1 & 0xffff0000u));
+          }
+          // 128-byte swizzle: 16-byte chunk g of pixel p at chunk g ^ (p & 7)
+          const int off = p * kPixBytes + ((g ^ (p & 7)) << 4);
+          *reinterpret_cast<uint4*>(xs + off) = w1;
+          *reinterpret_cast<uint4*>(xs + kXRegion + off) = w2;
+        }
+        // generic-proxy smem writes -> read by the tensor core (async proxy)
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&slot_full[sl]);
+          mbar_arrive(&stage_empty[st]);
+        }
+      }
+    }
+  } else if (warp < kIssuer2) {
+    // ------------------------------------------------ epilogue (4 warps)
+    const int q = warp & 3;
+    const int m = 32 * q + lane;  // TMEM lane = 2 c + (0: w1 row, 1: w2 row)
+    const int c = m >> 1;
+    uint32_t z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0u;
+    const int64_t plane = (int64_t)h * w;
+    int o = 0;
+    for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
+      int n, w0, r0, nr;
+      item_of(it, n, w0, r0, nr);
+      float* ybase = y + ((int64_t)n * args.cout + co_tile * kCo + c) * plane + w0;
+      for (int rr = 0; rr < nr; ++rr, ++o) {
+        const int acc = o & 1;
+        mbar_wait_sleep(&d_full[acc], (o >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + acc * kDStride;
+        float* yr = ybase + (int64_t)(r0 + rr) * w;
+        for (int p0 = 0; p0 < wt; p0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(taddr + p0, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          tmem_st16(taddr + p0, z);  // re-arm the accumulator
+          float sum[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            sum[i] = __uint_as_float(v[i]) + __shfl_xor_sync(0xffffffffu, __uint_as_float(v[i]), 1);
+          // lanes 2c and 2c+1 both hold channel c: each stores half the pixels
+          const bool odd = lane & 1;
+          float hv[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) hv[i] = odd ? sum[8 + i] : sum[i];
+          float* dst = yr + p0 + (odd ? 8 : 0);
+          if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = hv[i];
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_empty[acc]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// w[co][ci][3][3] -> A rows per 64-channel tile: row 2c = bf16 w1, row 2c+1 =
+// bf16 w2 = bf16(w - w1); column k2 packs K elements (2 k2, 2 k2 + 1) with
+// K = tap * Cin + ci (low half = even element)
+__global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __restrict__ apack,
+                                    int cin, int cout) {
+  const int a_cols = 9 * cin / 2;
+  const int total = (cout / kCo) * 128 * a_cols;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int k2 = e % a_cols;
+    const int m = (e / a_cols) % 128;
+    const int tile = e / (a_cols * 128);
+    const int co = tile * kCo + (m >> 1), hlf = m & 1;
+    uint32_t packed = 0;
+    for (int t = 0; t < 2; ++t) {
+      const int kidx = 2 * k2 + t;
+      const int tap = kidx / cin, ci = kidx % cin;
+      const float v = wt[((int64_t)co * cin + ci) * 9 + tap];
+      const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
+      const __nv_bfloat16 part = hlf ? __float2bfloat16_rn(v - __bfloat162float(v1)) : v1;
+      packed |= (uint32_t)__bfloat16_as_ushort(part) << (16 * t);
+    }
+    apack[e] = packed;
+  }
+}
+
+int pick_tile_width(int64_t w) {
+  for (int t = kMaxWt / 16; t >= 1; --t)
+    if ((w / 16) % t == 0) return 16 * t;
+  return 16;
+}
+
+}  // namespace
+
+// Returns SC_OK / an error if it ran, 1 if the shape is outside its range.
+int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
+               int64_t cout, float* y, cudaStream_t st) {
+  if (cin > kMaxCin || cin % 32 != 0 || cout % kCo != 0 || w % 16 != 0 ||
+      (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
+      nb * cout * h * w >= ((int64_t)1 << 31) || h < 1)
+    return 1;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int tw = pick_tile_width(w);
+  WsArgs a;
+  a.nb = (int)nb, a.cin = (int)cin, a.h = (int)h, a.w = (int)w, a.cout = (int)cout;
+  a.wt = tw;
+  a.col_tiles = (int)(w / tw);
+  const int co_tiles = (int)(cout / kCo);
+  const int sms = sm_count();
+  a.ctas_per_co = std::max(1, sms / co_tiles);
+  const int64_t rows_total = nb * a.col_tiles * h;
+  a.seg_rows = (int)std::max<int64_t>(4, (rows_total + a.ctas_per_co - 1) / a.ctas_per_co);
+  a.seg_rows = std::min<int>(a.seg_rows, (int)h);
+  a.segs = (int)((h + a.seg_rows - 1) / a.seg_rows);
+  a.items_per_co = (int)(nb * a.col_tiles * a.segs);
+  a.ctas_per_co = std::min(a.ctas_per_co, a.items_per_co);
+
+  cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)cin, (cuuint64_t)nb};
+  cuuint64_t strides[3] = {(cuuint64_t)(w * 4), (cuuint64_t)(h * w * 4),
+                           (cuuint64_t)(cin * h * w * 4)};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMap mx, mh;
+  {
+    cuuint32_t box[4] = {(cuuint32_t)tw, 1, (cuuint32_t)cin, 1};
+    CUresult r = enc(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw ws: x tensor map failed");
+  }
+  {
+    cuuint32_t box[4] = {kHaloW, 1, (cuuint32_t)cin, 1};
+    CUresult r = enc(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw ws: halo tensor map failed");
+  }
+  uint32_t* apack = nullptr;
+  const size_t abytes = (size_t)co_tiles * 128 * (9 * cin / 2) * sizeof(uint32_t);
+  SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&apack), abytes, st));
+  pack_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (int64_t)(abytes / 4 + 255) / 256), 256,
+                        0, st>>>(wt, apack, (int)cin, (int)cout);
+  SC_LAUNCH_CHECK("pack_weights_kernel");
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(nchw3x3_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kSmem));
+    attr = true;
+  }
+  const unsigned grid = (unsigned)(a.ctas_per_co * co_tiles);
+  nchw3x3_ws_kernel<<<grid, kThreads, kSmem, st>>>(mx, mh, apack, y, a);
+  SC_LAUNCH_CHECK("nchw3x3_ws_kernel");
+  SC_CUDA(cudaFreeAsync(apack, st));
+  return SC_OK;
+}
+
+}  // namespace sc

@@ -16,7 +16,7 @@ __device__ __forceinline__ void mma(uint32_t d, uint32_t a, uint64_t b, uint32_t
                ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(1u) : "memory");
 }
 
-__global__ void k(int n0, int n1, int iters, long long* out, int fill) {
+__global__ void k(int n0, int n1, int iters, long long* out, int fill, int boff) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* base = sm + ((1024 - (su32(sm) & 1023)) & 1023);
   __shared__ uint32_t tb;
@@ -57,7 +57,7 @@ __global__ void k(int n0, int n1, int iters, long long* out, int fill) {
   const int n = warp == 0 ? n0 : n1;
   if (warp < 2 && lane == 0 && n > 0) {
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
-    const uint64_t db = mk(su32(base));
+    const uint64_t db = mk(su32(base) + boff);
     const uint32_t a0 = tb + 256 + warp * 32;
     long long t0 = clock64();
     for (int i = 0; i < iters; i += 4) {
@@ -81,8 +81,9 @@ int main(int argc, char** argv) {
   d[0] = d[1] = 0;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 20000);
   const int fill = argc > 4 ? atoi(argv[4]) : 0;
-  k<<<148, 128, 20000>>>(n0, n1, iters, d, fill);
+  const int boff = argc > 5 ? atoi(argv[5]) : 0;
+  k<<<148, 128, 20000>>>(n0, n1, iters, d, fill, boff);
   cudaError_t e = cudaDeviceSynchronize();
-  printf("fill=%d n0=%d n1=%d (%s): warp0 %.1f warp1 %.1f cycles per k-step\n", fill, n0, n1, cudaGetErrorString(e),
+  printf("boff=%d fill=%d n0=%d n1=%d (%s): warp0 %.1f warp1 %.1f cycles per k-step\n", argc > 5 ? atoi(argv[5]) : 0, fill, n0, n1, cudaGetErrorString(e),
          (double)d[0] / iters, (double)d[1] / iters);
 }

@@ -13,7 +13,7 @@ from oracle import slideconv_oracle as O  # noqa: E402
 rng = np.random.default_rng(4)
 for_shapes = not os.environ.get("TC_ONLY_TIME")
 for (n, cin, cout, h, w) in [(1, 32, 64, 8, 16), (1, 64, 64, 16, 32), (2, 64, 64, 112, 112),
-                             (1, 32, 128, 20, 24), (3, 64, 128, 13, 48), (1, 128, 64, 9, 32), (1, 64, 64, 112, 112),
+                             (1, 32, 128, 20, 24), (3, 64, 128, 13, 48), (1, 128, 64, 9, 32), (1, 64, 64, 112, 112), (2, 32, 64, 30, 224),
                              (2, 32, 192, 17, 160)]:
     x = rng.standard_normal((n, cin, h, w), dtype=np.float32)
     wt = (rng.standard_normal((cout, cin, 3, 3), dtype=np.float32) / np.float32(np.sqrt(9 * cin))).astype(np.float32)
