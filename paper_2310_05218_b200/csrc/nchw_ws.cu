@@ -6,18 +6,21 @@
 // TMEM for every tap; both cost shared-memory bandwidth, which is what bounds
 // it.  Here the roles flip:
 //   * A (M = 128 TMEM lanes) = the 64 output channels' weights, split
-//     w = w1 + w2 (bf16, as in nchw_tc.cu) and interleaved by lane
-//     (lane 2c = w1[c], lane 2c+1 = w2[c]), K = 9 taps x Cin in TMEM columns
-//     -- loaded ONCE per CTA and resident for all its rows (288 columns).
+//     w = w1 + w2 (bf16, as in nchw_tc.cu): in lane quarter q, lanes 0-15
+//     hold w1 of channels 16q..16q+15 and lanes 16-31 their w2; K = 9 taps x
+//     Cin in TMEM columns -- loaded ONCE per CTA and resident for all its rows
+//     (288 columns).
 //   * B (N = a row segment of Wt <= 112 pixels) = the input, split
 //     x = x1 + x2, read by the MMA straight from shared memory: each input
 //     row is converted once into a 128-byte-swizzled K-major [pixel][channel]
 //     slot (the canonical UMMA layout, 8-pixel core groups 1024 B apart), and
 //     the tap (dj, di) is just a descriptor at slot(r+dj) + (1+di) pixels.
-//   * D[m, p] += A x B for B = x1 and B = x2 (two issuer warps, one per
-//     product, same accumulator), so lanes 2c / 2c+1 hold w1.x and w2.x; the
-//     epilogue adds them with one shuffle: out = w1 x1 + w1 x2 + w2 x1 + w2 x2,
-//     error ~2^-16 per product as in nchw_tc.cu.
+//   * Issuer 1: D += A x x1 with M = 128 (w1 x1 and w2 x1).  Issuer 2:
+//     D += A x x2 with M = 64, which reads / writes only lanes 0-15 of every
+//     quarter (measured, tools/micro/umma_m64_probe.cu) = the w1 rows: w1 x2
+//     at half the tensor time of an M = 128 product, and no wasted w2 x2.
+//     The epilogue adds lanes j and j + 16 with one shuffle:
+//     out = w1 x1 + w1 x2 + w2 x1, error ~2^-16 per product as in nchw_tc.cu.
 //   * A CTA walks a segment of output rows of one image with a rolling window
 //     of four split input-row slots: row r needs input rows r-1, r, r+1, and
 //     row r+2 is converted while row r's MMAs run.  TMA brings each input row
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cta_in_co = blockIdx.x / (args.cout / kCo);
   const int a_cols = 9 * cin / 2;
   const int ksteps = cin / 16;
-  const uint32_t idesc = idesc_bf16(128, wt);
+  const uint32_t idesc128 = idesc_bf16(128, wt), idesc64 = idesc_bf16(64, wt);
 
   // item -> (image, column tile, first row, row count)
   auto item_of = [&](int it, int& n, int& w0, int& r0, int& nr) {
@@ -196,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ MMA issuers (x1 / x2)
     if (lane == 0) {
       const int part = warp == 1 ? 0 : 1;  // which split product this thread issues
+      const uint32_t idesc = part ? idesc64 : idesc128;
       mbar_wait(&a_ready, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       int s = 0, o = 0;
@@ -303,8 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp < kIssuer2) {
     // ------------------------------------------------ epilogue (4 warps)
     const int q = warp & 3;
-    const int m = 32 * q + lane;  // TMEM lane = 2 c + (0: w1 row, 1: w2 row)
-    const int c = m >> 1;
+    const int c = 16 * q + (lane & 15);  // lanes j, j + 16: w1 / w2 rows of channel c
     uint32_t z[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) z[i] = 0u;
@@ -328,9 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           float sum[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            sum[i] = __uint_as_float(v[i]) + __shfl_xor_sync(0xffffffffu, __uint_as_float(v[i]), 1);
-          // lanes 2c and 2c+1 both hold channel c: each stores half the pixels
-          const bool odd = lane & 1;
+            sum[i] = __uint_as_float(v[i]) + __shfl_xor_sync(0xffffffffu, __uint_as_float(v[i]), 16);
+          // lanes j and j + 16 both hold channel c: each stores half the pixels
+          const bool odd = lane >= 16;
           float hv[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) hv[i] = odd ? sum[8 + i] : sum[i];
@@ -360,9 +363,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// w[co][ci][3][3] -> A rows per 64-channel tile: row 2c = bf16 w1, row 2c+1 =
-// bf16 w2 = bf16(w - w1); column k2 packs K elements (2 k2, 2 k2 + 1) with
-// K = tap * Cin + ci (low half = even element)
+// w[co][ci][3][3] -> A rows per 64-channel tile: row 32q + j holds channel
+// 16q + (j & 15), bf16 w1 for j < 16 and bf16 w2 = bf16(w - w1) for j >= 16;
+// column k2 packs K elements (2 k2, 2 k2 + 1) with K = tap * Cin + ci (low
+// half = even element)
 __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __restrict__ apack,
                                     int cin, int cout) {
   const int a_cols = 9 * cin / 2;
@@ -371,7 +375,7 @@ __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __re
     const int k2 = e % a_cols;
     const int m = (e / a_cols) % 128;
     const int tile = e / (a_cols * 128);
-    const int co = tile * kCo + (m >> 1), hlf = m & 1;
+    const int co = tile * kCo + 16 * (m >> 5) + (m & 15), hlf = (m >> 4) & 1;
     uint32_t packed = 0;
     for (int t = 0; t < 2; ++t) {
       const int kidx = 2 * k2 + t;
