@@ -160,11 +160,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // off with __nanosleep between probes so the spin loop does not steal issue
 // slots from the FMA / tensor warps sharing the SM sub-partition (ncu on the
 // 7x7 conv: 490 M SYNCS + 514 M BRA + 486 M YIELD vs 828 M FFMA2 executed).
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t ns = 32;
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity,
+                                                uint32_t ns0 = 32, uint32_t ns_max = 512) {
+  uint32_t ns = ns0;
   while (!mbar_try_wait(bar, parity)) {
     __nanosleep(ns);
-    ns = ns < 512 ? ns * 2 : 512;
+    ns = ns < ns_max ? ns * 2 : ns_max;
   }
 }
 
