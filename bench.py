@@ -321,7 +321,7 @@ def per_config(torch, sc, hbm_peak, args, traffic):
     except (OSError, KeyError, ValueError):
         bf16_peak, bf16_src = 2250.0, "fallback nominal dense bf16 (B200_PROFILING.md)"
     # nchw3x3_tc_kernel runs 3 bf16 products per useful MAC (x1 w1, x1 w2, x2 w1)
-    tensor = {"kernel": "nchw3x3_tc_kernel (tcgen05 kind::f16, bf16x3 split)",
+    tensor = {"kernel": "nchw3x3_ws_kernel (tcgen05 kind::f16, bf16x3 split, weights in TMEM)",
               "executed_bf16_tflops": round(3 * fl / t / 1e12, 1), "peak": bf16_peak,
               "peak_source": bf16_src, "frac": round(3 * fl / t / 1e12 / bf16_peak, 4),
               "fp32_equiv_tflops": round(fl / t / 1e12, 1)}
