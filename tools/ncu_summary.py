@@ -5,7 +5,7 @@ import subprocess
 import sys
 
 KEYS = [
-    ("gpu__time_duration.sum", "us", 1e-3),
+    ("gpu__time_duration.sum", "us", None),  # unit-aware (ncu reports ns / us / ms)
     ("dram__bytes_read.sum", "rdMB", 1.0),
     ("dram__bytes_write.sum", "wrMB", 1.0),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1),
@@ -52,7 +52,12 @@ def main(path, filt="_kernel"):
             if key in hdr:
                 v = r[hdr.index(key)]
                 try:
-                    f = float(v.replace(",", "")) * scale
+                    f = float(v.replace(",", ""))
+                    if scale is None:
+                        u = units[hdr.index(key)]
+                        f *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
+                    else:
+                        f *= scale
                     vals.append(f"{short}={f:.4g}")
                 except ValueError:
                     pass
