@@ -6,8 +6,8 @@ import sys
 
 KEYS = [
     ("gpu__time_duration.sum", "us", None),  # unit-aware (ncu reports ns / us / ms)
-    ("dram__bytes_read.sum", "rdMB", 1.0),
-    ("dram__bytes_write.sum", "wrMB", 1.0),
+    ("dram__bytes_read.sum", "rdMB", None),
+    ("dram__bytes_write.sum", "wrMB", None),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%", 1),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue%", 1),
@@ -55,7 +55,9 @@ def main(path, filt="_kernel"):
                     f = float(v.replace(",", ""))
                     if scale is None:
                         u = units[hdr.index(key)]
-                        f *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u, 1.0)
+                        f *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                              "msecond": 1e3, "s": 1e6, "second": 1e6,
+                              "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
                     else:
                         f *= scale
                     vals.append(f"{short}={f:.4g}")
