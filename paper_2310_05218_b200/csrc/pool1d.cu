@@ -18,6 +18,8 @@
 //    and for very wide windows.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sc {
@@ -426,10 +428,15 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
     if (rc != 1) return rc;
   }
   // wide windows: O(1) per output -- prefix sums (fast mode) or the exact
-  // block-decomposition max.  For 64 < k <= 256 the striped register
-  // doubling is still the faster exact max on B200 (k = 255: 132 us vs
-  // 232 us, tools/pool_sweep.py), so the block kernel serves k > 256.
-  if ((kOp == SC_POOL_MAX && k > 256) || (kOp != SC_POOL_MAX && !exact)) {
+  // van Herk / Gil-Werman max.  For 64 < k <= 256 the striped register
+  // doubling is still the faster exact max on B200 (k = 255: 130 us vs
+  // 179 us, tools/pool_sweep.py), so the vHGW kernel serves k > 256
+  // (SC_POOL_MAX_WIDE_MIN moves the threshold).
+  static const int max_wide_min = [] {
+    const char* e = getenv("SC_POOL_MAX_WIDE_MIN");
+    return e ? atoi(e) : 257;
+  }();
+  if ((kOp == SC_POOL_MAX && k >= max_wide_min) || (kOp != SC_POOL_MAX && !exact)) {
     const int rc = pool1d_wide(kOp, x, batch, length, k, y, st);
     if (rc != 1) return rc;
   }

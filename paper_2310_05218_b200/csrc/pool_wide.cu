@@ -14,10 +14,10 @@
 //    y(i) = E(i + k) - E(i) read lane-striped -> coalesced stores.  Anchoring
 //    every 4,096 samples bounds |E| and the cancellation error (measured
 //    ~1e-7 normwise vs the reference for N(0,1); tolerance 1e-5 k).
-//  * MAX (always bit-exact): van Herk / Gil-Werman -- blocks of k samples
-//    anchored at the tile start; P = running max from the block start, S =
-//    running max to the block end (segmented lane / warp / CTA scans), then
-//    y(i) = max(S(i), P(i + k - 1)).  Every combine takes (earlier, later)
+//  * MAX (always bit-exact): van Herk / Gil-Werman -- segments of k samples
+//    anchored at the tile start; P = running max from the segment start,
+//    S = running max to the segment end (segmented lane / warp / CTA scans),
+//    then y(i) = max(S(i), P(i + k - 1)).  Every combine takes (earlier, later)
 //    operands, so with np.maximum's tie rule the result is the rightmost
 //    maximal element, exactly what the reference's doubling order yields.
 //    The fast pass uses max.NaN; if any output of the tile is zero (the only
@@ -72,27 +72,88 @@ __device__ __forceinline__ float mx(float a, float b) {  // a earlier, b later
   else return max_nan(a, b);
 }
 
-constexpr int kBlocks = kWarps * 32;   // 16-sample blocks per tile (one per lane)
-constexpr int kLevels = 8;              // sparse-table levels over block maxima
-
-// Block-decomposition max over a tile (exact order): each lane's 16 samples
-// form a block with lane-local prefix P and suffix S maxima; block maxima get
-// a sparse table L[t][b] = max(blocks b .. b + 2^t - 1).  A window [i, e]
-// (e = i + k - 1, k > 16) is S(i) ++ full blocks ++ P(e), the full blocks
-// covered by two overlapping sparse-table entries.  Every combine is
-// (earlier, later), so ties resolve to the rightmost maximal element like the
-// reference's doubling with np.maximum.
+// van Herk / Gil-Werman max over a tile: segments of k samples anchored at
+// the tile start (k > kT, so a lane's 16 samples hold at most one segment
+// start jb and at most one segment end e).  P(p) = running max from the
+// segment start, S(p) = running max to the segment end, as segmented scans:
+// lane-local, then across lanes (shuffles) and warps (shared memory).  Every
+// combine is mx(earlier, later), so ties keep the rightmost maximal element.
+// Writes P and S to shared memory (swizzled like the tile).
 template <bool kExact>
-__device__ __forceinline__ void blocks_tile(const float (&s)[kT], int p0, int levels, int warp,
-                                            int lane, unsigned char* arr_p, unsigned char* arr_s,
-                                            float* table) {
+__device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int jb, int e, int warp,
+                                          int lane, unsigned char* arr_p, unsigned char* arr_s,
+                                          float* wv, int* wf) {
+  const float kId = -__int_as_float(0x7f800000);  // -inf: identity of max
   float P[kT], S[kT];
+  // ---- prefix, left to right; reset at the segment start jb
   P[0] = s[0];
 #pragma unroll
-  for (int j = 1; j < kT; ++j) P[j] = mx<kExact>(P[j - 1], s[j]);
+  for (int j = 1; j < kT; ++j) P[j] = (j == jb) ? s[j] : mx<kExact>(P[j - 1], s[j]);
+  {
+    float v = P[kT - 1];
+    int f = jb < kT;  // a segment starts inside this lane
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float pv = __shfl_up_sync(0xffffffffu, v, d);
+      const int pf = __shfl_up_sync(0xffffffffu, f, d);
+      if (lane >= d) {
+        if (!f) v = mx<kExact>(pv, v);
+        f |= pf;
+      }
+    }
+    if (lane == 31) {
+      wv[warp] = v;
+      wf[warp] = f;
+    }
+    float cv = __shfl_up_sync(0xffffffffu, v, 1);
+    int cf = __shfl_up_sync(0xffffffffu, f, 1);
+    bar_consumers();
+    float wc = kId;  // carry from the warps to the left
+    for (int w = 0; w < warp; ++w) wc = wf[w] ? wv[w] : mx<kExact>(wc, wv[w]);
+    if (lane == 0) {
+      cv = wc;
+    } else if (!cf) {
+      cv = mx<kExact>(wc, cv);
+    }
+#pragma unroll
+    for (int j = 0; j < kT; ++j)
+      if (j < jb) P[j] = mx<kExact>(cv, P[j]);
+  }
+  // ---- suffix, right to left; reset at the segment end e
   S[kT - 1] = s[kT - 1];
 #pragma unroll
-  for (int j = kT - 2; j >= 0; --j) S[j] = mx<kExact>(s[j], S[j + 1]);
+  for (int j = kT - 2; j >= 0; --j) S[j] = (j == e) ? s[j] : mx<kExact>(s[j], S[j + 1]);
+  bar_consumers();  // wv / wf reuse
+  {
+    float v = S[0];
+    int f = e >= 0;  // a segment ends inside this lane
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const float pv = __shfl_down_sync(0xffffffffu, v, d);
+      const int pf = __shfl_down_sync(0xffffffffu, f, d);
+      if (lane + d < 32) {
+        if (!f) v = mx<kExact>(v, pv);
+        f |= pf;
+      }
+    }
+    if (lane == 0) {
+      wv[warp] = v;
+      wf[warp] = f;
+    }
+    float cv = __shfl_down_sync(0xffffffffu, v, 1);
+    int cf = __shfl_down_sync(0xffffffffu, f, 1);
+    bar_consumers();
+    float wc = kId;  // carry from the warps to the right
+    for (int w = kWarps - 1; w > warp; --w) wc = wf[w] ? wv[w] : mx<kExact>(wv[w], wc);
+    if (lane == 31) {
+      cv = wc;
+    } else if (!cf) {
+      cv = mx<kExact>(cv, wc);
+    }
+#pragma unroll
+    for (int j = 0; j < kT; ++j)
+      if (j > e) S[j] = mx<kExact>(S[j], cv);
+  }
 #pragma unroll
   for (int q = 0; q < kT / 4; ++q) {
     *reinterpret_cast<float4*>(arr_p + swz(p0 + 4 * q)) =
@@ -100,30 +161,7 @@ __device__ __forceinline__ void blocks_tile(const float (&s)[kT], int p0, int le
     *reinterpret_cast<float4*>(arr_s + swz(p0 + 4 * q)) =
         make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
   }
-  const int blk = warp * 32 + lane;
-  table[blk] = P[kT - 1];
   bar_consumers();
-  for (int t = 1; t < levels; ++t) {
-    const int half = 1 << (t - 1);
-    const float* lo = table + (t - 1) * kBlocks;
-    if (blk + half < kBlocks) table[t * kBlocks + blk] = mx<kExact>(lo[blk], lo[blk + half]);
-    bar_consumers();
-  }
-}
-
-template <bool kExact>
-__device__ __forceinline__ float window_max(int i, int k, const unsigned char* arr_p,
-                                            const unsigned char* arr_s, const float* table) {
-  const int e = i + k - 1;
-  const int b0 = i >> 4, b1 = e >> 4;
-  const int c = b1 - b0 - 1;  // full blocks strictly inside the window
-  float y = *reinterpret_cast<const float*>(arr_s + swz(i));
-  if (c > 0) {
-    const int t = 31 - __clz(c);
-    const float* lt = table + t * kBlocks;
-    y = mx<kExact>(y, mx<kExact>(lt[b0 + 1], lt[b1 - (1 << t)]));
-  }
-  return mx<kExact>(y, *reinterpret_cast<const float*>(arr_p + swz(e)));
 }
 
 template <int kOp>
@@ -135,7 +173,6 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
   __shared__ __align__(8) uint64_t full_bar[kNbuf];
   __shared__ __align__(8) uint64_t empty_bar[kNbuf];
   __shared__ float wv[kWarps];
-  __shared__ float table[kLevels * kBlocks];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* arr_a = base + kNbuf * kBufBytes;   // E (sum) or P (max)
   unsigned char* arr_b = arr_a + kArrBytes;         // S (max)
@@ -171,12 +208,15 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
   }
 
   const int p0 = warp * (32 * kT) + kT * lane;
-  // sparse-table levels needed: the widest run of full blocks is (k+14)/16 - 1
-  int levels = 1;
-  while ((1 << levels) <= (k + 14) / 16) ++levels;
-  levels = min(levels, kLevels);
   const float fk = (float)k;
   const float inv_k = 1.0f / fk;
+  // vHGW segment start / end inside this lane (same for every tile)
+  const int first_start = (p0 + k - 1) / k * k;  // first multiple of k >= p0
+  const int jb = first_start - p0 < kT ? first_start - p0 : kT;
+  const int end_pos = (p0 / k + 1) * k - 1;      // end of p0's segment
+  const int e = end_pos - p0 < kT ? end_pos - p0 : -1;
+  __shared__ float seg_v[kWarps];
+  __shared__ int seg_f[kWarps];
   int it = 0;
   for (unsigned t = t_begin; t < nt; ++t, ++it) {
     const int b = it % kNbuf;
@@ -208,23 +248,26 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
       release();  // the window stays in registers for a possible exact redo
       // fast pass (max.NaN), stored at once; if any output of the tile is zero
       // (a +0/-0 tie may resolve differently) the tile is redone exactly
-      blocks_tile<false>(s, p0, levels, warp, lane, arr_a, arr_b, table);
+      vhgw_tile<false>(s, p0, jb, e, warp, lane, arr_a, arr_b, seg_v, seg_f);
       bool zero = false;
 #pragma unroll
       for (int m = 0; m < kT; ++m) {
         const int i = warp * (32 * kT) + 32 * m + lane;
         if (i < lim) {
-          const float o = window_max<false>(i, k, arr_a, arr_b, table);
+          const float o = mx<false>(*reinterpret_cast<const float*>(arr_b + swz(i)),
+                                    *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
           zero |= (o == 0.0f);
           yr[i] = o;
         }
       }
       if (bar_consumers_or(zero)) {
-        blocks_tile<true>(s, p0, levels, warp, lane, arr_a, arr_b, table);
+        vhgw_tile<true>(s, p0, jb, e, warp, lane, arr_a, arr_b, seg_v, seg_f);
 #pragma unroll
         for (int m = 0; m < kT; ++m) {
           const int i = warp * (32 * kT) + 32 * m + lane;
-          if (i < lim) yr[i] = window_max<true>(i, k, arr_a, arr_b, table);
+          if (i < lim)
+            yr[i] = mx<true>(*reinterpret_cast<const float*>(arr_b + swz(i)),
+                             *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
         }
         bar_consumers();
       }
