@@ -34,6 +34,10 @@ def test_config4_exact_matches_composed_oracle():
                                                  (2, 64, 64, 16, 32, 3, 1), (1, 64, 128, 21, 48, 3, 1),
                                                  (3, 128, 64, 9, 16, 3, 1), (1, 64, 64, 1, 16, 3, 1),
                                                  (2, 192, 128, 7, 48, 3, 1),
+                                                 # weights-stationary (Cin 32 / 64): several
+                                                 # column tiles with halos, 3 co-tiles, H = 1, 2
+                                                 (2, 32, 64, 30, 224, 3, 1), (2, 32, 192, 17, 160, 3, 1),
+                                                 (1, 64, 64, 2, 48, 3, 1), (3, 64, 128, 5, 96, 3, 1),
                                                  # Cin % 64 != 0 -> CUDA-core kernel
                                                  (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1)])
 def test_nchw_shapes(n, cin, cout, h, w, k, p):
