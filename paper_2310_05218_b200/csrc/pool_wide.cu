@@ -85,81 +85,68 @@ __device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int jb, 
                                           float* wv, int* wf) {
   const float kId = -__int_as_float(0x7f800000);  // -inf: identity of max
   float P[kT], S[kT];
-  // ---- prefix, left to right; reset at the segment start jb
+  // ---- lane-local segmented scans: prefix (reset at the segment start jb),
+  // suffix (reset at the segment end e)
   P[0] = s[0];
 #pragma unroll
   for (int j = 1; j < kT; ++j) P[j] = (j == jb) ? s[j] : mx<kExact>(P[j - 1], s[j]);
-  {
-    float v = P[kT - 1];
-    int f = jb < kT;  // a segment starts inside this lane
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const float pv = __shfl_up_sync(0xffffffffu, v, d);
-      const int pf = __shfl_up_sync(0xffffffffu, f, d);
-      if (lane >= d) {
-        if (!f) v = mx<kExact>(pv, v);
-        f |= pf;
-      }
-    }
-    if (lane == 31) {
-      wv[warp] = v;
-      wf[warp] = f;
-    }
-    float cv = __shfl_up_sync(0xffffffffu, v, 1);
-    int cf = __shfl_up_sync(0xffffffffu, f, 1);
-    bar_consumers();
-    float wc = kId;  // carry from the warps to the left
-    for (int w = 0; w < warp; ++w) wc = wf[w] ? wv[w] : mx<kExact>(wc, wv[w]);
-    if (lane == 0) {
-      cv = wc;
-    } else if (!cf) {
-      cv = mx<kExact>(wc, cv);
-    }
-#pragma unroll
-    for (int j = 0; j < kT; ++j)
-      if (j < jb) P[j] = mx<kExact>(cv, P[j]);
-  }
-  // ---- suffix, right to left; reset at the segment end e
   S[kT - 1] = s[kT - 1];
 #pragma unroll
   for (int j = kT - 2; j >= 0; --j) S[j] = (j == e) ? s[j] : mx<kExact>(s[j], S[j + 1]);
-  bar_consumers();  // wv / wf reuse
-  {
-    float v = S[0];
-    int f = e >= 0;  // a segment ends inside this lane
+  // ---- across lanes (shuffles): inclusive segmented scans of the lane
+  // aggregates, left to right for P, right to left for S
+  float pv = P[kT - 1], sv = S[0];
+  int pf = jb < kT, sf = e >= 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const float pv = __shfl_down_sync(0xffffffffu, v, d);
-      const int pf = __shfl_down_sync(0xffffffffu, f, d);
-      if (lane + d < 32) {
-        if (!f) v = mx<kExact>(v, pv);
-        f |= pf;
-      }
+  for (int d = 1; d < 32; d <<= 1) {
+    const float upv = __shfl_up_sync(0xffffffffu, pv, d);
+    const int upf = __shfl_up_sync(0xffffffffu, pf, d);
+    const float dnv = __shfl_down_sync(0xffffffffu, sv, d);
+    const int dnf = __shfl_down_sync(0xffffffffu, sf, d);
+    if (lane >= d) {
+      if (!pf) pv = mx<kExact>(upv, pv);
+      pf |= upf;
     }
-    if (lane == 0) {
-      wv[warp] = v;
-      wf[warp] = f;
+    if (lane + d < 32) {
+      if (!sf) sv = mx<kExact>(sv, dnv);
+      sf |= dnf;
     }
-    float cv = __shfl_down_sync(0xffffffffu, v, 1);
-    int cf = __shfl_down_sync(0xffffffffu, f, 1);
-    bar_consumers();
-    float wc = kId;  // carry from the warps to the right
-    for (int w = kWarps - 1; w > warp; --w) wc = wf[w] ? wv[w] : mx<kExact>(wv[w], wc);
-    if (lane == 31) {
-      cv = wc;
-    } else if (!cf) {
-      cv = mx<kExact>(cv, wc);
-    }
-#pragma unroll
-    for (int j = 0; j < kT; ++j)
-      if (j > e) S[j] = mx<kExact>(S[j], cv);
   }
+  // ---- across warps (one barrier): warp totals to shared memory
+  if (lane == 31) {
+    wv[warp] = pv;
+    wf[warp] = pf;
+  }
+  if (lane == 0) {
+    wv[kWarps + warp] = sv;
+    wf[kWarps + warp] = sf;
+  }
+  float cpv = __shfl_up_sync(0xffffffffu, pv, 1);    // exclusive, from the left
+  const int cpf = __shfl_up_sync(0xffffffffu, pf, 1);
+  float csv = __shfl_down_sync(0xffffffffu, sv, 1);  // exclusive, from the right
+  const int csf = __shfl_down_sync(0xffffffffu, sf, 1);
+  bar_consumers();
+  float wl = kId, wr = kId;
+  for (int w = 0; w < warp; ++w) wl = wf[w] ? wv[w] : mx<kExact>(wl, wv[w]);
+  for (int w = kWarps - 1; w > warp; --w)
+    wr = wf[kWarps + w] ? wv[kWarps + w] : mx<kExact>(wv[kWarps + w], wr);
+  if (lane == 0) cpv = wl;
+  else if (!cpf) cpv = mx<kExact>(wl, cpv);
+  if (lane == 31) csv = wr;
+  else if (!csf) csv = mx<kExact>(csv, wr);
 #pragma unroll
   for (int q = 0; q < kT / 4; ++q) {
-    *reinterpret_cast<float4*>(arr_p + swz(p0 + 4 * q)) =
-        make_float4(P[4 * q], P[4 * q + 1], P[4 * q + 2], P[4 * q + 3]);
-    *reinterpret_cast<float4*>(arr_s + swz(p0 + 4 * q)) =
-        make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
+    float4 p4, s4;
+    p4.x = (4 * q + 0 < jb) ? mx<kExact>(cpv, P[4 * q + 0]) : P[4 * q + 0];
+    p4.y = (4 * q + 1 < jb) ? mx<kExact>(cpv, P[4 * q + 1]) : P[4 * q + 1];
+    p4.z = (4 * q + 2 < jb) ? mx<kExact>(cpv, P[4 * q + 2]) : P[4 * q + 2];
+    p4.w = (4 * q + 3 < jb) ? mx<kExact>(cpv, P[4 * q + 3]) : P[4 * q + 3];
+    s4.x = (4 * q + 0 > e) ? mx<kExact>(S[4 * q + 0], csv) : S[4 * q + 0];
+    s4.y = (4 * q + 1 > e) ? mx<kExact>(S[4 * q + 1], csv) : S[4 * q + 1];
+    s4.z = (4 * q + 2 > e) ? mx<kExact>(S[4 * q + 2], csv) : S[4 * q + 2];
+    s4.w = (4 * q + 3 > e) ? mx<kExact>(S[4 * q + 3], csv) : S[4 * q + 3];
+    *reinterpret_cast<float4*>(arr_p + swz(p0 + 4 * q)) = p4;
+    *reinterpret_cast<float4*>(arr_s + swz(p0 + 4 * q)) = s4;
   }
   bar_consumers();
 }
@@ -215,8 +202,8 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), 2)
   const int jb = first_start - p0 < kT ? first_start - p0 : kT;
   const int end_pos = (p0 / k + 1) * k - 1;      // end of p0's segment
   const int e = end_pos - p0 < kT ? end_pos - p0 : -1;
-  __shared__ float seg_v[kWarps];
-  __shared__ int seg_f[kWarps];
+  __shared__ float seg_v[2 * kWarps];
+  __shared__ int seg_f[2 * kWarps];
   int it = 0;
   for (unsigned t = t_begin; t < nt; ++t, ++it) {
     const int b = it % kNbuf;
