@@ -125,20 +125,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmw, float* __restrict__ y, int cin,
                       int h, int w, int cout, int ntiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-#ifdef SC_TC_TRACE
-  // debugging aid: per-k-block clock64 stamps of CTA 0 written over y
-  auto TR = [&](int slot, int i) {
-    if (blockIdx.x == 0 && i < 128) reinterpret_cast<uint32_t*>(y)[slot * 128 + i] = (uint32_t)clock64();
-  };
-  auto GT = [&](int which) {
-    uint64_t g;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-    reinterpret_cast<uint64_t*>(y)[1024 + blockIdx.x * 4 + which] = g;
-  };
-  if (threadIdx.x == 0) GT(0);
-#else
-  auto TR = [](int, int) {};
-#endif
   __shared__ __align__(8) uint64_t a_full[kAStages], a_empty[kAStages];
   // kb_full[s]: B landed (tx) + 8 split warps stored X1/X2; kb_free[s]: both
   // issuers' MMAs of the k-block retired (commit); d_full / d_empty: the
@@ -243,7 +229,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int tap = 0; tap < 9; ++tap, ++bc) {
             const int sb = bc % kStages;
             if (bc >= kStages) mbar_wait(&kb_free[sb], ((bc / kStages) - 1) & 1);
-            TR(5, bc);
             mbar_arrive_expect_tx(&kb_full[sb], kBBytes);
             tma_load_3d(b_ring + sb * kBBytes, &tmw, &kb_full[sb], chunk * kKB, 2 * co0, tap);
           }
@@ -269,7 +254,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < 9 * cchunks; ++kb, ++kc) {
           const int s = kc % kStages;
           mbar_wait(&kb_full[s], (kc / kStages) & 1);
-          if (first) TR(0, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           // B: K-major SW128 (128-byte rows of 64 bf16 channels, SBO = 1 KiB
           // per 8-row group); a 16-channel k-step advances the start by 32 B
@@ -282,9 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int ks = 0; ks < kKB / kKS; ++ks) mma_bf16_ts<kN>(d, xa + 8 * ks, db + 2 * ks, 1u);
           }
-          if (first) TR(8, kc);
           umma_commit(&kb_free[s]);
-          if (first) TR(2, kc);
         }
         umma_commit(&d_full[acc]);
       }
@@ -355,7 +337,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ss = kc % kStages;
           const int dj = tap / 3, di = tap % 3 - 1;
           if (kc >= kStages) mbar_wait(&kb_free[ss], ((kc / kStages) - 1) & 1);
-          if (q == 0 && lane == 0 && half == 0) TR(3, kc);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kTmemA + ss * 2 * kACols +
                               half * (kACols / 2);
@@ -372,12 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tmem_st16(ta, v1);
           tmem_st16(ta + kACols, v2);
-          if (q == 0 && lane == 0 && half == 0) TR(4, kc);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          if (q == 0 && lane == 0 && half == 0) TR(7, kc);
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
-          if (q == 0 && lane == 0 && half == 0) TR(6, kc);
           if (lane == 0) mbar_arrive(&kb_full[ss]);
         }
       }
@@ -408,11 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         tmem_st16(taddr + ch0, zero16);  // re-arm the accumulator for tile it + 2
         tmem_st16(taddr + kN + ch0, zero16);
-#ifdef SC_TC_TRACE
-        if (false) {
-#else
         if (oh < h) {
-#endif
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
@@ -425,13 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-#ifdef SC_TC_TRACE
-  if (warp == 1 && lane == 0) GT(2);
-#endif
   __syncthreads();
-#ifdef SC_TC_TRACE
-  if (threadIdx.x == 0) GT(3);
-#endif
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
