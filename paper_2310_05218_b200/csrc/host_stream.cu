@@ -34,6 +34,28 @@ constexpr size_t kMaxChunkBytes = size_t(64) << 20;
 
 // Chunk size: ~1/16 of the transfer (so the unoverlapped first H2D and last
 // D2H are short), between 8 and 64 MiB (SC_HOST_CHUNK_MB overrides).
+// Chunk sizes (in units: signals, images or output rows) that ramp up
+// geometrically from `min_unit` to `full` and back down at the end, so the
+// first H2D copy and the last D2H copy -- the parts of the pipeline that
+// cannot overlap anything -- are small.
+std::vector<int64_t> ramp_sizes(int64_t total, int64_t full, int64_t min_unit) {
+  std::vector<int64_t> up, out;
+  int64_t s = std::max<int64_t>(1, min_unit), used = 0;
+  while (s < full && used + 2 * s <= total) {
+    up.push_back(s);
+    used += 2 * s;
+    s *= 2;
+  }
+  out = up;
+  for (int64_t mid = total - used; mid > 0;) {
+    const int64_t c = std::min(full, mid);
+    out.push_back(c);
+    mid -= c;
+  }
+  for (auto it = up.rbegin(); it != up.rend(); ++it) out.push_back(*it);
+  return out;
+}
+
 size_t chunk_bytes(size_t total) {
   if (const char* e = getenv("SC_HOST_CHUNK_MB")) {
     const long mb = atol(e);
@@ -220,9 +242,11 @@ extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t
   const size_t kChunkBytes = chunk_bytes((size_t)(batch * row_bytes));
   if (row_bytes <= (int64_t)kChunkBytes) {
     const int64_t rows = std::max<int64_t>(1, (int64_t)kChunkBytes / row_bytes);
-    for (int64_t r = 0; r < batch; r += rows) {
-      const int64_t nr = std::min(rows, batch - r);
-      chunks.push_back({x + r * length, (size_t)(nr * length) * sizeof(float), y + r * out_len,
+    int64_t r = 0;
+    for (const int64_t nr : ramp_sizes(batch, rows, 1)) {
+      const int64_t r0 = r;
+      r += nr;
+      chunks.push_back({x + r0 * length, (size_t)(nr * length) * sizeof(float), y + r0 * out_len,
                         (size_t)(nr * out_len) * sizeof(float),
                         [=](const float* din, float* dout, cudaStream_t st) {
                           return sc_pool1d_f32(op, din, nr, length, k, mode, dout, st);
@@ -263,8 +287,10 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
   const size_t kChunkBytes = chunk_bytes((size_t)(batch * img_bytes));
   if (img_bytes <= (int64_t)kChunkBytes) {
     const int64_t imgs = std::max<int64_t>(1, (int64_t)kChunkBytes / img_bytes);
-    for (int64_t b = 0; b < batch; b += imgs) {
-      const int64_t nb = std::min(imgs, batch - b);
+    int64_t b_next = 0;
+    for (const int64_t nb : ramp_sizes(batch, imgs, 1)) {
+      const int64_t b = b_next;
+      b_next += nb;
       chunks.push_back({x + b * h * w, (size_t)(nb * h * w) * sizeof(float), y + b * oh * ow,
                         (size_t)(nb * oh * ow) * sizeof(float),
                         [=, &taps](const float* din, float* dout, cudaStream_t st) {
@@ -276,9 +302,11 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
     // row bands with a kh-1 row halo (bit-identical to the whole image)
     const int64_t band = std::max<int64_t>(1, (int64_t)kChunkBytes / (w * (int64_t)sizeof(float)) -
                                                   (kh - 1));
-    for (int64_t b = 0; b < batch; ++b)
-      for (int64_t o = 0; o < oh; o += band) {
-        const int64_t no = std::min(band, oh - o);
+    for (int64_t b = 0; b < batch; ++b) {
+      int64_t o_next = 0;
+      for (const int64_t no : ramp_sizes(oh, band, std::max<int64_t>(1, band / 8))) {
+        const int64_t o = o_next;
+        o_next += no;
         const int64_t ni = no + kh - 1;
         chunks.push_back({x + (b * h + o) * w, (size_t)(ni * w) * sizeof(float),
                           y + (b * oh + o) * ow, (size_t)(no * ow) * sizeof(float),
@@ -287,6 +315,7 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
                                                        dout, st);
                           }});
       }
+    }
   }
   return run_pipeline(device, chunks, is_pinned(x), is_pinned(y));
 }
