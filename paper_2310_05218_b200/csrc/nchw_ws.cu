@@ -146,14 +146,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int chunks = a_cols / 16;                // 18 for Cin 64, 9 for Cin 32
     const int per = (chunks + 2) / 3;
     const int c_lo = third * per, c_hi = min(chunks, c_lo + per);
-    const uint4* arow = reinterpret_cast<const uint4*>(
-        apack + ((size_t)co_tile * 128 + 32 * q + lane) * a_cols);
+    // apack is [tile][16-column chunk][4 x 16 B][128 lanes]: a warp's load of
+    // one 16-byte piece is 512 contiguous bytes
+    const uint4* abase = reinterpret_cast<const uint4*>(apack) +
+                         (size_t)co_tile * chunks * 4 * 128 + 32 * q + lane;
     uint4 buf[6][4];
 #pragma unroll
     for (int k = 0; k < 6; ++k)
       if (c_lo + k < c_hi)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) buf[k][v] = __ldg(arow + (c_lo + k) * 4 + v);
+        for (int v = 0; v < 4; ++v) buf[k][v] = __ldg(abase + ((c_lo + k) * 4 + v) * 128);
 #pragma unroll
     for (int k = 0; k < 6; ++k)
       if (c_lo + k < c_hi) tmem_st16(lane_base + kTmemA + (c_lo + k) * 16,
@@ -363,7 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// w[co][ci][3][3] -> A rows per 64-channel tile: row 32q + j holds channel
+// w[co][ci][3][3] -> A for each 64-channel tile (stored chunk-major for
+// coalesced loads, see the A load above): row 32q + j holds channel
 // 16q + (j & 15), bf16 w1 for j < 16 and bf16 w2 = bf16(w - w1) for j >= 16;
 // column k2 packs K elements (2 k2, 2 k2 + 1) with K = tap * Cin + ci (low
 // half = even element)
@@ -385,7 +388,9 @@ __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __re
       const __nv_bfloat16 part = hlf ? __float2bfloat16_rn(v - __bfloat162float(v1)) : v1;
       packed |= (uint32_t)__bfloat16_as_ushort(part) << (16 * t);
     }
-    apack[e] = packed;
+    // [tile][chunk = k2 / 16][piece = (k2 % 16) / 4][lane m][word k2 % 4]
+    const int chunk = k2 >> 4, piece = (k2 >> 2) & 3, word = k2 & 3;
+    apack[((((size_t)tile * (a_cols / 16) + chunk) * 4 + piece) * 128 + m) * 4 + word] = packed;
   }
 }
 
