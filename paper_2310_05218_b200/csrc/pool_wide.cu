@@ -152,7 +152,7 @@ __device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int jb, 
 }
 
 template <int kOp>
-__global__ void __launch_bounds__(32 * (kWarps + 1), 2)
+__global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
     pool_wide_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y, int k,
                      int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
                      int vt) {
