@@ -194,7 +194,12 @@ int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_p
   for (size_t i = 0; i < chunks.size() && status == SC_OK; ++i) {
     Slot& s = ctx.slot[i % kSlots];
     Chunk& c = chunks[i];
-    if ((status = finish_slot(s))) break;
+    // A slot's device buffers are reused by chunk i + kSlots on the same
+    // stream, so stream order alone protects them.  The host only has to
+    // wait when it touches the staging buffers (pageable input / output):
+    // with pinned data everything is enqueued up front and the copy engines
+    // never wait for a host wake-up.
+    if (!(in_pinned && out_pinned) && (status = finish_slot(s))) break;
     const float* src = c.in;
     if (!in_pinned) {
       parallel_memcpy(s.h_in, c.in, c.in_bytes);

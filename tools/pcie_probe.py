@@ -44,3 +44,23 @@ t = timed(d2h)
 print(f"D2H alone: {nb / t / 1e9:.1f} GB/s")
 t = timed(both)
 print(f"H2D + D2H concurrent: {nb / t / 1e9:.1f} GB/s each direction, {2 * nb / t / 1e9:.1f} total")
+
+# chunked, the host pipeline's pattern: 16 x 16 MB, each chunk H2D then D2H
+# on one of 3 streams (chunk i+3 reuses chunk i's device buffer)
+streams = [torch.cuda.Stream() for _ in range(3)]
+cn = n // 16
+dev_in = [torch.empty(cn, device="cuda") for _ in range(3)]
+dev_out = [torch.empty(cn, device="cuda") for _ in range(3)]
+
+
+def chunked():
+    for i in range(16):
+        s = streams[i % 3]
+        with torch.cuda.stream(s):
+            dev_in[i % 3].copy_(h_in[i * cn:(i + 1) * cn], non_blocking=True)
+            dev_out[i % 3].copy_(dev_in[i % 3])
+            h_out[i * cn:(i + 1) * cn].copy_(dev_out[i % 3], non_blocking=True)
+
+
+t = timed(chunked)
+print(f"chunked 16 x 16 MB, 3 streams: {nb / t / 1e9:.1f} GB/s each direction")
