@@ -75,3 +75,23 @@ def test_conv2d_im2col_matches_direct():
     assert c.im2col_elems == 296 * 696 * 25
     y2, c2 = sc.run_variant(sc.KernelVariant.IM2COL_GEMM, x, f, sc.VectorModel(16))
     assert c2.im2col_elems == c.im2col_elems
+
+
+def test_nonfinite_inputs():
+    # exact mode reproduces the reference's inf / NaN pattern bit for bit; the
+    # fast tensor-core path (bf16x3 split: inf - bf16(inf) = NaN) keeps every
+    # affected output non-finite and every unaffected one within tolerance
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((1, 64, 16, 32), dtype=np.float32)
+    x[0, 5, 7, 9] = np.inf
+    x[0, 40, 2, 30] = np.nan
+    w = (rng.standard_normal((64, 64, 3, 3), dtype=np.float32) / np.float32(24.0)).astype(np.float32)
+    want = O.conv2d_nchw(x, w, 1)
+    exact = sc.conv2d_nchw(x, w, 1, exact=True)
+    assert np.array_equal(exact, want, equal_nan=True)
+    fast = sc.conv2d_nchw(x, w, 1)
+    bad = ~np.isfinite(want)
+    assert np.all(~np.isfinite(fast[bad]))
+    good = ~bad
+    ref64 = O.conv2d_nchw_f64(np.where(np.isfinite(x), x, 0).astype(np.float32), w, 1)
+    assert np.allclose(fast[good], ref64[good], rtol=1e-4, atol=1e-4)
