@@ -227,6 +227,131 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
   }
 }
 
+// ------------------------------------------------ 4-column rolling kernel
+// conv2d_cols4_kernel<K>: the FP32-bound 7 x 7 (config 5).  A lane owns FOUR
+// consecutive output columns and K rolling accumulator rows (4K registers).
+// Per input row it reads its K + 3 inputs (two LDS.128 + one LDS.64 ... as
+// float4 / float2, conflict-free) and issues 4 K^2 FFMAs with the taps as
+// constant-bank operands: ~97 % of the issued instructions are FMAs (the
+// column-pair kernel above spends ~30 % on loads and packing).  Each consumer
+// warp covers 128 columns with its own TMA box per stage.
+constexpr int kC4Warps = 4;                        // consumer warps per CTA (one TMA box each)
+constexpr int kC4Cols = 128;                       // output columns per warp
+constexpr int kC4Stages = 4;
+constexpr int kC4RS = 7;                          // input rows per stage (= K)
+__host__ __device__ constexpr int c4_box(int k) { return (kC4Cols + k - 1 + 3) / 4 * 4; }
+__host__ __device__ constexpr int c4_sub(int k) {  // one warp's box, 128-byte aligned
+  return (kC4RS * c4_box(k) + 31) / 32 * 32;
+}
+
+template <int K, bool kExact>
+__global__ void __launch_bounds__(32 * (kC4Warps + 1))
+    conv2d_cols4_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
+                        int64_t oh, int64_t ow, int rows_per_cta, const Taps<K, K> taps) {
+  constexpr int BW = c4_box(K);
+  constexpr int SUB = c4_sub(K);
+  constexpr int STAGE = kC4Warps * SUB;
+  static_assert(kC4RS % K == 0, "rows per stage must be a multiple of K");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
+  __shared__ __align__(8) uint64_t full_bar[kC4Stages];
+  __shared__ __align__(8) uint64_t empty_bar[kC4Stages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * (kC4Warps * kC4Cols);
+  const int r0 = blockIdx.y * rows_per_cta;
+  const int b = blockIdx.z;
+  const int rc = (int)min((int64_t)rows_per_cta, oh - r0);
+  const int n_in = rc + K - 1;
+  const int n_stage = (n_in + kC4RS - 1) / kC4RS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kC4Stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kC4Warps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kC4Warps) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      for (int s = 0; s < n_stage; ++s) {
+        const int slot = s % kC4Stages;
+        if (s >= kC4Stages) mbar_wait_sleep(&empty_bar[slot], ((s / kC4Stages) - 1) & 1);
+        mbar_arrive_expect_tx(&full_bar[slot], kC4Warps * kC4RS * BW * (uint32_t)sizeof(float));
+        for (int wv = 0; wv < kC4Warps; ++wv)
+          tma_load_3d(smem + slot * STAGE + wv * SUB, &tmap, &full_bar[slot], c0 + wv * kC4Cols,
+                      r0 + s * kC4RS, b);
+      }
+    }
+    return;
+  }
+
+  const int col = warp * kC4Cols + 4 * lane;       // first of the lane's 4 columns
+  const int64_t gcol = (int64_t)c0 + col;
+  float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
+  // scalar FFMA (fast) / FMUL + FADD (exact) accumulators: a packed FFMA2
+  // variant needs the odd-offset input pairs re-packed every row and measured
+  // slower (9.2 vs 7.5 ms) -- with ~97 % FFMAs issue slots are not the limit
+  float acc[K][4];
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[j][c] = 0.0f;
+
+  for (int s = 0; s < n_stage; ++s) {
+    const int slot = s % kC4Stages;
+    mbar_wait(&full_bar[slot], (s / kC4Stages) & 1);
+    const float* buf = smem + slot * STAGE + warp * SUB + 4 * lane;
+    auto load = [&](int rr, float (&v)[K + 3]) {
+      const float* p = buf + rr * BW;
+#pragma unroll
+      for (int q = 0; q < (K + 3) / 4; ++q) {
+        const float4 t = reinterpret_cast<const float4*>(p)[q];
+        v[4 * q] = t.x, v[4 * q + 1] = t.y, v[4 * q + 2] = t.z, v[4 * q + 3] = t.w;
+      }
+#pragma unroll
+      for (int q = (K + 3) / 4 * 4; q < K + 3; ++q) v[q] = p[q];
+    };
+    float cur[K + 3];
+    load(0, cur);
+#pragma unroll 1
+    for (int g = 0; g < kC4RS / K; ++g) {
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        const int rr = g * K + u;
+        float nxt[K + 3];
+        if (rr + 1 < kC4RS) load(rr + 1, nxt);
+        // output row t - j lives in slot (u - j) mod K (kC4RS % K == 0)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int sl = ((u - j) % K + K) % K;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float a = (j == 0) ? 0.0f : acc[sl][c];
+#pragma unroll
+            for (int i = 0; i < K; ++i) a = mac<kExact>(a, taps.f[j * K + i], cur[c + i]);
+            acc[sl][c] = a;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < K + 3; ++q) cur[q] = nxt[q];
+        const int t = s * kC4RS + rr;  // input row relative to r0
+        if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
+          const int sl = (u + 1) % K;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (gcol + c < ow) ynext[c] = acc[sl][c];
+        }
+        ynext += ow;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+  }
+}
+
 // --------------------------------------------------------------- generic
 template <typename T, bool kExact>
 __global__ void conv2d_generic_kernel(const T* __restrict__ x, int64_t batch, int64_t h,
@@ -333,6 +458,41 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   return SC_OK;
 }
 
+template <int K, bool kExact>
+int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, float* y,
+                 cudaStream_t st) {
+  constexpr int BW = c4_box(K);
+  const int64_t oh = h - K + 1, ow = w - K + 1;
+  CUtensorMap map;
+  int rc = make_tmap(&map, x, batch, h, w, BW, kC4RS);
+  if (rc) return rc;
+  Taps<K, K> taps;
+  for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
+  const int64_t strips = (ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols);
+  static const int env_rows = [] {
+    const char* e = getenv("SC_CONV_ROWS");
+    return e ? atoi(e) : 0;
+  }();
+  // long row segments (less halo re-reading; measured best at ~900 rows)
+  int64_t rows = env_rows > 0 ? env_rows : (int64_t)kC4RS * 128 - (K - 1);
+  rows = std::min<int64_t>(rows, oh);
+  const int64_t segs = (oh + rows - 1) / rows;
+  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
+    return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
+  const size_t smem = (size_t)kC4Stages * kC4Warps * c4_sub(K) * sizeof(float) + 128;
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(conv2d_cols4_kernel<K, kExact>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
+  conv2d_cols4_kernel<K, kExact><<<grid, 32 * (kC4Warps + 1), smem, st>>>(map, y, oh, ow,
+                                                                         (int)rows, taps);
+  SC_LAUNCH_CHECK("conv2d_cols4_kernel");
+  return SC_OK;
+}
+
 template <typename T>
 int launch_generic(const T* x, int64_t batch, int64_t h, int64_t w, const T* f, int64_t kh,
                    int64_t kw, bool exact, T* y, cudaStream_t st) {
@@ -367,6 +527,15 @@ int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
   *done = false;
   if (!tma_ok<KH, KW>(x, h, w)) return SC_OK;
   *done = true;
+  if constexpr (KH == 7 && KW == 7) {
+    static const bool pairs_kernel = [] {
+      const char* e = getenv("SC_CONV7_PAIRS");
+      return e && e[0] == '1';
+    }();
+    if (!pairs_kernel && w >= c4_box(7))
+      return exact ? launch_cols4<7, true>(x, batch, h, w, f, y, st)
+                   : launch_cols4<7, false>(x, batch, h, w, f, y, st);
+  }
   return exact ? launch_tma<KH, KW, true>(x, batch, h, w, f, y, st)
                : launch_tma<KH, KW, false>(x, batch, h, w, f, y, st);
 }
