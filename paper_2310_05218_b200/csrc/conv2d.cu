@@ -352,6 +352,121 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   }
 }
 
+// ------------------------------------------- rotating 4-column kernel
+// conv2d_rot4_kernel<K>: the same lane tiling for the paper's larger square
+// filters (K = 9 .. 29): 4 columns x K accumulator rows per lane, taps in the
+// constant bank, but instead of unrolling K input rows to make the rolling
+// slot indices static, the accumulator rows are shifted by one after each
+// input row (4 (K - 1) moves against 4 K^2 FFMAs), so the code size is one
+// row body (4 K^2 FFMAs) and the stage depth is independent of K.
+constexpr int kR4RS = 8;
+template <int K>
+struct BigSquareTaps {
+  float f[K * K];
+};
+
+template <int K, bool kExact>
+__global__ void __launch_bounds__(32 * (kC4Warps + 1))
+    conv2d_rot4_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
+                       int64_t oh, int64_t ow, int rows_per_cta,
+                       const __grid_constant__ BigSquareTaps<K> taps) {
+  constexpr int BW = c4_box(K);
+  constexpr int SUB = (kR4RS * BW + 31) / 32 * 32;
+  constexpr int STAGE = kC4Warps * SUB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* smem = reinterpret_cast<float*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
+  __shared__ __align__(8) uint64_t full_bar[kC4Stages];
+  __shared__ __align__(8) uint64_t empty_bar[kC4Stages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * (kC4Warps * kC4Cols);
+  const int r0 = blockIdx.y * rows_per_cta;
+  const int b = blockIdx.z;
+  const int rc = (int)min((int64_t)rows_per_cta, oh - r0);
+  const int n_in = rc + K - 1;
+  const int n_stage = (n_in + kR4RS - 1) / kR4RS;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kC4Stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kC4Warps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kC4Warps) {
+    if (lane == 0) {
+      prefetch_tmap(&tmap);
+      for (int s = 0; s < n_stage; ++s) {
+        const int slot = s % kC4Stages;
+        if (s >= kC4Stages) mbar_wait_sleep(&empty_bar[slot], ((s / kC4Stages) - 1) & 1);
+        mbar_arrive_expect_tx(&full_bar[slot], kC4Warps * kR4RS * BW * (uint32_t)sizeof(float));
+        for (int wv = 0; wv < kC4Warps; ++wv)
+          tma_load_3d(smem + slot * STAGE + wv * SUB, &tmap, &full_bar[slot], c0 + wv * kC4Cols,
+                      r0 + s * kR4RS, b);
+      }
+    }
+    return;
+  }
+
+  const int col = warp * kC4Cols + 4 * lane;
+  const int64_t gcol = (int64_t)c0 + col;
+  float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
+  // acc[j]: output row t - (K - 1) + j for the input row t just consumed
+  float acc[K][4];
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[j][c] = 0.0f;
+
+  int t = 0;  // input row relative to r0
+  for (int s = 0; s < n_stage; ++s) {
+    const int slot = s % kC4Stages;
+    mbar_wait(&full_bar[slot], (s / kC4Stages) & 1);
+    const float* buf = smem + slot * STAGE + warp * SUB + 4 * lane;
+    const int rows_here = min(kR4RS, n_in - s * kR4RS);
+#pragma unroll 1
+    for (int rr = 0; rr < rows_here; ++rr, ++t) {
+      float cur[K + 3];
+      const float* p = buf + rr * BW;
+#pragma unroll
+      for (int q = 0; q < (K + 3) / 4; ++q) {
+        const float4 v = reinterpret_cast<const float4*>(p)[q];
+        cur[4 * q] = v.x, cur[4 * q + 1] = v.y, cur[4 * q + 2] = v.z, cur[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int q = (K + 3) / 4 * 4; q < K + 3; ++q) cur[q] = p[q];
+      // input row t feeds output rows t - j' for filter row j' = K-1 .. 0:
+      // acc[j] holds output row t - (K-1) + j, i.e. filter row K-1-j
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float a = acc[j][c];
+#pragma unroll
+          for (int i = 0; i < K; ++i) a = mac<kExact>(a, taps.f[(K - 1 - j) * K + i], cur[c + i]);
+          acc[j][c] = a;
+        }
+      }
+      // acc[0] (output row t - K + 1) is complete
+      if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (gcol + c < ow) ynext[c] = acc[0][c];
+      }
+      ynext += ow;
+#pragma unroll
+      for (int j = 0; j < K - 1; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[j][c] = acc[j + 1][c];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[K - 1][c] = 0.0f;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+  }
+}
+
 // --------------------------------------------------------------- generic
 template <typename T, bool kExact>
 __global__ void conv2d_generic_kernel(const T* __restrict__ x, int64_t batch, int64_t h,
@@ -493,6 +608,55 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
   return SC_OK;
 }
 
+template <int K, bool kExact>
+int launch_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, float* y,
+                cudaStream_t st) {
+  constexpr int BW = c4_box(K);
+  const int64_t oh = h - K + 1, ow = w - K + 1;
+  CUtensorMap map;
+  int rc = make_tmap(&map, x, batch, h, w, BW, kR4RS);
+  if (rc) return rc;
+  BigSquareTaps<K> taps;
+  for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
+  const int64_t strips = (ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols);
+  // rows per CTA: long segments for big images, at least ~2 waves otherwise
+  int64_t rows = 1024;
+  while (rows > 64 && batch * strips * ((oh + rows - 1) / rows) < 2 * sm_count()) rows /= 2;
+  rows = std::min<int64_t>(rows, oh);
+  const int64_t segs = (oh + rows - 1) / rows;
+  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
+    return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
+  const size_t smem =
+      (size_t)kC4Stages * kC4Warps * ((kR4RS * BW + 31) / 32 * 32) * sizeof(float) + 128;
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(conv2d_rot4_kernel<K, kExact>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
+  conv2d_rot4_kernel<K, kExact><<<grid, 32 * (kC4Warps + 1), smem, st>>>(map, y, oh, ow,
+                                                                        (int)rows, taps);
+  SC_LAUNCH_CHECK("conv2d_rot4_kernel");
+  return SC_OK;
+}
+
+template <int K>
+int try_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, bool exact,
+             float* y, cudaStream_t st, bool* done) {
+  *done = false;
+  if ((reinterpret_cast<uintptr_t>(x) % 16) || (w % 4) || w < c4_box(K) || h < K) return SC_OK;
+  // 512-column CTAs: for a grid smaller than ~one wave (one 512^2 image) the
+  // register-blocked conv2d_big kernel, with its smaller tiles, is faster
+  const int64_t oh = h - K + 1, ow = w - K + 1;
+  const int64_t ctas = batch * ((ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols)) *
+                       ((oh + 63) / 64);
+  if (ctas < sm_count()) return SC_OK;
+  *done = true;
+  return exact ? launch_rot4<K, true>(x, batch, h, w, f, y, st)
+               : launch_rot4<K, false>(x, batch, h, w, f, y, st);
+}
+
 template <typename T>
 int launch_generic(const T* x, int64_t batch, int64_t h, int64_t w, const T* f, int64_t kh,
                    int64_t kw, bool exact, T* y, cudaStream_t st) {
@@ -564,6 +728,13 @@ int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, con
   else if (kh == 7 && kw == 7) rc = try_tma<7, 7>(x, batch, h, w, f, exact, y, st, &done);
   else if (kh == 1 && kw == 7) rc = try_tma<1, 7>(x, batch, h, w, f, exact, y, st, &done);
   else if (kh == 1 && kw == 3) rc = try_tma<1, 3>(x, batch, h, w, f, exact, y, st, &done);
+  // the paper's mid-size square filters: rotating 4-column kernels
+  else if (kh == 9 && kw == 9) rc = try_rot4<9>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 11 && kw == 11) rc = try_rot4<11>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 13 && kw == 13) rc = try_rot4<13>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 15 && kw == 15) rc = try_rot4<15>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 17 && kw == 17) rc = try_rot4<17>(x, batch, h, w, f, exact, y, st, &done);
+  else if (kh == 21 && kw == 21) rc = try_rot4<21>(x, batch, h, w, f, exact, y, st, &done);
   if (rc || done) return rc;
   // runtime (kh, kw) up to 64 x 64: the register-blocked kernel (conv2d_big.cu)
   rc = conv2d_big(x, batch, h, w, f, kh, kw, exact, y, st);

@@ -53,6 +53,19 @@ def test_runtime_k_register_blocked_kernel(kh, kw, n, h, w):
     assert O.normwise_error(fast, ref64) <= O.north_star_tol(max(kh, kw))
 
 
+@pytest.mark.parametrize("k", [9, 11, 13, 15, 17, 21])
+def test_rotating_4col_kernels(k):
+    # conv2d_rot4_kernel<K>: large batches of images (>= one wave of 512-col CTAs)
+    x = rand(k + 900, (24, 256, 600))
+    f = rand(k + 901, (k, k))
+    xd = torch.from_numpy(x).cuda()
+    got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
+    assert np.array_equal(got, O.conv2d_batched(x, f))
+    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    ref64 = np.stack([O.oracle_conv2d(img, f) for img in x[:3]])
+    assert O.normwise_error(fast[:3], ref64) <= O.north_star_tol(k)
+
+
 @pytest.mark.parametrize("exact", [True, False])
 def test_runtime_k_nonfinite_inputs_match_reference(exact):
     # a zero-padded tap must never multiply an inf beyond the filter width
