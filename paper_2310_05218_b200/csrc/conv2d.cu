@@ -238,10 +238,11 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
 constexpr int kC4Warps = 4;                        // consumer warps per CTA (one TMA box each)
 constexpr int kC4Cols = 128;                       // output columns per warp
 constexpr int kC4Stages = 4;
-constexpr int kC4RS = 7;                          // input rows per stage (= K)
+// input rows per stage: a multiple of K (static rolling slots), ~7-10 rows
+__host__ __device__ constexpr int c4_rs(int k) { return k >= 7 ? k : 2 * k; }
 __host__ __device__ constexpr int c4_box(int k) { return (kC4Cols + k - 1 + 3) / 4 * 4; }
 __host__ __device__ constexpr int c4_sub(int k) {  // one warp's box, 128-byte aligned
-  return (kC4RS * c4_box(k) + 31) / 32 * 32;
+  return (c4_rs(k) * c4_box(k) + 31) / 32 * 32;
 }
 
 template <int K, bool kExact>
@@ -251,6 +252,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   constexpr int BW = c4_box(K);
   constexpr int SUB = c4_sub(K);
   constexpr int STAGE = kC4Warps * SUB;
+  constexpr int kC4RS = c4_rs(K);
   static_assert(kC4RS % K == 0, "rows per stage must be a multiple of K");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* smem = reinterpret_cast<float*>(smem_raw + ((128 - (smem_u32(smem_raw) & 127)) & 127));
@@ -579,7 +581,7 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
   constexpr int BW = c4_box(K);
   const int64_t oh = h - K + 1, ow = w - K + 1;
   CUtensorMap map;
-  int rc = make_tmap(&map, x, batch, h, w, BW, kC4RS);
+  int rc = make_tmap(&map, x, batch, h, w, BW, c4_rs(K));
   if (rc) return rc;
   Taps<K, K> taps;
   for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
@@ -589,7 +591,10 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
     return e ? atoi(e) : 0;
   }();
   // long row segments (less halo re-reading; measured best at ~900 rows)
-  int64_t rows = env_rows > 0 ? env_rows : (int64_t)kC4RS * 128 - (K - 1);
+  // measured (tools/conv_sweep.py): ~890 rows for the FP32-bound 7 x 7, ~450
+  // for the bandwidth-bound 5 x 5 (shorter segments keep streams adjacent)
+  const int64_t seg_rows = K >= 7 ? 896 : 450;
+  int64_t rows = env_rows > 0 ? env_rows : (int64_t)c4_rs(K) * (seg_rows / c4_rs(K)) - (K - 1);
   rows = std::min<int64_t>(rows, oh);
   const int64_t segs = (oh + rows - 1) / rows;
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
@@ -691,14 +696,14 @@ int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
   *done = false;
   if (!tma_ok<KH, KW>(x, h, w)) return SC_OK;
   *done = true;
-  if constexpr (KH == 7 && KW == 7) {
+  if constexpr ((KH == 7 && KW == 7) || (KH == 5 && KW == 5)) {
     static const bool pairs_kernel = [] {
-      const char* e = getenv("SC_CONV7_PAIRS");
+      const char* e = getenv(KH == 7 ? "SC_CONV7_PAIRS" : "SC_CONV5_PAIRS");
       return e && e[0] == '1';
     }();
-    if (!pairs_kernel && w >= c4_box(7))
-      return exact ? launch_cols4<7, true>(x, batch, h, w, f, y, st)
-                   : launch_cols4<7, false>(x, batch, h, w, f, y, st);
+    if (!pairs_kernel && w >= c4_box(KH))
+      return exact ? launch_cols4<KH, true>(x, batch, h, w, f, y, st)
+                   : launch_cols4<KH, false>(x, batch, h, w, f, y, st);
   }
   return exact ? launch_tma<KH, KW, true>(x, batch, h, w, f, y, st)
                : launch_tma<KH, KW, false>(x, batch, h, w, f, y, st);
