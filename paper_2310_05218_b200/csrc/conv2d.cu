@@ -367,12 +367,16 @@ struct BigSquareTaps {
   float f[K * K];
 };
 
-template <int K, bool kExact>
+// C = columns per lane (4; a 2-column variant for K = 29..37 measured slower
+// than conv2d_big, 18-25 vs 36 TFLOP/s); a warp covers 32 C columns.
+__host__ __device__ constexpr int rot_box(int k, int c) { return (32 * c + k - 1 + 3) / 4 * 4; }
+
+template <int K, int C, bool kExact>
 __global__ void __launch_bounds__(32 * (kC4Warps + 1))
     conv2d_rot4_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                        int64_t oh, int64_t ow, int rows_per_cta,
                        const __grid_constant__ BigSquareTaps<K> taps) {
-  constexpr int BW = c4_box(K);
+  constexpr int BW = rot_box(K, C);
   constexpr int SUB = (kR4RS * BW + 31) / 32 * 32;
   constexpr int STAGE = kC4Warps * SUB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   __shared__ __align__(8) uint64_t full_bar[kC4Stages];
   __shared__ __align__(8) uint64_t empty_bar[kC4Stages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c0 = blockIdx.x * (kC4Warps * kC4Cols);
+  const int c0 = blockIdx.x * (kC4Warps * 32 * C);
   const int r0 = blockIdx.y * rows_per_cta;
   const int b = blockIdx.z;
   const int rc = (int)min((int64_t)rows_per_cta, oh - r0);
@@ -404,46 +408,57 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
         if (s >= kC4Stages) mbar_wait_sleep(&empty_bar[slot], ((s / kC4Stages) - 1) & 1);
         mbar_arrive_expect_tx(&full_bar[slot], kC4Warps * kR4RS * BW * (uint32_t)sizeof(float));
         for (int wv = 0; wv < kC4Warps; ++wv)
-          tma_load_3d(smem + slot * STAGE + wv * SUB, &tmap, &full_bar[slot], c0 + wv * kC4Cols,
-                      r0 + s * kR4RS, b);
+          tma_load_3d(smem + slot * STAGE + wv * SUB, &tmap, &full_bar[slot],
+                      c0 + wv * 32 * C, r0 + s * kR4RS, b);
       }
     }
     return;
   }
 
-  const int col = warp * kC4Cols + 4 * lane;
+  const int col = warp * 32 * C + C * lane;
   const int64_t gcol = (int64_t)c0 + col;
   float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
   // acc[j]: output row t - (K - 1) + j for the input row t just consumed
-  float acc[K][4];
+  float acc[K][C];
 #pragma unroll
   for (int j = 0; j < K; ++j)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[j][c] = 0.0f;
+    for (int c = 0; c < C; ++c) acc[j][c] = 0.0f;
 
   int t = 0;  // input row relative to r0
   for (int s = 0; s < n_stage; ++s) {
     const int slot = s % kC4Stages;
     mbar_wait(&full_bar[slot], (s / kC4Stages) & 1);
-    const float* buf = smem + slot * STAGE + warp * SUB + 4 * lane;
+    const float* buf = smem + slot * STAGE + warp * SUB + C * lane;
     const int rows_here = min(kR4RS, n_in - s * kR4RS);
 #pragma unroll 1
     for (int rr = 0; rr < rows_here; ++rr, ++t) {
-      float cur[K + 3];
+      constexpr int NW = K + C - 1;  // the lane's input window
+      float cur[NW];
       const float* p = buf + rr * BW;
+      if constexpr (C == 4) {
 #pragma unroll
-      for (int q = 0; q < (K + 3) / 4; ++q) {
-        const float4 v = reinterpret_cast<const float4*>(p)[q];
-        cur[4 * q] = v.x, cur[4 * q + 1] = v.y, cur[4 * q + 2] = v.z, cur[4 * q + 3] = v.w;
+        for (int q = 0; q < NW / 4; ++q) {
+          const float4 v = reinterpret_cast<const float4*>(p)[q];
+          cur[4 * q] = v.x, cur[4 * q + 1] = v.y, cur[4 * q + 2] = v.z, cur[4 * q + 3] = v.w;
+        }
+#pragma unroll
+        for (int q = NW / 4 * 4; q < NW; ++q) cur[q] = p[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < NW / 2; ++q) {
+          const float2 v = reinterpret_cast<const float2*>(p)[q];
+          cur[2 * q] = v.x, cur[2 * q + 1] = v.y;
+        }
+#pragma unroll
+        for (int q = NW / 2 * 2; q < NW; ++q) cur[q] = p[q];
       }
-#pragma unroll
-      for (int q = (K + 3) / 4 * 4; q < K + 3; ++q) cur[q] = p[q];
       // input row t feeds output rows t - j' for filter row j' = K-1 .. 0:
       // acc[j] holds output row t - (K-1) + j, i.e. filter row K-1-j
 #pragma unroll
       for (int j = 0; j < K; ++j) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < C; ++c) {
           float a = acc[j][c];
 #pragma unroll
           for (int i = 0; i < K; ++i) a = mac<kExact>(a, taps.f[(K - 1 - j) * K + i], cur[c + i]);
@@ -453,16 +468,16 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
       // acc[0] (output row t - K + 1) is complete
       if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < C; ++c)
           if (gcol + c < ow) ynext[c] = acc[0][c];
       }
       ynext += ow;
 #pragma unroll
       for (int j = 0; j < K - 1; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[j][c] = acc[j + 1][c];
+        for (int c = 0; c < C; ++c) acc[j][c] = acc[j + 1][c];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[K - 1][c] = 0.0f;
+      for (int c = 0; c < C; ++c) acc[K - 1][c] = 0.0f;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[slot]);
@@ -613,17 +628,17 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
   return SC_OK;
 }
 
-template <int K, bool kExact>
+template <int K, int C, bool kExact>
 int launch_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, float* y,
                 cudaStream_t st) {
-  constexpr int BW = c4_box(K);
+  constexpr int BW = rot_box(K, C);
   const int64_t oh = h - K + 1, ow = w - K + 1;
   CUtensorMap map;
   int rc = make_tmap(&map, x, batch, h, w, BW, kR4RS);
   if (rc) return rc;
   BigSquareTaps<K> taps;
   for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
-  const int64_t strips = (ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols);
+  const int64_t strips = (ow + kC4Warps * 32 * C - 1) / (kC4Warps * 32 * C);
   // rows per CTA: long segments for big images, at least ~2 waves otherwise
   int64_t rows = 1024;
   while (rows > 64 && batch * strips * ((oh + rows - 1) / rows) < 2 * sm_count()) rows /= 2;
@@ -635,12 +650,12 @@ int launch_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float
       (size_t)kC4Stages * kC4Warps * ((kR4RS * BW + 31) / 32 * 32) * sizeof(float) + 128;
   static bool attr = false;
   if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(conv2d_rot4_kernel<K, kExact>,
+    SC_CUDA(cudaFuncSetAttribute(conv2d_rot4_kernel<K, C, kExact>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
-  conv2d_rot4_kernel<K, kExact><<<grid, 32 * (kC4Warps + 1), smem, st>>>(map, y, oh, ow,
+  conv2d_rot4_kernel<K, C, kExact><<<grid, 32 * (kC4Warps + 1), smem, st>>>(map, y, oh, ow,
                                                                         (int)rows, taps);
   SC_LAUNCH_CHECK("conv2d_rot4_kernel");
   return SC_OK;
@@ -649,17 +664,18 @@ int launch_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float
 template <int K>
 int try_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, bool exact,
              float* y, cudaStream_t st, bool* done) {
+  constexpr int C = K <= 21 ? 4 : 2;
   *done = false;
-  if ((reinterpret_cast<uintptr_t>(x) % 16) || (w % 4) || w < c4_box(K) || h < K) return SC_OK;
+  if ((reinterpret_cast<uintptr_t>(x) % 16) || (w % 4) || w < rot_box(K, C) || h < K) return SC_OK;
   // 512-column CTAs: for a grid smaller than ~one wave (one 512^2 image) the
   // register-blocked conv2d_big kernel, with its smaller tiles, is faster
   const int64_t oh = h - K + 1, ow = w - K + 1;
-  const int64_t ctas = batch * ((ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols)) *
+  const int64_t ctas = batch * ((ow + kC4Warps * 32 * C - 1) / (kC4Warps * 32 * C)) *
                        ((oh + 63) / 64);
   if (ctas < sm_count()) return SC_OK;
   *done = true;
-  return exact ? launch_rot4<K, true>(x, batch, h, w, f, y, st)
-               : launch_rot4<K, false>(x, batch, h, w, f, y, st);
+  return exact ? launch_rot4<K, C, true>(x, batch, h, w, f, y, st)
+               : launch_rot4<K, C, false>(x, batch, h, w, f, y, st);
 }
 
 template <typename T>
@@ -701,7 +717,11 @@ int try_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
       const char* e = getenv(KH == 7 ? "SC_CONV7_PAIRS" : "SC_CONV5_PAIRS");
       return e && e[0] == '1';
     }();
-    if (!pairs_kernel && w >= c4_box(KH))
+    // 512-column CTAs need a grid of at least ~2 waves (config 3 / 5 sizes);
+    // small images stay on the 128-column pair kernel
+    const int64_t ctas = batch * ((w - KW + 1 + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols)) *
+                         ((h - KH + 1 + 255) / 256);
+    if (!pairs_kernel && w >= c4_box(KH) && ctas >= 2 * sm_count())
       return exact ? launch_cols4<KH, true>(x, batch, h, w, f, y, st)
                    : launch_cols4<KH, false>(x, batch, h, w, f, y, st);
   }
