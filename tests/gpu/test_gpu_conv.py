@@ -53,6 +53,20 @@ def test_runtime_k_register_blocked_kernel(kh, kw, n, h, w):
     assert O.normwise_error(fast, ref64) <= O.north_star_tol(max(kh, kw))
 
 
+@pytest.mark.parametrize("k", [5, 7])
+def test_four_column_kernels_on_large_grids(k):
+    # conv2d_cols4_kernel<5 / 7>: grids of >= 2 waves of 512-column CTAs, ragged
+    # right edge (ow % 4 != 0) and a partial last row segment
+    x = rand(k + 700, (64, 261, 1031))
+    f = rand(k + 701, (k, k))
+    xd = torch.from_numpy(x).cuda()
+    got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
+    assert np.array_equal(got, O.conv2d_batched(x, f))
+    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    ref64 = np.stack([O.oracle_conv2d(img, f) for img in x[:2]])
+    assert O.normwise_error(fast[:2], ref64) <= O.north_star_tol(k)
+
+
 @pytest.mark.parametrize("k", [9, 11, 13, 15, 17, 21])
 def test_rotating_4col_kernels(k):
     # conv2d_rot4_kernel<K>: large batches of images (>= one wave of 512-col CTAs)
