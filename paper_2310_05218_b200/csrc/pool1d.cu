@@ -27,6 +27,8 @@ int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k,
                cudaStream_t st);
 int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                 cudaStream_t st);
+int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st);
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
@@ -429,9 +431,15 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
   }
   // wide windows: O(1) per output -- prefix sums (fast mode) or the exact
   // van Herk / Gil-Werman max.  For 64 < k <= 256 the striped register
-  // doubling is still the faster exact max on B200 (k = 255: 130 us vs
-  // 179 us, tools/pool_sweep.py), so the vHGW kernel serves k > 256
+  // doubling is still the faster exact max on B200 (k = 255 before the aligned
+  // kernel: 179 us unaligned vHGW vs 130 us doubling), so that kernel serves k > 256
   // (SC_POOL_MAX_WIDE_MIN moves the threshold).
+  // k = B - 1 or B (B = 128 / 256 / 512): the aligned-block van Herk /
+  // Gil-Werman max, ~7 instructions per output (pool_block.cu)
+  if constexpr (kOp == SC_POOL_MAX) {
+    const int rc = pool1d_block_max(x, batch, length, k, y, st);
+    if (rc != 1) return rc;
+  }
   static const int max_wide_min = [] {
     const char* e = getenv("SC_POOL_MAX_WIDE_MIN");
     return e ? atoi(e) : 257;

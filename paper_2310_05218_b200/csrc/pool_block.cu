@@ -1,0 +1,274 @@
+// Aligned-block sliding-window max for windows of k = B - 1 or B samples,
+// B in {128, 256, 512} (BASELINE config 2's k = 255 sweep point; replaces
+// pooling.py:60-78 for those windows, bit-exact).
+//
+// Van Herk / Gil-Werman with the blocks aligned to the register layout: a
+// warp holds a window of 1,024 samples, lane l the 32 CONSECUTIVE samples
+// [32 l, 32 l + 32) (read from the swizzled TMA tile with four conflict-free
+// LDS.128 ... one 128-byte row per lane), so a block of B samples is B / 32
+// whole lanes.  Per lane: a 31-step prefix max P and suffix max S in
+// registers, then one segmented shuffle scan of the lane aggregates inside
+// each block (log2(B/32) steps, once per lane, not per sample).  Output
+// i = 32 l + r is max(S(i), P(i + k - 1)); P(i + k - 1) sits a compile-time
+// (lane, register) offset away, one __shfl_down_sync per output.  About 7
+// instructions per output against ~40 for the striped log2(k) doubling
+// (pool1d.cu), so the kernel is left HBM-bound.
+//
+// Windows that fall inside one block (i on a block start, or i one past it
+// when k = B - 1) take P or S alone.  Every combine is mx(earlier, later);
+// with np.maximum's tie rule (common.cuh np_max) that is the rightmost
+// maximal element, which is what the reference's doubling order yields.
+// The fast pass uses max.NaN; a warp whose outputs include a zero (the only
+// case -- a +0/-0 tie -- where the two rules can differ) re-reads its window
+// and redoes it with np_max.
+//
+// Tiles of 8 warps x (1024 - B) outputs arrive by one 2-D TMA box each in a
+// 2-deep ring (no producer warp: the last warp done with a slot refills it),
+// two 8-warp CTAs per SM, CTAs own contiguous runs of tiles; outputs are
+// staged through padded shared memory and written with coalesced stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace sc {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kT = 32;           // consecutive samples per lane
+constexpr int kWin = 32 * kT;    // samples per warp window
+constexpr int kNbuf = 2;
+constexpr int kPitch = kT + 4;   // staging row (floats), conflict-free STS.128
+
+template <int B>
+struct Geo {
+  static constexpr int V = kWin - B;                         // outputs per warp
+  static constexpr int kOutLanes = V / 32;                   // lanes holding outputs
+  static constexpr int kRows = ((kWarps - 1) * V + kWin) / 32;  // TMA box rows
+  static constexpr int kBuf = (kRows * 128 + 1023) / 1024 * 1024;
+  static constexpr int kStage = kOutLanes * kPitch;          // floats per warp
+  static_assert(kRows <= 256, "TMA box rows");
+};
+
+template <bool kExact>
+__device__ __forceinline__ float mx(float a, float b) {  // a earlier, b later
+  if constexpr (kExact) return np_max(a, b);
+  else return max_nan(a, b);
+}
+
+// Reads the lane's 32 samples (one swizzled 128-byte row of the tile),
+// computes y(32 lane + r) and writes the outputs of lanes < V/32 to the
+// warp's staging rows; returns whether a valid output was zero.
+template <int B, int K, bool kEx>
+__device__ __forceinline__ bool block_max(const unsigned char* rowp, int swz, int lane,
+                                          float* stage_row, int lim) {
+  constexpr int LB = B / 32;               // lanes per block
+  constexpr int m = (K - 1) / 32, c = (K - 1) % 32;
+  constexpr int kOutLanes = (kWin - B) / 32;
+  const float kId = -__int_as_float(0x7f800000);
+  float P[kT], S[kT];
+#pragma unroll
+  for (int q = 0; q < kT / 4; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(rowp + ((q ^ swz) << 4));
+    S[4 * q] = v.x;
+    S[4 * q + 1] = v.y;
+    S[4 * q + 2] = v.z;
+    S[4 * q + 3] = v.w;
+  }
+  P[0] = S[0];
+#pragma unroll
+  for (int j = 1; j < kT; ++j) P[j] = mx<kEx>(P[j - 1], S[j]);     // lane prefix
+#pragma unroll
+  for (int j = kT - 2; j >= 0; --j) S[j] = mx<kEx>(S[j], S[j + 1]);  // lane suffix
+  // inclusive segmented scans of the lane aggregates inside each block
+  // (lane-uniform selects, no divergence)
+  const int lb = lane % LB;
+  float pv = P[kT - 1], sv = S[0];
+#pragma unroll
+  for (int d = 1; d < LB; d <<= 1) {
+    const float up = __shfl_up_sync(0xffffffffu, pv, d, LB);
+    const float dn = __shfl_down_sync(0xffffffffu, sv, d, LB);
+    pv = lb >= d ? mx<kEx>(up, pv) : pv;
+    sv = lb + d < LB ? mx<kEx>(sv, dn) : sv;
+  }
+  // exclusive aggregates; identity (-inf) at the block edges
+  float pe = __shfl_up_sync(0xffffffffu, pv, 1, LB);
+  float se = __shfl_down_sync(0xffffffffu, sv, 1, LB);
+  pe = lb > 0 ? pe : kId;
+  se = lb < LB - 1 ? se : kId;
+#pragma unroll
+  for (int j = 0; j < kT; ++j) P[j] = mx<kEx>(pe, P[j]);
+#pragma unroll
+  for (int j = 0; j < kT; ++j) S[j] = mx<kEx>(S[j], se);
+  // y(i) = mx(S(i), P(i + K - 1)); P(i + K - 1) of output register r lives in
+  // register (r + c) % 32 of lane + m (+1 when r + c wraps)
+  bool zero = false;
+#pragma unroll
+  for (int q = 0; q < kT / 4; ++q) {
+    float o[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = 4 * q + u;
+      float pj = (r + c < kT) ? __shfl_down_sync(0xffffffffu, P[(r + c) % kT], m)
+                              : __shfl_down_sync(0xffffffffu, P[(r + c) % kT], m + 1);
+      float si = S[r];
+      if (r == 0) si = lb == 0 ? kId : si;                   // window in one block: P alone
+      if (r > 0 && r == B - K) pj = lb == 0 ? kId : pj;      // ends on the block end: S alone
+      o[u] = mx<kEx>(si, pj);
+      if constexpr (!kEx) zero |= (o[u] == 0.0f) && (kT * lane + r < lim);
+    }
+    if (lane < kOutLanes)
+      *reinterpret_cast<float4*>(stage_row + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  return zero;
+}
+
+// kNbuf-deep TMA ring without a producer warp: the first load of each slot
+// is issued up front, and the LAST warp to finish with a slot (a shared
+// counter) refills it with the CTA's next tile at once.
+template <int B, int K>
+__global__ void __launch_bounds__(32 * kWarps, 2)
+    pool_block_max_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
+                          int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
+                          int tiles_per_cta) {
+  using G = Geo<B>;
+  constexpr int V = G::V;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kNbuf];
+  __shared__ int done_cnt[kNbuf];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  float* stage_all = reinterpret_cast<float*>(base + kNbuf * G::kBuf);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned tpr = (unsigned)tiles_per_row;
+  const unsigned t_begin = blockIdx.x * (unsigned)tiles_per_cta;
+  const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
+  auto issue = [&](unsigned t, int b) {
+    const unsigned row = t / tpr;
+    const unsigned s0 = (t - row * tpr) * (unsigned)(kWarps * V);
+    mbar_arrive_expect_tx(&full_bar[b], G::kRows * 128);
+    tma_load_3d(base + b * G::kBuf, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
+  };
+  if (tid == 0) {
+    prefetch_tmap(&tmap);
+    for (int i = 0; i < kNbuf; ++i) {
+      mbar_init(&full_bar[i], 1);
+      done_cnt[i] = 0;
+    }
+    fence_mbar_init();
+    for (int i = 0; i < kNbuf && t_begin + i < nt; ++i) issue(t_begin + i, i);
+  }
+  __syncthreads();
+
+  const int row0 = (warp * V) / 32 + lane;  // this lane's 128-byte row in the tile
+  float* stage = stage_all + warp * G::kStage;
+  int it = 0;
+  for (unsigned t = t_begin; t < nt; ++t, ++it) {
+    const int b = it % kNbuf;
+    mbar_wait(&full_bar[b], (it / kNbuf) & 1);
+    const unsigned char* rowp = base + b * G::kBuf + row0 * 128;
+    const unsigned row = t / tpr;
+    const unsigned o_in_row = (t - row * tpr) * (unsigned)(kWarps * V) + warp * V;
+    const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
+    float* srow = stage + lane * kPitch;
+    const bool zero = block_max<B, K, false>(rowp, row0 & 7, lane, srow, lim);
+    if (__any_sync(0xffffffffu, zero)) {  // rare: redo with np.maximum's rule
+      __syncwarp();
+      block_max<B, K, true>(rowp, row0 & 7, lane, srow, lim);
+    }
+    __syncwarp();
+    if (lane == 0) {  // done with slot b: the last warp refills it
+      __threadfence_block();
+      if (atomicAdd(&done_cnt[b], 1) == kWarps - 1) {
+        done_cnt[b] = 0;
+        if (t + kNbuf < nt) {
+          fence_proxy_async();
+          issue(t + kNbuf, b);
+        }
+      }
+    }
+    float* yr = y + (int64_t)row * out_len + o_in_row + lane;
+    const float* sp = stage + lane;
+    if (lim == V) {
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm) yr[32 * mm] = sp[mm * kPitch];
+    } else {
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm)
+        if (32 * mm + lane < lim) yr[32 * mm] = sp[mm * kPitch];
+    }
+    __syncwarp();  // staging reused by the next tile
+  }
+}
+
+template <int B, int K>
+int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st) {
+  using G = Geo<B>;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[3] = {32, (cuuint64_t)(length / 32), (cuuint64_t)batch};
+  cuuint64_t strides[2] = {128, (cuuint64_t)length * sizeof(float)};
+  cuuint32_t box[3] = {32, (cuuint32_t)G::kRows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "pool block tensor map encode failed");
+  const int64_t out_len = length - K + 1;
+  const int64_t tiles_per_row = (out_len + kWarps * G::V - 1) / (kWarps * G::V);
+  const int64_t n_tiles = tiles_per_row * batch;
+  if (n_tiles >= 0x7fffffff) return 1;
+  const size_t smem = 1024 + kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    SC_CUDA(cudaFuncSetAttribute(pool_block_max_kernel<B, K>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  // one wave of 2 CTAs per SM, each a balanced contiguous run of tiles
+  // (measured: ~4% faster than 8-tile CTAs over 4-5 waves); env override
+  static const int tpc_env = [] {
+    const char* e = getenv("SC_POOL_BLOCK_TPC");
+    const int n = e ? atoi(e) : 0;
+    return (n >= 1 && n <= 4096) ? n : 0;
+  }();
+  const int64_t slots = 2 * (int64_t)sm_count();
+  // (B = 128, 9% more tiles per byte: 8-tile CTAs measured 5% faster)
+  const int tpc = tpc_env ? tpc_env
+                  : B == 128 ? 8
+                             : (int)std::max<int64_t>(1, (n_tiles + slots - 1) / slots);
+  const int64_t grid = (n_tiles + tpc - 1) / tpc;
+  pool_block_max_kernel<B, K><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+      map, y, out_len, tiles_per_row, n_tiles, tpc);
+  SC_LAUNCH_CHECK("pool_block_max_kernel");
+  return SC_OK;
+}
+
+}  // namespace
+
+// Exact sliding max for k in {127, 128, 255, 256, 511, 512} on 16-byte
+// aligned signals whose length is a multiple of 32 (>= 1,024).  Returns
+// SC_OK / an error if it ran, 1 if it does not apply.
+int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st) {
+  static const bool off = getenv("SC_POOL_NO_BLOCK") != nullptr;
+  if (off || reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || length < kWin ||
+      length / 32 > 0x7fffffff || batch > 0x7fffffff)
+    return 1;
+  switch (k) {
+    case 127: return launch<128, 127>(x, batch, length, y, st);
+    case 128: return launch<128, 128>(x, batch, length, y, st);
+    case 255: return launch<256, 255>(x, batch, length, y, st);
+    case 256: return launch<256, 256>(x, batch, length, y, st);
+    case 511: return launch<512, 511>(x, batch, length, y, st);
+    case 512: return launch<512, 512>(x, batch, length, y, st);
+    default: return 1;
+  }
+}
+
+}  // namespace sc

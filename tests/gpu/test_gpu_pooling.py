@@ -40,7 +40,7 @@ def test_config2_full_size(cfg2, op, k):
 
 
 @pytest.mark.parametrize("k", list(range(1, 40)) + [47, 63, 64, 65, 100, 127, 128, 129, 200, 255,
-                                                     256, 257, 300, 511, 1000, 4097, 9000])
+                                                     256, 257, 300, 511, 512, 1000, 4097, 9000])
 @pytest.mark.parametrize("n", [12_345, 8192, 544])
 def test_every_window_branch(k, n):
     rng = np.random.default_rng(k)
@@ -82,7 +82,7 @@ def test_reference_kats():
 
 
 @pytest.mark.parametrize("n", [5000, 5024])
-@pytest.mark.parametrize("k", [2, 3, 16, 17, 33, 64, 255, 300])
+@pytest.mark.parametrize("k", [2, 3, 16, 17, 33, 64, 127, 128, 255, 256, 300, 511, 512])
 def test_max_nan_and_signed_zero_semantics(k, n):
     rng = np.random.default_rng(99 + k)
     x = rng.standard_normal((2, n), dtype=np.float32)
