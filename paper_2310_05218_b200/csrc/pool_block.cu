@@ -23,13 +23,12 @@
 // and redoes it with np_max.
 //
 // Tiles of 8 warps x (1024 - B) outputs arrive by one 2-D TMA box each in a
-// 2-deep ring (no producer warp: the last warp done with a slot refills it),
-// two 8-warp CTAs per SM, CTAs own contiguous runs of tiles; outputs are
+// 2- or 3-deep ring (no producer warp: the last warp done with a slot refills
+// it), two 8-warp CTAs per SM, CTAs own contiguous runs of tiles; outputs are
 // staged through padded shared memory and written with coalesced stores.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
-#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -41,7 +40,6 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kT = 32;           // consecutive samples per lane
 constexpr int kWin = 32 * kT;    // samples per warp window
-constexpr int kNbuf = 2;
 constexpr int kPitch = kT + 4;   // staging row (floats), conflict-free STS.128
 
 template <int B>
@@ -51,6 +49,8 @@ struct Geo {
   static constexpr int kRows = ((kWarps - 1) * V + kWin) / 32;  // TMA box rows
   static constexpr int kBuf = (kRows * 128 + 1023) / 1024 * 1024;
   static constexpr int kStage = kOutLanes * kPitch;          // floats per warp
+  // ring depth: 3 where two CTAs per SM still fit in shared memory
+  static constexpr int kNbuf = B == 128 ? 2 : 3;
   static_assert(kRows <= 256, "TMA box rows");
 };
 
@@ -138,6 +138,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
   using G = Geo<B>;
   constexpr int V = G::V;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  constexpr int kNbuf = G::kNbuf;
   __shared__ __align__(8) uint64_t full_bar[kNbuf];
   __shared__ int done_cnt[kNbuf];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -223,25 +224,21 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   const int64_t tiles_per_row = (out_len + kWarps * G::V - 1) / (kWarps * G::V);
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
-  const size_t smem = 1024 + kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
+  const size_t smem = 1024 + G::kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
   static bool attr = false;
   if (!attr) {
     SC_CUDA(cudaFuncSetAttribute(pool_block_max_kernel<B, K>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  // one wave of 2 CTAs per SM, each a balanced contiguous run of tiles
-  // (measured: ~4% faster than 8-tile CTAs over 4-5 waves); env override
+  // contiguous runs of tiles per CTA (tools/pbcheck.py sweep on config 2:
+  // 6 tiles for B = 256, 8 otherwise); env override
   static const int tpc_env = [] {
     const char* e = getenv("SC_POOL_BLOCK_TPC");
     const int n = e ? atoi(e) : 0;
     return (n >= 1 && n <= 4096) ? n : 0;
   }();
-  const int64_t slots = 2 * (int64_t)sm_count();
-  // (B = 128, 9% more tiles per byte: 8-tile CTAs measured 5% faster)
-  const int tpc = tpc_env ? tpc_env
-                  : B == 128 ? 8
-                             : (int)std::max<int64_t>(1, (n_tiles + slots - 1) / slots);
+  const int tpc = tpc_env ? tpc_env : B == 256 ? 6 : 8;
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   pool_block_max_kernel<B, K><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
       map, y, out_len, tiles_per_row, n_tiles, tpc);
