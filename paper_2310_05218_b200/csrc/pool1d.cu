@@ -424,6 +424,12 @@ template <int kOp>
 int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode, float* y,
              cudaStream_t st) {
   const bool exact = mode == SC_MODE_EXACT;
+  // k = B - 1 or B (B = 64 / 128 / 256 / 512): the aligned-block van Herk /
+  // Gil-Werman max, ~7 instructions per output (pool_block.cu)
+  if constexpr (kOp == SC_POOL_MAX) {
+    const int rc = pool1d_block_max(x, batch, length, k, y, st);
+    if (rc != 1) return rc;
+  }
   // TMA-staged blocked kernel: bit-exact doubling order, so it serves both modes
   {
     const int rc = pool1d_tma(kOp, x, batch, length, k, y, st);
@@ -434,12 +440,6 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
   // doubling is still the faster exact max on B200 (k = 255 before the aligned
   // kernel: 179 us unaligned vHGW vs 130 us doubling), so that kernel serves k > 256
   // (SC_POOL_MAX_WIDE_MIN moves the threshold).
-  // k = B - 1 or B (B = 128 / 256 / 512): the aligned-block van Herk /
-  // Gil-Werman max, ~7 instructions per output (pool_block.cu)
-  if constexpr (kOp == SC_POOL_MAX) {
-    const int rc = pool1d_block_max(x, batch, length, k, y, st);
-    if (rc != 1) return rc;
-  }
   static const int max_wide_min = [] {
     const char* e = getenv("SC_POOL_MAX_WIDE_MIN");
     return e ? atoi(e) : 257;

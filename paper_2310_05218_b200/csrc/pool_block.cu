@@ -1,5 +1,5 @@
 // Aligned-block sliding-window max for windows of k = B - 1 or B samples,
-// B in {128, 256, 512} (BASELINE config 2's k = 255 sweep point; replaces
+// B in {64, 128, 256, 512} (BASELINE config 2's k = 255 sweep point; replaces
 // pooling.py:60-78 for those windows, bit-exact).
 //
 // Van Herk / Gil-Werman with the blocks aligned to the register layout: a
@@ -50,7 +50,7 @@ struct Geo {
   static constexpr int kBuf = (kRows * 128 + 1023) / 1024 * 1024;
   static constexpr int kStage = kOutLanes * kPitch;          // floats per warp
   // ring depth: 3 where two CTAs per SM still fit in shared memory
-  static constexpr int kNbuf = B == 128 ? 2 : 3;
+  static constexpr int kNbuf = B <= 128 ? 2 : 3;
   static_assert(kRows <= 256, "TMA box rows");
 };
 
@@ -248,7 +248,7 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
 
 }  // namespace
 
-// Exact sliding max for k in {127, 128, 255, 256, 511, 512} on 16-byte
+// Exact sliding max for k in {63, 64, 127, 128, 255, 256, 511, 512} on 16-byte
 // aligned signals whose length is a multiple of 32 (>= 1,024).  Returns
 // SC_OK / an error if it ran, 1 if it does not apply.
 int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
@@ -258,6 +258,8 @@ int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, f
       length / 32 > 0x7fffffff || batch > 0x7fffffff)
     return 1;
   switch (k) {
+    case 63: return launch<64, 63>(x, batch, length, y, st);
+    case 64: return launch<64, 64>(x, batch, length, y, st);
     case 127: return launch<128, 127>(x, batch, length, y, st);
     case 128: return launch<128, 128>(x, batch, length, y, st);
     case 255: return launch<256, 255>(x, batch, length, y, st);
