@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslideconv_b200.so")
+# SLIDECONV_B200_LIB: an alternative build of the same ABI (A/B timing tools)
+LIB_PATH = os.environ.get("SLIDECONV_B200_LIB") or os.path.join(_HERE, "libslideconv_b200.so")
 
 SC_OK = 0
 SC_ERR_SHAPE = -1

@@ -110,6 +110,43 @@ __device__ __forceinline__ void div_all_by_k(float (&v)[N], float k, float r) {
   }
 }
 
+// Output stores of the FP32-bound conv kernels.  A lane stores C
+// consecutive outputs per row.  The column range check is hoisted out of the
+// row loop into a store mode computed from warp-uniform values only (kernel
+// parameters and the warp's first column), so the per-row test compiles to a
+// uniform branch: a divergent per-row branch splits the unrolled row bodies
+// into separate scheduling regions, a copy of the row loop per mode thrashes
+// the instruction cache when warps of one SM run different copies, and
+// 64-bit per-column compares with predicated stores cost ~25 instructions
+// per row (ISETP.EX pairs and an R2UR descriptor copy per predicated STG).
+//   pairs:     the warp's 32 C columns are in range and the row pitch and
+//              base are 8-byte aligned -> C / 2 STG.64;
+//   otherwise: the lane's count of in-range columns, predicated STG.32.
+struct OutCols {
+  bool pairs;  // warp-uniform (broadcast by a shuffle so the compiler knows it)
+  int nv;      // this lane's in-range columns (used when !pairs)
+};
+template <int C>
+__device__ __forceinline__ OutCols out_cols(const float* y, int64_t ow, int64_t wcol0,
+                                            int64_t gcol) {
+  const bool pairs = C % 2 == 0 && wcol0 + 32 * C <= ow &&
+                     ((reinterpret_cast<uintptr_t>(y) | (uintptr_t)(ow * 4)) & 7) == 0;
+  return {__shfl_sync(0xffffffffu, (int)pairs, 0) != 0,
+          (int)max((int64_t)0, min((int64_t)C, ow - gcol))};
+}
+
+template <int C>
+__device__ __forceinline__ void store_cols(float* p, const OutCols& m, const float (&v)[C]) {
+  if (m.pairs) {
+#pragma unroll
+    for (int c = 0; c < C; c += 2) *reinterpret_cast<float2*>(p + c) = make_float2(v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+      if (c < m.nv) p[c] = v[c];
+  }
+}
+
 // ------------------------------------------------------ mbarrier / TMA PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   const int col = warp * kC4Cols + 4 * lane;       // first of the lane's 4 columns
   const int64_t gcol = (int64_t)c0 + col;
   float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
+  const OutCols nvc = out_cols<4>(y, ow, c0 + warp * kC4Cols, gcol);
   // scalar FFMA (fast) / FMUL + FADD (exact) accumulators: a packed FFMA2
   // variant needs the odd-offset input pairs re-packed every row and measured
   // slower (9.2 vs 7.5 ms) -- with ~97 % FFMAs issue slots are not the limit
@@ -341,10 +343,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
         for (int q = 0; q < K + 3; ++q) cur[q] = nxt[q];
         const int t = s * kC4RS + rr;  // input row relative to r0
         if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
-          const int sl = (u + 1) % K;
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (gcol + c < ow) ynext[c] = acc[sl][c];
+          store_cols<4>(ynext, nvc, acc[(u + 1) % K]);
         }
         ynext += ow;
       }
@@ -418,6 +417,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   const int col = warp * 32 * C + C * lane;
   const int64_t gcol = (int64_t)c0 + col;
   float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
+  const OutCols nvc = out_cols<C>(y, ow, c0 + warp * 32 * C, gcol);
   // acc[j]: output row t - (K - 1) + j for the input row t just consumed
   float acc[K][C];
 #pragma unroll
@@ -467,9 +467,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
       }
       // acc[0] (output row t - K + 1) is complete
       if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
-#pragma unroll
-        for (int c = 0; c < C; ++c)
-          if (gcol + c < ow) ynext[c] = acc[0][c];
+        store_cols<C>(ynext, nvc, acc[0]);
       }
       ynext += ow;
 #pragma unroll
