@@ -19,7 +19,10 @@
 //     slides an 8-value register window in steps of 4 taps: one LDS.128 of
 //     inputs and, per live output row, one broadcast LDS.128 of 4 taps for
 //     16 FMAs -- ~14 FMAs per shared-memory load, so the FP32 pipe, not
-//     shared memory, is the limit.
+//     shared memory, is the limit.  The taps are stored block-major so the
+//     8 rows' tap loads are immediate offsets from one pointer, and three
+//     input blocks rotate through the window so no register moves are
+//     needed (k = 25..63: +8-13 % over row-major taps with a shifted window).
 //   * kExact: __fmul_rn + __fadd_rn, and every output still accumulates in
 //     the reference's order (j ascending as q ascends, i ascending within a
 //     row, from 0): bit-identical to _accumulate_taps (reference.py:15-23).
@@ -41,10 +44,17 @@ __host__ __device__ constexpr int pad4(int v) { return (v + 3) & ~3; }
 // tile row pitch: columns read up to 124 + 3 + (pad4(kw) - 4) + 4
 __host__ __device__ constexpr int tile_pitch(int kw) { return kTileCols + pad4(kw) + 4; }
 
+// one 4-tap block for one output row: 16 FMAs against the 8-value window w
 template <bool kExact>
-__device__ __forceinline__ void mac4(float (&acc)[kC], float t, const float (&xw)[12], int off) {
+__device__ __forceinline__ void block4(float (&acc)[kC], const float4 t, const float (&w)[8]) {
 #pragma unroll
-  for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t, xw[c + off]);
+  for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t.x, w[c]);
+#pragma unroll
+  for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t.y, w[c + 1]);
+#pragma unroll
+  for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t.z, w[c + 2]);
+#pragma unroll
+  for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t.w, w[c + 3]);
 }
 
 // the filter travels in the launch parameters (16 KiB < the 32 KiB limit):
@@ -65,7 +75,11 @@ __global__ void __launch_bounds__(32 * kWarps)
   extern __shared__ __align__(16) float smem[];
   const int kwp = pad4(kw);
   const int pitch = tile_pitch(kw);
-  float* taps = smem;                        // [kh][kwp], zero padded
+  // taps, block-major: 4-tap block b of filter row j at taps[(b * kh + j) * 4],
+  // so the blocks of the (up to 8) filter rows one input row meets sit at
+  // compile-time offsets -16 r bytes from one pointer (no per-row address
+  // arithmetic in the inner loop); zero padded past kw
+  float* taps = smem;
   float* tile = smem + kh * kwp;             // [kTileRows + kh - 1][pitch]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = blockIdx.y * kTileRows, c0 = blockIdx.x * kTileCols;
@@ -74,7 +88,7 @@ __global__ void __launch_bounds__(32 * kWarps)
 
   for (int e = threadIdx.x; e < kh * kwp; e += blockDim.x) {
     const int j = e / kwp, i = e - j * kwp;
-    taps[e] = i < kw ? f[j * kw + i] : 0.0f;
+    taps[((i >> 2) * kh + j) * 4 + (i & 3)] = i < kw ? f[j * kw + i] : 0.0f;
   }
   const int rows = kTileRows + kh - 1;
   for (int rr = warp; rr < rows; rr += kWarps) {
@@ -94,7 +108,8 @@ __global__ void __launch_bounds__(32 * kWarps)
 #pragma unroll
     for (int c = 0; c < kC; ++c) acc[r][c] = 0.0f;
 
-  const int kfull = kw & ~3, krem = kw & 3;
+  const int nfull = kw >> 2, krem = kw & 3;
+  const int bstride = kh * 4;  // floats between consecutive tap blocks of one row
   const float* band = tile + warp * kR * pitch + kC * lane;
   // One input row: ALL = every output row of the band is live (kR-1 <= q <=
   // kh-1), so the r loop has no branches and the 8 tap loads can be hoisted
@@ -102,50 +117,61 @@ __global__ void __launch_bounds__(32 * kWarps)
   auto row = [&](auto all_tag, int q) {
     constexpr bool ALL = decltype(all_tag)::value;
     const int rlo = max(0, q - kh + 1), rhi = min(kR - 1, q);
-    const float* xr = band + q * pitch;
-    const float* tq = taps + q * kwp;  // row j = q - r at tq - r * kwp
-    float xw[12];
-    *reinterpret_cast<float4*>(&xw[0]) = *reinterpret_cast<const float4*>(xr);
-    // one 4-tap block against the window starting at xw[base]
-    auto block = [&](int i0, auto base_tag) {
-      constexpr int B = decltype(base_tag)::value;
+    const float4* xr = reinterpret_cast<const float4*>(band + q * pitch);
+    const float* tq = taps + q * 4;  // block 0 of filter row q; row q - r at tq - 4 r
+    // one 4-tap block against the window (u, v) of two 4-input blocks
+    auto blk = [&](const float4 u, const float4 v, const float* tb) {
+      const float wv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         if (!ALL && (r < rlo || r > rhi)) continue;  // warp-uniform
-        const float4 t = *reinterpret_cast<const float4*>(tq - r * kwp + i0);
-        mac4<kExact>(acc[r], t.x, xw, B + 0);
-        mac4<kExact>(acc[r], t.y, xw, B + 1);
-        mac4<kExact>(acc[r], t.z, xw, B + 2);
-        mac4<kExact>(acc[r], t.w, xw, B + 3);
+        block4<kExact>(acc[r], *reinterpret_cast<const float4*>(tb - 4 * r), wv);
       }
     };
-    int i0 = 0;
-    // two blocks per trip: windows xw[0..7] then xw[4..11], then one shift
-    for (; i0 + 8 <= kfull; i0 += 8) {
-      *reinterpret_cast<float4*>(&xw[4]) = *reinterpret_cast<const float4*>(xr + i0 + 4);
-      *reinterpret_cast<float4*>(&xw[8]) = *reinterpret_cast<const float4*>(xr + i0 + 8);
-      block(i0, std::integral_constant<int, 0>{});
-      block(i0 + 4, std::integral_constant<int, 4>{});
-#pragma unroll
-      for (int v = 0; v < 4; ++v) xw[v] = xw[v + 8];
+    // three input blocks rotate through (A, B), (B, C), (C, A): no moves
+    float4 A = xr[0], B, C;
+    int b = 0;
+    for (; b + 3 <= nfull; b += 3) {
+      B = xr[b + 1];
+      blk(A, B, tq);
+      tq += bstride;
+      C = xr[b + 2];
+      blk(B, C, tq);
+      tq += bstride;
+      A = xr[b + 3];
+      blk(C, A, tq);
+      tq += bstride;
     }
-    if (i0 < kfull) {
-      *reinterpret_cast<float4*>(&xw[4]) = *reinterpret_cast<const float4*>(xr + i0 + 4);
-      block(i0, std::integral_constant<int, 0>{});
-#pragma unroll
-      for (int v = 0; v < 4; ++v) xw[v] = xw[v + 4];
-      i0 += 4;
+    if (b < nfull) {
+      B = xr[b + 1];
+      blk(A, B, tq);
+      tq += bstride;
+      A = B;
+      ++b;
+      if (b < nfull) {
+        B = xr[b + 1];
+        blk(A, B, tq);
+        tq += bstride;
+        A = B;
+        ++b;
+      }
     }
     if (krem) {  // last partial block: only the real taps (a zero tap times
                  // an inf/NaN input would poison the result)
-      *reinterpret_cast<float4*>(&xw[4]) = *reinterpret_cast<const float4*>(xr + i0 + 4);
+      B = xr[b + 1];
+      const float wv[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         if (!ALL && (r < rlo || r > rhi)) continue;
-        const float4 t = *reinterpret_cast<const float4*>(tq - r * kwp + i0);
-        mac4<kExact>(acc[r], t.x, xw, 0);
-        if (krem > 1) mac4<kExact>(acc[r], t.y, xw, 1);
-        if (krem > 2) mac4<kExact>(acc[r], t.z, xw, 2);
+        const float4 t = *reinterpret_cast<const float4*>(tq - 4 * r);
+#pragma unroll
+        for (int c = 0; c < kC; ++c) acc[r][c] = mac<kExact>(acc[r][c], t.x, wv[c]);
+        if (krem > 1)
+#pragma unroll
+          for (int c = 0; c < kC; ++c) acc[r][c] = mac<kExact>(acc[r][c], t.y, wv[c + 1]);
+        if (krem > 2)
+#pragma unroll
+          for (int c = 0; c < kC; ++c) acc[r][c] = mac<kExact>(acc[r][c], t.z, wv[c + 2]);
       }
     }
   };
