@@ -206,6 +206,19 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity,
   }
 }
 
+// 4-byte cp.async global -> shared (zero-fill when pred is false)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool pred) {
+  const int n = pred ? 4 : 0;  // zero-fill when predicated off
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // 3-D tiled TMA load global -> shared, completion on an mbarrier.
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar,
                                             int c0, int c1, int c2) {

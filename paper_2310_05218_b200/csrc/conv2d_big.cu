@@ -35,18 +35,26 @@ namespace sc {
 namespace {
 
 constexpr int kR = 8;                 // output rows per thread
-constexpr int kC = 4;                 // output columns per thread
-constexpr int kTileCols = 32 * kC;                // 128
+constexpr int kC = 4;                 // output columns per thread and column group
 constexpr int kMaxK = 64;
 
+// kG column groups: lane l owns columns 4l .. 4l+3 of each 128-column group
+// (conflict-free LDS.128 per group); a broadcast tap load feeds 16 kG FMAs.
+// kG = 2 (8 x 8 outputs per thread, ~120 registers) measured 10-25 % slower
+// than kG = 1 on the 11..63 sweep (fewer resident warps), so only kG = 1 is
+// instantiated.
+__host__ __device__ constexpr int tile_cols(int g) { return 128 * g; }
 __host__ __device__ constexpr int tile_rows(int warps) { return kR * warps; }
 __host__ __device__ constexpr int pad4(int v) { return (v + 3) & ~3; }
-// tile row pitch: columns read up to 124 + 3 + (pad4(kw) - 4) + 4
-__host__ __device__ constexpr int tile_pitch(int kw) { return kTileCols + pad4(kw) + 4; }
+// tile row pitch: columns read up to 128 (g - 1) + 124 + 3 + (pad4(kw) - 4) + 4
+__host__ __device__ constexpr int tile_pitch(int kw, int g) { return tile_cols(g) + pad4(kw) + 4; }
+__host__ __device__ constexpr size_t big_smem(int kh, int kw, int warps, int g) {
+  return ((size_t)kh * pad4(kw) + (size_t)(tile_rows(warps) + kh - 1) * tile_pitch(kw, g)) * 4;
+}
 
 // one 4-tap block for one output row: 16 FMAs against the 8-value window w
 template <bool kExact>
-__device__ __forceinline__ void block4(float (&acc)[kC], const float4 t, const float (&w)[8]) {
+__device__ __forceinline__ void block4(float* acc, const float4 t, const float (&w)[8]) {
 #pragma unroll
   for (int c = 0; c < kC; ++c) acc[c] = mac<kExact>(acc[c], t.x, w[c]);
 #pragma unroll
@@ -65,16 +73,17 @@ struct BigTaps {
 
 // kWarps = 8 (64-row tiles, less halo, more warps per SM) for big grids;
 // 4 when a single image would leave SMs idle
-template <bool kExact, int kWarps>
+template <bool kExact, int kWarps, int kG>
 __global__ void __launch_bounds__(32 * kWarps)
     conv2d_big_kernel(const float* __restrict__ x, int h, int w,
                       const __grid_constant__ BigTaps ft, int kh, int kw, float* __restrict__ y,
                       int oh, int ow) {
   constexpr int kTileRows = tile_rows(kWarps);
+  constexpr int kTileCols = tile_cols(kG);
   const float* f = ft.f;
   extern __shared__ __align__(16) float smem[];
   const int kwp = pad4(kw);
-  const int pitch = tile_pitch(kw);
+  const int pitch = tile_pitch(kw, kG);
   // taps, block-major: 4-tap block b of filter row j at taps[(b * kh + j) * 4],
   // so the blocks of the (up to 8) filter rows one input row meets sit at
   // compile-time offsets -16 r bytes from one pointer (no per-row address
@@ -95,83 +104,97 @@ __global__ void __launch_bounds__(32 * kWarps)
     const int gr = r0 + rr;
     float* dst = tile + rr * pitch;
     const float* src = xi + (int64_t)gr * w;
+    // cp.async: every load of the fill is in flight at once (an LDG -> STS
+    // loop waits out the global latency per element: ~6 % of the kernel)
     for (int cc = lane; cc < pitch; cc += 32) {
       const int gc = c0 + cc;
-      dst[cc] = (gr < h && gc < w) ? __ldg(src + gc) : 0.0f;
+      const bool ok = gr < h && gc < w;
+      cp_async4(dst + cc, ok ? src + gc : xi, ok);
     }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
 
-  float acc[kR][kC];
+  float acc[kR][kG * kC];
 #pragma unroll
   for (int r = 0; r < kR; ++r)
 #pragma unroll
-    for (int c = 0; c < kC; ++c) acc[r][c] = 0.0f;
+    for (int c = 0; c < kG * kC; ++c) acc[r][c] = 0.0f;
 
   const int nfull = kw >> 2, krem = kw & 3;
   const int bstride = kh * 4;  // floats between consecutive tap blocks of one row
   const float* band = tile + warp * kR * pitch + kC * lane;
   // One input row: ALL = every output row of the band is live (kR-1 <= q <=
   // kh-1), so the r loop has no branches and the 8 tap loads can be hoisted
-  // ahead of the 128 FMAs; otherwise rows outside [rlo, rhi] are skipped.
+  // ahead of the FMAs; otherwise rows outside [rlo, rhi] are skipped.
   auto row = [&](auto all_tag, int q) {
     constexpr bool ALL = decltype(all_tag)::value;
     const int rlo = max(0, q - kh + 1), rhi = min(kR - 1, q);
-    const float4* xr = reinterpret_cast<const float4*>(band + q * pitch);
+    const float4* xr = reinterpret_cast<const float4*>(band + q * pitch);  // group g at + 32 g
     const float* tq = taps + q * 4;  // block 0 of filter row q; row q - r at tq - 4 r
-    // one 4-tap block against the window (u, v) of two 4-input blocks
-    auto blk = [&](const float4 u, const float4 v, const float* tb) {
-      const float wv[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+    // one 4-tap block against the windows (u[g], v[g]) of two 4-input blocks
+    auto blk = [&](const float4 (&u)[kG], const float4 (&v)[kG], const float* tb) {
+      float wv[kG][8];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        wv[g][0] = u[g].x, wv[g][1] = u[g].y, wv[g][2] = u[g].z, wv[g][3] = u[g].w;
+        wv[g][4] = v[g].x, wv[g][5] = v[g].y, wv[g][6] = v[g].z, wv[g][7] = v[g].w;
+      }
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         if (!ALL && (r < rlo || r > rhi)) continue;  // warp-uniform
-        block4<kExact>(acc[r], *reinterpret_cast<const float4*>(tb - 4 * r), wv);
+        const float4 t = *reinterpret_cast<const float4*>(tb - 4 * r);
+#pragma unroll
+        for (int g = 0; g < kG; ++g) block4<kExact>(&acc[r][g * kC], t, wv[g]);
       }
     };
+    auto ld = [&](float4 (&d)[kG], int bi) {
+#pragma unroll
+      for (int g = 0; g < kG; ++g) d[g] = xr[bi + 32 * g];
+    };
     // three input blocks rotate through (A, B), (B, C), (C, A): no moves
-    float4 A = xr[0], B, C;
+    float4 A[kG], B[kG], C[kG];
+    ld(A, 0);
     int b = 0;
     for (; b + 3 <= nfull; b += 3) {
-      B = xr[b + 1];
+      ld(B, b + 1);
       blk(A, B, tq);
       tq += bstride;
-      C = xr[b + 2];
+      ld(C, b + 2);
       blk(B, C, tq);
       tq += bstride;
-      A = xr[b + 3];
+      ld(A, b + 3);
       blk(C, A, tq);
       tq += bstride;
     }
-    if (b < nfull) {
-      B = xr[b + 1];
+    for (; b < nfull; ++b) {  // 0..2 blocks
+      ld(B, b + 1);
       blk(A, B, tq);
       tq += bstride;
-      A = B;
-      ++b;
-      if (b < nfull) {
-        B = xr[b + 1];
-        blk(A, B, tq);
-        tq += bstride;
-        A = B;
-        ++b;
-      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g) A[g] = B[g];
     }
     if (krem) {  // last partial block: only the real taps (a zero tap times
                  // an inf/NaN input would poison the result)
-      B = xr[b + 1];
-      const float wv[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+      ld(B, b + 1);
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         if (!ALL && (r < rlo || r > rhi)) continue;
         const float4 t = *reinterpret_cast<const float4*>(tq - 4 * r);
 #pragma unroll
-        for (int c = 0; c < kC; ++c) acc[r][c] = mac<kExact>(acc[r][c], t.x, wv[c]);
-        if (krem > 1)
+        for (int g = 0; g < kG; ++g) {
+          const float wv[8] = {A[g].x, A[g].y, A[g].z, A[g].w, B[g].x, B[g].y, B[g].z, B[g].w};
+          float* a = &acc[r][g * kC];
 #pragma unroll
-          for (int c = 0; c < kC; ++c) acc[r][c] = mac<kExact>(acc[r][c], t.y, wv[c + 1]);
-        if (krem > 2)
+          for (int c = 0; c < kC; ++c) a[c] = mac<kExact>(a[c], t.x, wv[c]);
+          if (krem > 1)
 #pragma unroll
-          for (int c = 0; c < kC; ++c) acc[r][c] = mac<kExact>(acc[r][c], t.z, wv[c + 2]);
+            for (int c = 0; c < kC; ++c) a[c] = mac<kExact>(a[c], t.y, wv[c + 1]);
+          if (krem > 2)
+#pragma unroll
+            for (int c = 0; c < kC; ++c) a[c] = mac<kExact>(a[c], t.z, wv[c + 2]);
+        }
       }
     }
   };
@@ -188,35 +211,45 @@ __global__ void __launch_bounds__(32 * kWarps)
     if (gr >= oh) break;
     float* yr = yi + (int64_t)gr * ow;
 #pragma unroll
-    for (int c = 0; c < kC; ++c) {
-      const int gc = c0 + kC * lane + c;
-      if (gc < ow) yr[gc] = acc[r][c];
-    }
+    for (int g = 0; g < kG; ++g)
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        const int gc = c0 + 128 * g + kC * lane + c;
+        if (gc < ow) yr[gc] = acc[r][g * kC + c];
+      }
   }
 }
 
-template <bool kExact, int kWarps>
+template <bool kExact, int kWarps, int kG>
 int launch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigTaps& taps,
                int64_t kh, int64_t kw, float* y, cudaStream_t st) {
   constexpr int kTileRows = tile_rows(kWarps);
+  constexpr int kTileCols = tile_cols(kG);
   const int64_t oh = h - kh + 1, ow = w - kw + 1;
   const int64_t gx = (ow + kTileCols - 1) / kTileCols, gy = (oh + kTileRows - 1) / kTileRows;
   if (gy > 65535) return 1;
-  const size_t smem =
-      ((size_t)kh * pad4((int)kw) + (size_t)(kTileRows + kh - 1) * tile_pitch((int)kw)) * 4;
   static bool attr = false;
   if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(conv2d_big_kernel<kExact, kWarps>,
+    SC_CUDA(cudaFuncSetAttribute(conv2d_big_kernel<kExact, kWarps, kG>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(((size_t)kMaxK * pad4(kMaxK) +
-                                        (size_t)(kTileRows + kMaxK - 1) * tile_pitch(kMaxK)) * 4)));
+                                 (int)big_smem(kMaxK, kMaxK, kWarps, kG)));
     attr = true;
   }
-  conv2d_big_kernel<kExact, kWarps>
-      <<<dim3((unsigned)gx, (unsigned)gy, (unsigned)batch), 32 * kWarps, smem, st>>>(
-          x, (int)h, (int)w, taps, (int)kh, (int)kw, y, (int)oh, (int)ow);
+  conv2d_big_kernel<kExact, kWarps, kG>
+      <<<dim3((unsigned)gx, (unsigned)gy, (unsigned)batch), 32 * kWarps,
+         big_smem((int)kh, (int)kw, kWarps, kG), st>>>(x, (int)h, (int)w, taps, (int)kh, (int)kw,
+                                                       y, (int)oh, (int)ow);
   SC_LAUNCH_CHECK("conv2d_big_kernel");
   return SC_OK;
+}
+
+template <bool kExact>
+int dispatch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigTaps& taps,
+                 int64_t kh, int64_t kw, float* y, cudaStream_t st) {
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  const int64_t ctas8 = batch * ((ow + 127) / 128) * ((oh + 63) / 64);
+  return ctas8 < 2 * sm_count() ? launch_big<kExact, 4, 1>(x, batch, h, w, taps, kh, kw, y, st)
+                                : launch_big<kExact, 8, 1>(x, batch, h, w, taps, kh, kw, y, st);
 }
 
 }  // namespace
@@ -227,14 +260,8 @@ int conv2d_big(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   if (kh > kMaxK || kw > kMaxK || batch > 65535 || h * w >= ((int64_t)1 << 31)) return 1;
   static thread_local BigTaps taps;
   std::copy(f_host, f_host + kh * kw, taps.f);
-  const int64_t oh = h - kh + 1, ow = w - kw + 1;
-  const int64_t ctas8 = batch * ((ow + kTileCols - 1) / kTileCols) * ((oh + 63) / 64);
-  const bool small = ctas8 < 2 * sm_count();
-  if (exact)
-    return small ? launch_big<true, 4>(x, batch, h, w, taps, kh, kw, y, st)
-                 : launch_big<true, 8>(x, batch, h, w, taps, kh, kw, y, st);
-  return small ? launch_big<false, 4>(x, batch, h, w, taps, kh, kw, y, st)
-               : launch_big<false, 8>(x, batch, h, w, taps, kh, kw, y, st);
+  return exact ? dispatch_big<true>(x, batch, h, w, taps, kh, kw, y, st)
+               : dispatch_big<false>(x, batch, h, w, taps, kh, kw, y, st);
 }
 
 }  // namespace sc

@@ -38,18 +38,6 @@ constexpr int kXS = 20;        // padded row stride of the staged input
 constexpr int kXChunk = kCiT * kXR * kXS;
 constexpr int kWChunk = kCiT * 9 * kCoT;
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool pred) {
-  const int n = pred ? 4 : 0;  // zero-fill when predicated off
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(n)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 __global__ void __launch_bounds__(256, 2)
     nchw3x3_kernel(const float* __restrict__ x, int cin, int h, int w,
                    const float* __restrict__ wt, int cout, float* __restrict__ y, int tiles_w) {
