@@ -424,8 +424,8 @@ template <int kOp>
 int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode, float* y,
              cudaStream_t st) {
   const bool exact = mode == SC_MODE_EXACT;
-  // k = B - 1 or B (B = 64 / 128 / 256 / 512): the aligned-block van Herk /
-  // Gil-Werman max, ~7 instructions per output (pool_block.cu)
+  // 33 <= k <= 512 on aligned signals: the aligned-block van Herk /
+  // Gil-Werman max (pool_block.cu; one tiling for k = B - 1 / B, two otherwise)
   if constexpr (kOp == SC_POOL_MAX) {
     const int rc = pool1d_block_max(x, batch, length, k, y, st);
     if (rc != 1) return rc;

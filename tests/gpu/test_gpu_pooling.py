@@ -71,6 +71,20 @@ def test_ragged_and_tiny_signals(n, k):
         assert np.array_equal(y, O.pool_batched(x[None], k, op)[0])
 
 
+# pool_block.cu runtime-K kernel (two block tilings): every window 33..512
+# that is not B - 1 / B, on aligned signals long enough for several tiles
+@pytest.mark.parametrize("k", [33, 34, 35, 47, 48, 49, 62, 65, 66, 95, 96, 97, 126, 129, 130,
+                               160, 191, 192, 193, 254, 257, 258, 320, 383, 384, 385, 450, 510])
+def test_block_max_runtime_window(k):
+    rng = np.random.default_rng(7000 + k)
+    x = rng.standard_normal((3, 32 * 1061), dtype=np.float32)
+    x[1, ::7] = np.float32(2.5)                  # many exact ties
+    want = O.pool_batched(x, k, "max")
+    xd = torch.from_numpy(x).cuda()
+    assert np.array_equal(sc.sliding_window_max(xd, k)[0].cpu().numpy(), want)
+    assert np.array_equal(sc.sliding_window_max(xd, k, exact=True)[0].cpu().numpy(), want)
+
+
 def test_reference_kats():
     assert sc.sliding_window_sum([1, 2, 3, 4, 5], 3)[0].tolist() == [6, 9, 12]
     assert sc.sliding_window_max([3, 1, 4, 1, 5], 3)[0].tolist() == [4, 4, 5]
@@ -82,7 +96,8 @@ def test_reference_kats():
 
 
 @pytest.mark.parametrize("n", [5000, 5024])
-@pytest.mark.parametrize("k", [2, 3, 16, 17, 33, 63, 64, 127, 128, 255, 256, 300, 511, 512])
+@pytest.mark.parametrize("k", [2, 3, 16, 17, 33, 40, 63, 64, 100, 127, 128, 200, 255, 256, 300,
+                               400, 511, 512])
 def test_max_nan_and_signed_zero_semantics(k, n):
     rng = np.random.default_rng(99 + k)
     x = rng.standard_normal((2, n), dtype=np.float32)

@@ -13,7 +13,14 @@ dev = torch.device("cuda")
 g = torch.Generator(device=dev)
 g.manual_seed(1)
 vm = sc.VectorModel(16)
-if which.startswith("pool"):
+if which.startswith("psum") or which.startswith("pavg") or which.startswith("pmax"):
+    k = int(which[4:])
+    fn = {"psum": sc.sliding_window_sum, "pavg": sc.sliding_window_mean,
+          "pmax": sc.sliding_window_max}[which[:4]]
+    x = torch.randn((256, 262144), generator=g, device=dev)
+    for _ in range(reps):
+        fn(x, k)
+elif which.startswith("pool"):
     k = int(which[4:])
     x = torch.randn((256, 262144), generator=g, device=dev)
     for _ in range(reps):
