@@ -357,7 +357,7 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
 
 }  // namespace
 
-// Exact sliding max for 33 <= k <= 512 on 16-byte aligned signals whose
+// Exact sliding max for 34 <= k <= 512 on 16-byte aligned signals whose
 // length is a multiple of 32 (>= 1,024); k = B - 1 / B take the one-tiling
 // kernels.  Returns
 // SC_OK / an error if it ran, 1 if it does not apply.
@@ -378,8 +378,8 @@ int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, f
     case 512: return launch<512, 512>(x, batch, length, y, st);
     default: break;
   }
-  // any other window 33 .. 512: the two-tiling runtime-K kernel
-  if (k > 32 && k <= 512 && length >= k) {
+  // any other window 34 .. 512: the two-tiling runtime-K kernel
+  if (k > 33 && k <= 512 && length >= k) {  // k <= 33: pool_tma.cu is faster
     if (k <= 64) return launch<64, 0>(x, batch, length, y, st, (int)k);
     if (k <= 128) return launch<128, 0>(x, batch, length, y, st, (int)k);
     if (k <= 256) return launch<256, 0>(x, batch, length, y, st, (int)k);
