@@ -175,14 +175,18 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
   __syncthreads();
 
   const unsigned tpr = (unsigned)tiles_per_row;
-  const unsigned t_begin = blockIdx.x * (unsigned)tiles_per_cta;
-  const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
+  // persistent CTAs: groups of tiles_per_cta contiguous tiles, grid-strided
+  // (a CTA per group paid a pipeline fill -- the first tile's full load
+  // latency -- every few tiles)
+  const unsigned n_t = (unsigned)n_tiles, tpc = (unsigned)tiles_per_cta;
+  const unsigned g_stride = gridDim.x * tpc;
 
   if (warp == kWarps) {
     if (lane == 0) {
       prefetch_tmap(&tmap);
       int i = 0;
-      for (unsigned t = t_begin; t < nt; ++t, ++i) {
+      for (unsigned g0 = blockIdx.x * tpc; g0 < n_t; g0 += g_stride)
+      for (unsigned t = g0; t < min(n_t, g0 + tpc); ++t, ++i) {
         const int b = i % kNbuf;
         if (i >= kNbuf) mbar_wait_sleep(&empty_bar[b], ((i / kNbuf) - 1) & 1);
         const unsigned row = t / tpr;
@@ -205,7 +209,8 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
   __shared__ float seg_v[2 * kWarps];
   __shared__ int seg_f[2 * kWarps];
   int it = 0;
-  for (unsigned t = t_begin; t < nt; ++t, ++it) {
+  for (unsigned g0 = blockIdx.x * tpc; g0 < n_t; g0 += g_stride)
+  for (unsigned t = g0; t < min(n_t, g0 + tpc); ++t, ++it) {
     const int b = it % kNbuf;
     mbar_wait(&full_bar[b], (it / kNbuf) & 1);
     const unsigned char* buf = base + b * kBufBytes;
@@ -338,7 +343,8 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
     attr = true;
   }
   const int tpc = 4;
-  const int64_t grid = (n_tiles + tpc - 1) / tpc;
+  const int64_t grid = std::min<int64_t>((n_tiles + tpc - 1) / tpc,
+                                         (int64_t)sm_count() * (kOp == SC_POOL_MAX ? 2 : 3));
   pool_wide_kernel<kOp><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
       map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt);
   SC_LAUNCH_CHECK("pool_wide_kernel");
