@@ -342,7 +342,11 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
                                  (int)smem));
     attr = true;
   }
-  const int tpc = 4;
+  static const int tpc = [] {  // contiguous tiles per CTA (SC_WIDE_TPC)
+    const char* e = std::getenv("SC_WIDE_TPC");
+    const int n = e ? std::atoi(e) : 0;
+    return (n >= 1 && n <= 1024) ? n : 2;
+  }();
   const int64_t grid = std::min<int64_t>((n_tiles + tpc - 1) / tpc,
                                          (int64_t)sm_count() * (kOp == SC_POOL_MAX ? 2 : 3));
   pool_wide_kernel<kOp><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
