@@ -364,17 +364,19 @@ def rowband_bench(torch, sc, rank, world, hbm_peak, reps=3):
     dev = torch.device("cuda", torch.cuda.current_device())
     gen = torch.Generator(device=dev)
     gen.manual_seed(5000 + rank)
-    band = torch.empty((rows, W), device=dev)
+    # the band plus kh - 1 spare rows: the halo is received in place and the
+    # band is one conv launch (rowband.alloc_band)
+    band = sc.alloc_band(rows, W, 7, device=dev)
     for r0 in range(0, rows, 8192):
-        band[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
+        band[r0:min(rows, r0 + 8192)].uniform_(-1, 1, generator=gen)
     f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
           / np.float32(7)).astype(np.float32)
     group = dist.group.WORLD if world > 1 else None
     for _ in range(2):
         if world > 1:
-            sc.conv2d_rowband(band, f7, group=group)
+            sc.conv2d_rowband(band, f7, group=group, halo_in_place=True)
         else:
-            sc.conv2d_reference(band, f7)
+            sc.conv2d_reference(band[:rows], f7)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -382,7 +384,8 @@ def rowband_bench(torch, sc, rank, world, hbm_peak, reps=3):
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
-        y = sc.conv2d_rowband(band, f7, group=group)[0] if world > 1 else sc.conv2d_reference(band, f7)
+        y = (sc.conv2d_rowband(band, f7, group=group, halo_in_place=True)[0] if world > 1
+             else sc.conv2d_reference(band[:rows], f7))
     b.record()
     torch.cuda.synchronize()
     t = a.elapsed_time(b) / 1e3 / reps
@@ -397,6 +400,53 @@ def rowband_bench(torch, sc, rank, world, hbm_peak, reps=3):
     fl = 2 * o * o * 49
     return {"ms": round(t * 1e3, 3), "ranks": world, **roofline(nb, fl, t, hbm_peak * world),
             "halo_bytes_per_pair": 6 * W * 4, "note": "one 65536^2 image, row bands + NCCL halo"}
+
+
+def rowband_projection(torch, sc, reps=3):
+    """One GPU, no ranks: device time of ONE rank's share of config 5 at
+    G = 2 / 4 / 8 bands -- the single launch conv2d_rowband(...,
+    halo_in_place=True) issues per middle rank (band + received halo rows)
+    -- against the whole image.  E_proj(G) = T(1) / (G * T_rank(G)) leaves
+    out the 1.5 MiB NVLink halo exchange that precedes the launch."""
+    from paper_2310_05218_b200 import _ops
+    H = W = 65536
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
+          / np.float32(7)).astype(np.float32)
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / 1e3 / reps
+
+    out = {}
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(5000)
+    x = torch.empty((H, W), device=dev)
+    for r0 in range(0, H, 8192):
+        x[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
+    y = torch.empty((H - 6, W - 6), device=dev)
+    t1 = timed(lambda: _ops.conv2d_into(x, f7, y))
+    out["whole_ms"] = round(t1 * 1e3, 3)
+    for g in (2, 4, 8):
+        rows = H // g
+        buf = x[:rows + 6]                   # a middle rank's alloc_band buffer, halo received
+        yb = y[:rows]
+        tg = timed(lambda: _ops.conv2d_into(buf, f7, yb))
+        out[f"G{g}"] = {"rank_ms": round(tg * 1e3, 3), "proj_eff": round(t1 / (g * tg), 4)}
+    del x, y
+    torch.cuda.empty_cache()
+    out["note"] = ("one GPU: per-rank device time of the row-band path, halo transfer "
+                   "excluded; the multi-GPU run reports rowband_cfg5")
+    return out
 
 
 def run_ours(args, rank, world, local_rank):
@@ -557,6 +607,8 @@ def run_ours(args, rank, world, local_rank):
         line["per_config"] = per_config(torch, sc, hbm_peak, args, traffic)
     if rb is not None:
         line["rowband_cfg5"] = rb
+    if world == 1 and not args.no_extras:
+        line["rowband_cfg5_projection"] = rowband_projection(torch, sc)
     print(json.dumps(line), flush=True)
 
 

@@ -15,7 +15,7 @@ from .lanes import VectorModel
 from .nchw import conv2d_nchw
 from .pooling import sliding_window_max, sliding_window_mean, sliding_window_sum
 from .reference import conv1d_reference, conv2d_reference, oracle_conv2d, relative_error
-from .rowband import RowBandPlan, conv2d_rowband, plan_row_bands
+from .rowband import RowBandPlan, alloc_band, conv2d_rowband, plan_row_bands
 from .verify import PropertyResult, VerifyReport, verify_suite
 from .tensor import (ConvShape, CostCounters, FilterSizeError, FilterWidthError, ShapeError,
                      mac_count)
@@ -33,6 +33,6 @@ __all__ = [
     "analytic_counters", "compound_width", "counted_offsets", "variant_applicable",
     "relative_error", "verify_suite", "VerifyReport", "PropertyResult",
     # B200 extensions (BASELINE configs)
-    "sliding_window_mean", "conv2d_nchw", "conv2d_rowband", "plan_row_bands", "RowBandPlan",
+    "sliding_window_mean", "conv2d_nchw", "conv2d_rowband", "plan_row_bands", "RowBandPlan", "alloc_band",
     "pinned_empty", "set_default_mode",
 ]

@@ -38,6 +38,18 @@ def test_rowband_single_rank_equals_whole(nccl_world1):
     assert c.macs == O.mac_count(1030, 4096, 7, 7)
 
 
+def test_rowband_single_rank_halo_in_place(nccl_world1):
+    rng = np.random.default_rng(56)
+    x = rng.uniform(-1, 1, (777, 2048)).astype(np.float32)
+    f = rng.standard_normal((7, 7), dtype=np.float32)
+    buf = sc.alloc_band(777, 2048, 7, device="cuda")
+    buf[777:] = float("nan")                     # the last rank never reads the spare rows
+    buf[:777] = torch.from_numpy(x).cuda()
+    y, c = sc.conv2d_rowband(buf, f, exact=True, halo_in_place=True)
+    assert np.array_equal(y.cpu().numpy(), O.conv2d(x, f))
+    assert c.macs == O.mac_count(777, 2048, 7, 7)
+
+
 def test_rowband_plan_band_sizes():
     for g in (1, 2, 4, 8):
         plans = sc.plan_row_bands(65536, 7, g)

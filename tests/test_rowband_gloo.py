@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, h, w, kh, kw, q):
+def _worker(rank, world, port, h, w, kh, kw, q, in_place=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -32,24 +32,31 @@ def _worker(rank, world, port, h, w, kh, kw, q):
         x = rng.uniform(-1, 1, (h, w)).astype(np.float32)
         f = rng.standard_normal((kh, kw), dtype=np.float32)
         plan = sc.plan_row_bands(h, kh, world)[rank]
-        band = torch.from_numpy(x[plan.in_start:plan.in_stop].copy())
+        rows = plan.in_stop - plan.in_start
+        if in_place:
+            band = sc.alloc_band(rows, w, kh)
+            band[rows:] = float("nan")              # spare rows: must be overwritten
+            band[:rows] = torch.from_numpy(x[plan.in_start:plan.in_stop])
+        else:
+            band = torch.from_numpy(x[plan.in_start:plan.in_stop].copy())
 
         def conv(a, b):
             return torch.from_numpy(O.conv2d(a.numpy(), b))
 
-        y, c = sc.conv2d_rowband(band, f, conv=conv)
+        y, c = sc.conv2d_rowband(band, f, conv=conv, halo_in_place=in_place)
         q.put((rank, plan.out_start, plan.out_stop, y.numpy(), c.macs))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("in_place", [False, True])
 @pytest.mark.parametrize("world,h,w,kh,kw", [(2, 64, 40, 7, 7), (3, 50, 33, 5, 3),
                                               (2, 31, 17, 1, 4)])
-def test_rowband_gloo_matches_whole_image(world, h, w, kh, kw):
+def test_rowband_gloo_matches_whole_image(world, h, w, kh, kw, in_place):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, h, w, kh, kw, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, h, w, kh, kw, q, in_place))
              for r in range(world)]
     for p in procs:
         p.start()
