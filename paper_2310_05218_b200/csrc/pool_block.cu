@@ -1,8 +1,11 @@
 // Aligned-block sliding-window max for windows of k = B - 1 or B samples,
 // B in {64, 128, 256, 512} (BASELINE config 2's k = 255 sweep point; replaces
-// pooling.py:60-78 for those windows, bit-exact), and -- with a second block
-// tiling offset by B / 2 -- for every other window 33 <= k <= 512
-// (block_max_rt below; k = 100: 148 -> 111 us, k = 200: 166 -> 126 us).
+// pooling.py:60-78 for those windows, bit-exact), and for every other window
+// 34 <= k <= 512 as k = A + d (A = 32 / 64 / 128 / 256 the largest power of
+// two below k): the window-A kernel stages y_A in shared memory and the
+// store loop emits max(y_A(i), y_A(i + d)) -- two overlapping windows that
+// cover [i, i + k - 1] (k = 100: 148 -> 94 us, k = 200: 166 -> 99 us, k = 40:
+// 109 -> 91 us against the striped doubling they replace).
 //
 // Van Herk / Gil-Werman with the blocks aligned to the register layout: a
 // warp holds a window of 1,024 samples, lane l the 32 CONSECUTIVE samples
@@ -44,16 +47,13 @@ constexpr int kT = 32;           // consecutive samples per lane
 constexpr int kWin = 32 * kT;    // samples per warp window
 constexpr int kPitch = kT + 4;   // staging row (floats), conflict-free STS.128
 
-template <int B, int K = B>
+template <int B>
 struct Geo {
   static constexpr int V = kWin - B;                         // outputs per warp
   static constexpr int kOutLanes = V / 32;                   // lanes holding outputs
   static constexpr int kRows = ((kWarps - 1) * V + kWin) / 32;  // TMA box rows
   static constexpr int kBuf = (kRows * 128 + 1023) / 1024 * 1024;
-  // output staging per warp: kOutLanes rows of kPitch; the runtime-K kernel
-  // stages P in 32 rows of 33 floats first and reuses them for the outputs
-  static constexpr int kYPitch = K == 0 ? 33 : kPitch;
-  static constexpr int kStage = K == 0 ? 32 * 33 : kOutLanes * kPitch;  // floats per warp
+  static constexpr int kStage = kOutLanes * kPitch;          // floats per warp
   // ring depth: 3 where two CTAs per SM still fit in shared memory
   static constexpr int kNbuf = B <= 128 ? 2 : 3;
   static_assert(kRows <= 256, "TMA box rows");
@@ -132,100 +132,6 @@ __device__ __forceinline__ bool block_max(const unsigned char* rowp, int swz, in
   return zero;
 }
 
-// Runtime window, B/2 < K <= B (every K in 33 .. 512 not served above).
-// Two block tilings: T0 aligned to B, T1 offset by B/2 (both on lane
-// boundaries, so the lane-local prefix / suffix are shared).  A window that
-// crosses a T0 boundary is max(S0(i), P0(i + K - 1)); one that sits inside a
-// T0 block must contain its midpoint (K > B/2), so it crosses a T1 boundary
-// and is max(S1(i), P1(i + K - 1)) -- no window needs a third operand.  The
-// choice per output is a compare on i mod B.  P(i + K - 1) is a runtime
-// (lane, register) offset away, so P -- already reduced to the tiling each
-// position's window uses -- goes through the warp's 33-float-pitch staging
-// rows (conflict-free for the blocked writes and the shifted reads), which
-// then carry the outputs to the coalesced store loop.
-template <int B, bool kEx>
-__device__ __forceinline__ bool block_max_rt(const unsigned char* rowp, int swz, int lane,
-                                             float* wbuf, int K, int lim) {
-  constexpr int LB = B / 32;               // lanes per block
-  constexpr int kOutLanes = (kWin - B) / 32;
-  const float kId = -__int_as_float(0x7f800000);
-  float P[kT], S[kT];
-#pragma unroll
-  for (int q = 0; q < kT / 4; ++q) {
-    const float4 v = *reinterpret_cast<const float4*>(rowp + ((q ^ swz) << 4));
-    S[4 * q] = v.x;
-    S[4 * q + 1] = v.y;
-    S[4 * q + 2] = v.z;
-    S[4 * q + 3] = v.w;
-  }
-  P[0] = S[0];
-#pragma unroll
-  for (int j = 1; j < kT; ++j) P[j] = mx<kEx>(P[j - 1], S[j]);     // lane prefix
-#pragma unroll
-  for (int j = kT - 2; j >= 0; --j) S[j] = mx<kEx>(S[j], S[j + 1]);  // lane suffix
-  // inclusive segmented scans of the lane aggregates for both tilings; a
-  // shuffle that falls off the warp returns the lane's own value, and
-  // mx(v, v) = v, so the partial T1 segments at the warp edges are harmless
-  const int lb0 = lane % LB, lb1 = (lane + LB / 2) % LB;
-  float pv0 = P[kT - 1], sv0 = S[0], pv1 = pv0, sv1 = sv0;
-#pragma unroll
-  for (int d = 1; d < LB; d <<= 1) {
-    const float u0 = __shfl_up_sync(0xffffffffu, pv0, d);
-    const float n0 = __shfl_down_sync(0xffffffffu, sv0, d);
-    const float u1 = __shfl_up_sync(0xffffffffu, pv1, d);
-    const float n1 = __shfl_down_sync(0xffffffffu, sv1, d);
-    pv0 = lb0 >= d ? mx<kEx>(u0, pv0) : pv0;
-    sv0 = lb0 + d < LB ? mx<kEx>(sv0, n0) : sv0;
-    pv1 = lb1 >= d ? mx<kEx>(u1, pv1) : pv1;
-    sv1 = lb1 + d < LB ? mx<kEx>(sv1, n1) : sv1;
-  }
-  // exclusive aggregates; identity (-inf) at the block edges
-  float pe0 = __shfl_up_sync(0xffffffffu, pv0, 1);
-  float se0 = __shfl_down_sync(0xffffffffu, sv0, 1);
-  float pe1 = __shfl_up_sync(0xffffffffu, pv1, 1);
-  float se1 = __shfl_down_sync(0xffffffffu, sv1, 1);
-  pe0 = lb0 > 0 ? pe0 : kId;
-  se0 = lb0 < LB - 1 ? se0 : kId;
-  pe1 = lb1 > 0 ? pe1 : kId;
-  se1 = lb1 < LB - 1 ? se1 : kId;
-  // window [i, j = i + K - 1] crosses a T0 boundary iff (i mod B) >= B - K + 1
-  // iff (j mod B) < K - 1; with i mod B = 32 (lane mod LB) + r these are
-  // per-lane thresholds on the register index r
-  const int ib = 32 * (lane % LB);
-  int tS = B - K + 1 - ib, tP = K - 1 - ib;
-  // opaque copies: without them the compiler shares the 64 per-register
-  // compares between the fast pass and the exact redo and keeps them alive
-  // as bit masks (a LOP3 pair per compare, ~2x the instructions per output)
-  asm volatile("mov.b32 %0, %0;" : "+r"(tS));
-  asm volatile("mov.b32 %0, %0;" : "+r"(tP));
-  // stage P(j), j = 32 lane + r, in the tiling of the window ending at j
-  float* wrow = wbuf + 33 * lane;
-#pragma unroll
-  for (int r = 0; r < kT; ++r) wrow[r] = mx<kEx>(r < tP ? pe0 : pe1, P[r]);
-  __syncwarp();
-  // y(i) = mx(S(i), P(i + K - 1)), i = 32 lane + r; P(i + K - 1) at row
-  // lane + m (+1 once r + c wraps): pa[r] before the wrap, pa[r + 1] after
-  int m = (K - 1) >> 5, c = (K - 1) & 31;
-  asm volatile("mov.b32 %0, %0;" : "+r"(c));
-  const int lr = min(lane, kOutLanes - 1);  // lanes past the outputs read in bounds
-  const float* pa = wbuf + 33 * (lr + m) + c;
-  // zero test as a running min of |y| (one FMNMX per output; NaN-ignoring);
-  // outputs past lim may trigger a harmless redo
-  float zmin = __int_as_float(0x7f800000);
-#pragma unroll
-  for (int r = 0; r < kT; ++r) {
-    const float pj = r < 32 - c ? pa[r] : pa[r + 1];
-    const float si = mx<kEx>(S[r], r >= tS ? se0 : se1);
-    S[r] = mx<kEx>(si, pj);
-    if constexpr (!kEx) zmin = fminf(zmin, fabsf(S[r]));
-  }
-  const bool zero = !kEx && lane < kOutLanes && zmin == 0.0f;
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < kT; ++r) wrow[r] = S[r];
-  return zero;
-}
-
 // kNbuf-deep TMA ring without a producer warp: the first load of each slot
 // is issued up front, and the LAST warp to finish with a slot (a shared
 // counter) refills it with the CTA's next tile at once.
@@ -233,9 +139,11 @@ template <int B, int K>
 __global__ void __launch_bounds__(32 * kWarps, 2)
     pool_block_max_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
-                          int tiles_per_cta, int k_rt) {
-  using G = Geo<B, K>;
-  constexpr int V = G::V;
+                          int tiles_per_cta, int d) {
+  using G = Geo<B>;
+  // d > 0: the window is K + d; the warp stages y_K (window K) and stores
+  // max(y_K(i), y_K(i + d)) for Vd = floor32(V - d) outputs per warp
+  const int V = d ? (G::V - d) & ~31 : G::V;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int kNbuf = G::kNbuf;
   __shared__ __align__(8) uint64_t full_bar[kNbuf];
@@ -274,20 +182,13 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     const unsigned row = t / tpr;
     const unsigned o_in_row = (t - row * tpr) * (unsigned)(kWarps * V) + warp * V;
     const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
-    bool zero;
-    if constexpr (K == 0) {
-      zero = block_max_rt<B, false>(rowp, row0 & 7, lane, stage, k_rt, lim);
-      if (__any_sync(0xffffffffu, zero)) {  // rare: redo with np.maximum's rule
-        __syncwarp();
-        block_max_rt<B, true>(rowp, row0 & 7, lane, stage, k_rt, lim);
-      }
-    } else {
-      float* srow = stage + lane * kPitch;
-      zero = block_max<B, K, false>(rowp, row0 & 7, lane, srow, lim);
-      if (__any_sync(0xffffffffu, zero)) {  // rare: redo with np.maximum's rule
-        __syncwarp();
-        block_max<B, K, true>(rowp, row0 & 7, lane, srow, lim);
-      }
+    float* srow = stage + lane * kPitch;
+    const int lim_k = d ? G::V : lim;  // y_K outputs the combine reads
+    bool zero = block_max<B, K, false>(rowp, row0 & 7, lane, srow, lim_k);
+    zero = __any_sync(0xffffffffu, zero);
+    if (zero) {  // rare: redo with np.maximum's rule
+      __syncwarp();
+      block_max<B, K, true>(rowp, row0 & 7, lane, srow, lim_k);
     }
     __syncwarp();
     if (lane == 0) {  // done with slot b: the last warp refills it
@@ -302,22 +203,41 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     }
     float* yr = y + (int64_t)row * out_len + o_in_row + lane;
     const float* sp = stage + lane;
-    if (lim == V) {
+    if (d == 0) {
+      if (lim == V) {
 #pragma unroll
-      for (int mm = 0; mm < G::kOutLanes; ++mm) yr[32 * mm] = sp[mm * G::kYPitch];
+        for (int mm = 0; mm < G::kOutLanes; ++mm) yr[32 * mm] = sp[mm * kPitch];
+      } else {
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm)
+          if (32 * mm + lane < lim) yr[32 * mm] = sp[mm * kPitch];
+      }
     } else {
+      // y(i) = max(y_K(i), y_K(i + d)): i = 32 mm + lane, so i + d sits at
+      // row mm + (lane + d) / 32, column (lane + d) % 32 -- a per-lane base
+      // and the same immediate row offsets as the plain store
+      const int ld = lane + d;
+      const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+      const int lim_d = min(lim, V);
+      if (zero) {
 #pragma unroll
-      for (int mm = 0; mm < G::kOutLanes; ++mm)
-        if (32 * mm + lane < lim) yr[32 * mm] = sp[mm * G::kYPitch];
+        for (int mm = 0; mm < G::kOutLanes; ++mm)
+          if (32 * mm + lane < lim_d) yr[32 * mm] = mx<true>(sp[mm * kPitch], sq[mm * kPitch]);
+      } else {
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm)
+          if (32 * mm + lane < lim_d) yr[32 * mm] = mx<false>(sp[mm * kPitch], sq[mm * kPitch]);
+      }
     }
     __syncwarp();  // staging reused by the next tile
   }
 }
 
+// k = K + d (d = 0: the plain window K)
 template <int B, int K>
 int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
-           int k_rt = K) {
-  using G = Geo<B, K>;
+           int d = 0) {
+  using G = Geo<B>;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
@@ -329,8 +249,9 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "pool block tensor map encode failed");
-  const int64_t out_len = length - k_rt + 1;
-  const int64_t tiles_per_row = (out_len + kWarps * G::V - 1) / (kWarps * G::V);
+  const int64_t out_len = length - (K + d) + 1;
+  const int vw = d ? (G::V - d) & ~31 : G::V;  // outputs per warp
+  const int64_t tiles_per_row = (out_len + kWarps * vw - 1) / (kWarps * vw);
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + G::kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
@@ -350,7 +271,7 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   const int tpc = tpc_env ? tpc_env : B == 256 ? 6 : 8;
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   pool_block_max_kernel<B, K><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, k_rt);
+      map, y, out_len, tiles_per_row, n_tiles, tpc, d);
   SC_LAUNCH_CHECK("pool_block_max_kernel");
   return SC_OK;
 }
@@ -378,12 +299,16 @@ int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, f
     case 512: return launch<512, 512>(x, batch, length, y, st);
     default: break;
   }
-  // any other window 34 .. 512: the two-tiling runtime-K kernel
-  if (k > 33 && k <= 512 && length >= k) {  // k <= 33: pool_tma.cu is faster
-    if (k <= 64) return launch<64, 0>(x, batch, length, y, st, (int)k);
-    if (k <= 128) return launch<128, 0>(x, batch, length, y, st, (int)k);
-    if (k <= 256) return launch<256, 0>(x, batch, length, y, st, (int)k);
-    return launch<512, 0>(x, batch, length, y, st, (int)k);
+  // any other window 34 .. 512: k = A + d with A = 32 / 64 / 128 / 256 the
+  // largest power of two below k: the one-tiling kernel for window A, then
+  // max(y_A(i), y_A(i + d)) from the staging rows (the two windows overlap
+  // and cover [i, i + k - 1]; taking the later one on ties keeps the
+  // rightmost maximal element, as the reference's doubling does)
+  if (k > 33 && k <= 512) {  // k <= 33: pool_tma.cu is faster
+    if (k <= 64) return launch<32, 32>(x, batch, length, y, st, (int)k - 32);
+    if (k <= 128) return launch<64, 64>(x, batch, length, y, st, (int)k - 64);
+    if (k <= 256) return launch<128, 128>(x, batch, length, y, st, (int)k - 128);
+    return launch<256, 256>(x, batch, length, y, st, (int)k - 256);
   }
   return 1;
 }
