@@ -402,50 +402,62 @@ def rowband_bench(torch, sc, rank, world, hbm_peak, reps=3):
             "halo_bytes_per_pair": 6 * W * 4, "note": "one 65536^2 image, row bands + NCCL halo"}
 
 
-def rowband_projection(torch, sc, reps=3):
-    """One GPU, no ranks: device time of ONE rank's share of config 5 at
-    G = 2 / 4 / 8 bands -- the single launch conv2d_rowband(...,
-    halo_in_place=True) issues per middle rank (band + received halo rows)
-    -- against the whole image.  E_proj(G) = T(1) / (G * T_rank(G)) leaves
-    out the 1.5 MiB NVLink halo exchange that precedes the launch."""
+def rowband_projection(torch, sc, rounds=3):
+    """One GPU, no ranks: config 5 processed as G = 2 / 4 / 8 row bands one
+    after another -- each band exactly the single launch a middle rank of
+    conv2d_rowband(..., halo_in_place=True) issues (its rows + the 6 halo
+    rows) -- against the whole image in one launch, interleaved so all four
+    see the same (power-capped) clock.  E_proj(G) = T(whole) / T(G bands) is
+    the compute efficiency of banding; it leaves out the 1.5 MiB NVLink halo
+    exchange each rank waits for before its launch."""
     from paper_2310_05218_b200 import _ops
     H = W = 65536
     dev = torch.device("cuda", torch.cuda.current_device())
     f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
           / np.float32(7)).astype(np.float32)
-
-    def timed(fn):
-        for _ in range(2):
-            fn()
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
-            fn()
-        b.record()
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / 1e3 / reps
-
-    out = {}
     gen = torch.Generator(device=dev)
     gen.manual_seed(5000)
     x = torch.empty((H, W), device=dev)
     for r0 in range(0, H, 8192):
         x[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
     y = torch.empty((H - 6, W - 6), device=dev)
-    t1 = timed(lambda: _ops.conv2d_into(x, f7, y))
-    out["whole_ms"] = round(t1 * 1e3, 3)
-    for g in (2, 4, 8):
+
+    def whole():
+        _ops.conv2d_into(x, f7, y)
+
+    def banded(g):
         rows = H // g
-        buf = x[:rows + 6]                   # a middle rank's alloc_band buffer, halo received
-        yb = y[:rows]
-        tg = timed(lambda: _ops.conv2d_into(buf, f7, yb))
-        out[f"G{g}"] = {"rank_ms": round(tg * 1e3, 3), "proj_eff": round(t1 / (g * tg), 4)}
+        for b in range(g):
+            a = b * rows
+            if b < g - 1:
+                _ops.conv2d_into(x[a:a + rows + 6], f7, y[a:a + rows])
+            else:
+                _ops.conv2d_into(x[a:], f7, y[a:])
+
+    cases = {"whole": whole, **{f"G{g}": (lambda g=g: banded(g)) for g in (2, 4, 8)}}
+    for fn in cases.values():
+        fn()
+    torch.cuda.synchronize()
+    times = {k: [] for k in cases}
+    for _ in range(rounds):
+        for k, fn in cases.items():
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            times[k].append(a.elapsed_time(b) / 1e3)
+    med = {k: statistics.median(v) for k, v in times.items()}
+    out = {"whole_ms": round(med["whole"] * 1e3, 3)}
+    for g in (2, 4, 8):
+        t = med[f"G{g}"]
+        out[f"G{g}"] = {"rank_ms": round(t / g * 1e3, 3), "proj_eff": round(med["whole"] / t, 4)}
     del x, y
     torch.cuda.empty_cache()
-    out["note"] = ("one GPU: per-rank device time of the row-band path, halo transfer "
-                   "excluded; the multi-GPU run reports rowband_cfg5")
+    out["note"] = ("one GPU: the image as G bands (band + 6 halo rows, one launch each, "
+                   "rank_ms = total / G) vs one launch, interleaved; halo exchange excluded; "
+                   "the multi-GPU run reports rowband_cfg5")
     return out
 
 
