@@ -54,10 +54,14 @@ def test_runtime_k_register_blocked_kernel(kh, kw, n, h, w):
 
 
 @pytest.mark.parametrize("k", [5, 7])
-def test_four_column_kernels_on_large_grids(k):
-    # conv2d_cols4_kernel<5 / 7>: grids of >= 2 waves of 512-column CTAs, ragged
-    # right edge (ow % 4 != 0) and a partial last row segment
-    x = rand(k + 700, (64, 261, 1031))
+@pytest.mark.parametrize("n,h,w", [(64, 261, 1031), (64, 261, 1030), (40, 300, 1100),
+                                   (2, 3001, 2060)])
+def test_four_column_kernels_on_large_grids(k, n, h, w):
+    # conv2d_cols4_kernel<5 / 7>: grids of >= 2 waves of 512-column CTAs; odd
+    # output pitch (per-column stores), even pitch with whole warps (STG.64
+    # pairs) and with a partial last warp; tall images (the 7x7 segment
+    # length search), partial last row segments
+    x = rand(k + 700 + w, (n, h, w))
     f = rand(k + 701, (k, k))
     xd = torch.from_numpy(x).cuda()
     got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
