@@ -238,8 +238,14 @@ __global__ void __launch_bounds__(32 * (kConsumerWarps + 1))
 // warp covers 128 columns with its own TMA box per stage.
 constexpr int kC4Warps = 4;                        // consumer warps per CTA (one TMA box each)
 constexpr int kC4Cols = 128;                       // output columns per warp
-constexpr int kC4Stages = 4;
+#ifndef SC_C4_STAGES
+#define SC_C4_STAGES 4
+#endif
+constexpr int kC4Stages = SC_C4_STAGES;
 // input rows per stage: a multiple of K (static rolling slots), ~7-10 rows
+#ifndef SC_C4_PACKED
+#define SC_C4_PACKED 1
+#endif
 __host__ __device__ constexpr int c4_rs(int k) { return k >= 7 ? k : 2 * k; }
 __host__ __device__ constexpr int c4_box(int k) { return (kC4Cols + k - 1 + 3) / 4 * 4; }
 __host__ __device__ constexpr int c4_sub(int k) {  // one warp's box, 128-byte aligned
@@ -295,14 +301,20 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   const int64_t gcol = (int64_t)c0 + col;
   float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
   const OutCols nvc = out_cols<4>(y, ow, c0 + warp * kC4Cols, gcol);
-  // scalar FFMA (fast) / FMUL + FADD (exact) accumulators: a packed FFMA2
-  // variant needs the odd-offset input pairs re-packed every row and measured
-  // slower (9.2 vs 7.5 ms) -- with ~97 % FFMAs issue slots are not the limit
+  // fast mode: packed FFMA2 on column pairs (0,1), (2,3) with the tap as a
+  // broadcast uniform-register operand; the odd tap offsets read a second,
+  // shifted pair view of the input row (K / 2 + 1 pairs rebuilt once per
+  // row, shared by all K x K taps).  Half the FMA issue slots of scalar
+  // FFMA.  Exact mode: scalar FMUL + FADD in the reference order.
+  constexpr bool kPacked = !kExact && SC_C4_PACKED && K >= 7;  // 5x5: HBM-bound, scalar 1 % faster
   float acc[K][4];
+  float2 acc2[K][2];
 #pragma unroll
-  for (int j = 0; j < K; ++j)
+  for (int j = 0; j < K; ++j) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[j][c] = 0.0f;
+    acc2[j][0] = acc2[j][1] = make_float2(0.0f, 0.0f);
+  }
 
   for (int s = 0; s < n_stage; ++s) {
     const int slot = s % kC4Stages;
@@ -318,32 +330,91 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
 #pragma unroll
       for (int q = (K + 3) / 4 * 4; q < K + 3; ++q) v[q] = p[q];
     };
+    // packed path: the row as aligned pairs pe = (x0,x1),(x2,x3).. (LDS.128 /
+    // LDS.64) and shifted pairs po = (x1,x2),(x3,x4).. loaded straight into
+    // register pairs (scalar LDS: building them from pe costs ~8 moves per
+    // row that ptxas multiplies by re-materialising); two row buffers
+    // alternate with the (unrolled) row index, so the prefetch needs no copy
+    constexpr int kPe = (K + 3) / 2, kPo = K / 2 + 1;
+    float2 pe[2][kPe], po[2][kPo];
+    auto loadp = [&](int rr, int bsel) {
+      const float* p = buf + rr * BW;
+#pragma unroll
+      for (int q = 0; q < kPe / 2; ++q) {
+        const float4 t = reinterpret_cast<const float4*>(p)[q];
+        pe[bsel][2 * q] = make_float2(t.x, t.y);
+        pe[bsel][2 * q + 1] = make_float2(t.z, t.w);
+      }
+      if constexpr (kPe % 2) pe[bsel][kPe - 1] = reinterpret_cast<const float2*>(p)[kPe - 1];
+      // volatile loads: plain ones are CSE'd with the pe loads and the pairs
+      // rebuilt with moves
+#pragma unroll
+      for (int q = 0; q < kPo; ++q) {
+        float a, b;
+        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(a) : "r"(smem_u32(p + 2 * q + 1)));
+        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(b) : "r"(smem_u32(p + 2 * q + 2)));
+        po[bsel][q] = make_float2(a, b);
+      }
+    };
     float cur[K + 3];
-    load(0, cur);
+    if constexpr (kPacked) loadp(0, 0);
+    else load(0, cur);
 #pragma unroll 1
     for (int g = 0; g < kC4RS / K; ++g) {
 #pragma unroll
       for (int u = 0; u < K; ++u) {
         const int rr = g * K + u;
         float nxt[K + 3];
-        if (rr + 1 < kC4RS) load(rr + 1, nxt);
+        if constexpr (kPacked) {
+          if (rr + 1 < kC4RS) loadp(rr + 1, (u + 1) & 1);
+        } else {
+          if (rr + 1 < kC4RS) load(rr + 1, nxt);
+        }
         // output row t - j lives in slot (u - j) mod K (kC4RS % K == 0)
+        if constexpr (kPacked) {
+          const float2(&pe_u)[kPe] = pe[u & 1];
+          const float2(&po_u)[kPo] = po[u & 1];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int sl = ((u - j) % K + K) % K;
+          for (int j = 0; j < K; ++j) {
+            const int sl = ((u - j) % K + K) % K;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float a = (j == 0) ? 0.0f : acc[sl][c];
+            for (int pp = 0; pp < 2; ++pp) {
+              float2 a = (j == 0) ? make_float2(0.0f, 0.0f) : acc2[sl][pp];
 #pragma unroll
-            for (int i = 0; i < K; ++i) a = mac<kExact>(a, taps.f[j * K + i], cur[c + i]);
-            acc[sl][c] = a;
+              for (int i = 0; i < K; ++i) {
+                const float tv = taps.f[j * K + i];
+                a = __ffma2_rn(make_float2(tv, tv), (i & 1) ? po_u[pp + i / 2] : pe_u[pp + i / 2],
+                               a);
+              }
+              acc2[sl][pp] = a;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const int sl = ((u - j) % K + K) % K;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float a = (j == 0) ? 0.0f : acc[sl][c];
+#pragma unroll
+              for (int i = 0; i < K; ++i) a = mac<kExact>(a, taps.f[j * K + i], cur[c + i]);
+              acc[sl][c] = a;
+            }
           }
         }
+        if constexpr (!kPacked) {
 #pragma unroll
-        for (int q = 0; q < K + 3; ++q) cur[q] = nxt[q];
+          for (int q = 0; q < K + 3; ++q) cur[q] = nxt[q];
+        }
         const int t = s * kC4RS + rr;  // input row relative to r0
         if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
-          store_cols<4>(ynext, nvc, acc[(u + 1) % K]);
+          if constexpr (kPacked) {
+            const int sl = (u + 1) % K;
+            const float o[4] = {acc2[sl][0].x, acc2[sl][0].y, acc2[sl][1].x, acc2[sl][1].y};
+            store_cols<4>(ynext, nvc, o);
+          } else {
+            store_cols<4>(ynext, nvc, acc[(u + 1) % K]);
+          }
         }
         ynext += ow;
       }
