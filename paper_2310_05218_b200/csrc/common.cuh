@@ -33,15 +33,38 @@ int cuda_fail(cudaError_t e, const char* what);
 
 constexpr int kNumSMs = 148;
 
+constexpr int kMaxDevices = 64;
+
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & (kMaxDevices - 1);
+}
+
+// SM count of the current device (cached per device)
 inline int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-      n = kNumSMs;
+  static int n[kMaxDevices] = {};
+  const int dev = current_device();
+  if (n[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = kNumSMs;
+    n[dev] = v;
   }
-  return n;
+  return n[dev];
+}
+
+// Raise a kernel's dynamic shared-memory limit once per device
+// (cudaFuncSetAttribute applies to the current device only); `done` is the
+// caller's per-kernel bit set of devices already configured.
+template <typename F>
+cudaError_t set_smem_limit_once(F* func, size_t bytes, uint64_t* done) {
+  const uint64_t bit = 1ull << current_device();
+  if (__atomic_load_n(done, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) __atomic_fetch_or(done, bit, __ATOMIC_RELEASE);
+  return e;
 }
 
 // ------------------------------------------------------------ arithmetic

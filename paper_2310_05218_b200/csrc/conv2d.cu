@@ -646,12 +646,8 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
     return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
   const size_t smem = (size_t)kStages * stage_floats(RS, BW) * sizeof(float) + 128;
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(conv2d_tma_kernel<KH, KW, kExact>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(conv2d_tma_kernel<KH, KW, kExact>, (int)smem, &attr));
   dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
   conv2d_tma_kernel<KH, KW, kExact><<<grid, 32 * (kConsumerWarps + 1), smem, st>>>(
       map, y, oh, ow, (int)rows, taps, pairs);
@@ -680,10 +676,11 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
   const int64_t seg_rows = K >= 7 ? 896 : 450;
   int64_t rows = env_rows > 0 ? env_rows : (int64_t)c4_rs(K) * (seg_rows / c4_rs(K)) - (K - 1);
   const size_t smem = (size_t)kC4Stages * kC4Warps * c4_sub(K) * sizeof(float) + 128;
-  static int slots = 0;  // resident CTAs on the whole GPU
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(conv2d_cols4_kernel<K, kExact>, smem, &attr));
+  static int slots_dev[kMaxDevices] = {};  // resident CTAs on the whole GPU
+  int& slots = slots_dev[current_device()];
   if (!slots) {
-    SC_CUDA(cudaFuncSetAttribute(conv2d_cols4_kernel<K, kExact>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int occ = 0;
     SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, conv2d_cols4_kernel<K, kExact>, 32 * (kC4Warps + 1), smem));
@@ -735,12 +732,8 @@ int launch_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float
     return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
   const size_t smem =
       (size_t)kC4Stages * kC4Warps * ((kR4RS * BW + 31) / 32 * 32) * sizeof(float) + 128;
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(conv2d_rot4_kernel<K, C, kExact>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(conv2d_rot4_kernel<K, C, kExact>, (int)smem, &attr));
   dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
   conv2d_rot4_kernel<K, C, kExact><<<grid, 32 * (kC4Warps + 1), smem, st>>>(map, y, oh, ow,
                                                                         (int)rows, taps);

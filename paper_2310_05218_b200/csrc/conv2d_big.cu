@@ -228,13 +228,8 @@ int launch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigTap
   const int64_t oh = h - kh + 1, ow = w - kw + 1;
   const int64_t gx = (ow + kTileCols - 1) / kTileCols, gy = (oh + kTileRows - 1) / kTileRows;
   if (gy > 65535) return 1;
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(conv2d_big_kernel<kExact, kWarps, kG>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)big_smem(kMaxK, kMaxK, kWarps, kG)));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(conv2d_big_kernel<kExact, kWarps, kG>, (int)big_smem(kMaxK, kMaxK, kWarps, kG), &attr));
   conv2d_big_kernel<kExact, kWarps, kG>
       <<<dim3((unsigned)gx, (unsigned)gy, (unsigned)batch), 32 * kWarps,
          big_smem((int)kh, (int)kw, kWarps, kG), st>>>(x, (int)h, (int)w, taps, (int)kh, (int)kw,

@@ -473,12 +473,8 @@ int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: weight tensor map failed");
   }
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(nchw3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(nchw3x3_tc_kernel, (int)kSmem, &attr));
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sm_count());
   nchw3x3_tc_kernel<<<grid, kThreads, kSmem, st>>>(mx, mh, mw, y, (int)cin, (int)h, (int)w,
                                                    (int)cout, (int)ntiles);

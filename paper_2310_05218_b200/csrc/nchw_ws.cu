@@ -456,12 +456,8 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   pack_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (int64_t)(abytes / 4 + 255) / 256), 256,
                         0, st>>>(wt, apack, (int)cin, (int)cout);
   SC_LAUNCH_CHECK("pack_weights_kernel");
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(nchw3x3_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kSmem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(nchw3x3_ws_kernel, (int)kSmem, &attr));
   const unsigned grid = (unsigned)(a.ctas_per_co * co_tiles);
   nchw3x3_ws_kernel<<<grid, kThreads, kSmem, st>>>(mx, mh, apack, y, a);
   SC_LAUNCH_CHECK("nchw3x3_ws_kernel");

@@ -311,12 +311,8 @@ int launch_prefix(const float* x, int64_t batch, int64_t length, int k, float* y
   const int64_t tiles = (out_len + kPrefixTile - 1) / kPrefixTile;
   const size_t smem = (size_t)(kPrefixTile + k) * sizeof(double) +
                       (size_t)(kPrefixTile + k) * sizeof(float);
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[kOp]) {
-    SC_CUDA(cudaFuncSetAttribute(pool_prefix_kernel<kOp>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_set[kOp] = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set (one per kOp instantiation)
+  SC_CUDA(set_smem_limit_once(pool_prefix_kernel<kOp>, 200 * 1024, &attr));
   if (batch * tiles > 0x7fffffffLL) return fail(SC_ERR_UNSUPPORTED, "pool1d: grid too large");
   pool_prefix_kernel<kOp><<<(unsigned)(batch * tiles), kPrefixThreads, smem, st>>>(
       x, length, k, y, tiles);

@@ -255,12 +255,8 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + G::kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(pool_block_max_kernel<B, K>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<B, K>, (int)smem, &attr));
   // contiguous runs of tiles per CTA (tools/pbcheck.py sweep on config 2:
   // 6 tiles for B = 256, 8 otherwise); env override
   static const int tpc_env = [] {

@@ -295,12 +295,8 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
   if (n_tiles >= 0x7fffffff) return 1;  // not applicable: caller falls back
   const size_t smem = 1024 + NBUF * (size_t)tma_buf_bytes(K) +
                       (size_t)kTmaWarps * 32 * kStageStride * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(pool_tma_kernel<kOp, K, NBUF>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(pool_tma_kernel<kOp, K, NBUF>, (int)smem, &attr));
   const int tpc = env_int("SC_POOL_TPC", 4, 1, 64);
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   Taps1<K> taps{};

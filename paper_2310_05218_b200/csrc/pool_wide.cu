@@ -336,12 +336,8 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + (size_t)kNbuf * kBufBytes + (size_t)kArrBytes * 2;
-  static bool attr = false;
-  if (!attr) {
-    SC_CUDA(cudaFuncSetAttribute(pool_wide_kernel<kOp>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = true;
-  }
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp>, (int)smem, &attr));
   static const int tpc = [] {  // contiguous tiles per CTA (SC_WIDE_TPC)
     const char* e = std::getenv("SC_WIDE_TPC");
     const int n = e ? std::atoi(e) : 0;
