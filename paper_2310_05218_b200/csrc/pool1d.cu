@@ -27,6 +27,8 @@ int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k,
                cudaStream_t st);
 int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                 cudaStream_t st);
+int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st);
 int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st);
 namespace {
@@ -458,6 +460,12 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
   // SUM / AVG
   if (k <= 32) return launch_reg<kOp, 16, 1, 0>(x, batch, length, (int)k, y, st);
   if (exact) {
+    // 32 < k <= 512 on aligned signals: the reference's doubling + bit
+    // folding per tile in registers (pool_exact.cu)
+    {
+      const int rc = pool1d_exact_sum(kOp, x, batch, length, k, y, st);
+      if (rc != 1) return rc;
+    }
     // power-of-two windows need no retained partials: doubling only
     if (k == 64) return launch_reg<kOp, 16, 2, 64>(x, batch, length, 64, y, st);
     if (k == 128) return launch_reg<kOp, 32, 4, 128>(x, batch, length, 128, y, st);

@@ -1,0 +1,240 @@
+// Exact (bit-identical) sliding-window sums and averages for 32 < k <= 512
+// on aligned signals: the reference's own arithmetic (pooling.py:28-53), at
+// O(log k) adds per output instead of one global pass per stage.
+//
+// The reference builds doubling partials P_{2w}(j) = P_w(j) + P_w(j + w) up
+// to W = the largest power of two <= k, then folds in the other set bits of
+// k, largest first: acc = P_W(i); acc = acc + P_b(i + width); width += b.
+// Float addition is not associative, so every sum here is formed exactly
+// that way.
+//
+// A warp holds a 1,024-sample window, lane l the 32 CONSECUTIVE samples
+// [32 l, 32 l + 32) (one swizzled 128-byte TMA row, as in pool_block.cu).
+// A doubling level w is then register adds, with the w (w < 32) or all 32
+// (w >= 32) partners that sit in a later lane fetched by __shfl_down_sync.
+// The partials of the lower set bits are needed only after P_W, and keeping
+// them all would take up to 8 windows of shared memory per warp, so each is
+// RECOMPUTED from the tile (still in shared memory) when its turn comes:
+// k = 255 costs 28 levels instead of 7, ~40 adds per output, which the SMs
+// absorb next to the HBM stream.  Each partial passes through a
+// 33-float-pitch staging window (conflict-free blocked writes) and is read
+// lane-striped at the runtime offset width, which is a per-lane base plus
+// immediate row offsets; the running sums stay in registers lane-striped,
+// so the final stores are coalesced.  Averages divide by float32(k) with
+// the exact reciprocal + FMA correction of common.cuh (div_all_by_k).
+//
+// The tiles, ring and CTA walk are those of pool_block.cu: 8 warps, windows
+// advancing by V = 1024 - B samples (B = the next power of two >= k), a
+// 2-deep TMA ring refilled by the last warp done with a slot.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace sc {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kT = 32;           // consecutive samples per lane
+constexpr int kWin = 32 * kT;    // samples per warp window
+constexpr int kPitch = 33;       // staging row (floats): conflict-free both ways
+constexpr int kNbuf = 2;
+
+template <int B>
+struct XGeo {
+  static constexpr int V = kWin - B;                            // outputs per warp
+  static constexpr int kOutLanes = V / 32;                      // register slots per lane
+  static constexpr int kRows = ((kWarps - 1) * V + kWin) / 32;  // TMA box rows
+  static constexpr int kBuf = (kRows * 128 + 1023) / 1024 * 1024;
+  static constexpr int kStage = 32 * kPitch;                    // floats per warp
+  static_assert(kRows <= 256, "TMA box rows");
+};
+
+__device__ __forceinline__ void load_lane_row(const unsigned char* rowp, int swz,
+                                              float (&c)[kT]) {
+#pragma unroll
+  for (int q = 0; q < kT / 4; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(rowp + ((q ^ swz) << 4));
+    c[4 * q] = v.x;
+    c[4 * q + 1] = v.y;
+    c[4 * q + 2] = v.z;
+    c[4 * q + 3] = v.w;
+  }
+}
+
+// c = P_1 on entry, P_upto on exit (upto a power of two < 2 * kMaxW):
+// level w -> 2w is c(j) = c(j) + c(j + w), pooling.py:37-41
+template <int kMaxW>
+__device__ __forceinline__ void doubling(float (&c)[kT], int upto) {
+#pragma unroll
+  for (int w = 1; w < kMaxW; w <<= 1) {
+    if (w >= upto) break;  // warp-uniform
+    if (w < kT) {
+      // partners of the last w registers live in lane + 1; fetch them first
+      float sh[kT];
+#pragma unroll
+      for (int r = kT - w; r < kT; ++r) sh[r] = __shfl_down_sync(0xffffffffu, c[r + w - kT], 1);
+#pragma unroll
+      for (int r = 0; r < kT; ++r) c[r] = __fadd_rn(c[r], r + w < kT ? c[r + w] : sh[r]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < kT; ++r) c[r] = __fadd_rn(c[r], __shfl_down_sync(0xffffffffu, c[r], w / kT));
+    }
+  }
+}
+
+template <int B, int kOp>
+__global__ void __launch_bounds__(32 * kWarps, 2)
+    pool_exact_sum_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
+                          int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
+                          int tiles_per_cta, int k) {
+  using G = XGeo<B>;
+  constexpr int V = G::V;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kNbuf];
+  __shared__ int done_cnt[kNbuf];
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  float* stage_all = reinterpret_cast<float*>(base + kNbuf * G::kBuf);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned tpr = (unsigned)tiles_per_row;
+  const unsigned t_begin = blockIdx.x * (unsigned)tiles_per_cta;
+  const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
+  auto issue = [&](unsigned t, int b) {
+    const unsigned row = t / tpr;
+    const unsigned s0 = (t - row * tpr) * (unsigned)(kWarps * V);
+    mbar_arrive_expect_tx(&full_bar[b], G::kRows * 128);
+    tma_load_3d(base + b * G::kBuf, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
+  };
+  if (tid == 0) {
+    prefetch_tmap(&tmap);
+    for (int i = 0; i < kNbuf; ++i) {
+      mbar_init(&full_bar[i], 1);
+      done_cnt[i] = 0;
+    }
+    fence_mbar_init();
+    for (int i = 0; i < kNbuf && t_begin + i < nt; ++i) issue(t_begin + i, i);
+  }
+  __syncthreads();
+
+  const int kw = 1 << (31 - __clz(k));     // W: the largest power of two <= k
+  const float fk = (float)k, rk = 1.0f / fk;
+  const int row0 = (warp * V) / 32 + lane;  // this lane's 128-byte row in the tile
+  float* stage = stage_all + warp * G::kStage;
+  float* wrow = stage + lane * kPitch;
+  int it = 0;
+  for (unsigned t = t_begin; t < nt; ++t, ++it) {
+    const int b = it % kNbuf;
+    mbar_wait(&full_bar[b], (it / kNbuf) & 1);
+    const unsigned char* rowp = base + b * G::kBuf + row0 * 128;
+    float c[kT];
+    // acc = P_W(i), i = 32 mm + lane (lane-striped)
+    load_lane_row(rowp, row0 & 7, c);
+    doubling<B>(c, kw);
+#pragma unroll
+    for (int r = 0; r < kT; ++r) wrow[r] = c[r];
+    __syncwarp();
+    float acc[G::kOutLanes];
+#pragma unroll
+    for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = stage[kPitch * mm + lane];
+    // the other set bits, largest first: acc = acc + P_bit(i + width)
+    int width = kw;
+    for (int bit = kw >> 1; bit; bit >>= 1) {
+      if (!(k & bit)) continue;
+      load_lane_row(rowp, row0 & 7, c);
+      doubling<B>(c, bit);
+      __syncwarp();  // everyone done reading the previous partial
+#pragma unroll
+      for (int r = 0; r < kT; ++r) wrow[r] = c[r];
+      __syncwarp();
+      const int ld = lane + width;
+      const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], sq[kPitch * mm]);
+      width += bit;
+    }
+    __syncwarp();
+    if (lane == 0) {  // done with slot b: the last warp refills it
+      __threadfence_block();
+      if (atomicAdd(&done_cnt[b], 1) == kWarps - 1) {
+        done_cnt[b] = 0;
+        if (t + kNbuf < nt) {
+          fence_proxy_async();
+          issue(t + kNbuf, b);
+        }
+      }
+    }
+    if constexpr (kOp == SC_POOL_AVG) div_all_by_k<G::kOutLanes>(acc, fk, rk);
+    const unsigned row = t / tpr;
+    const unsigned o_in_row = (t - row * tpr) * (unsigned)(kWarps * V) + warp * V;
+    const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
+    float* yr = y + (int64_t)row * out_len + o_in_row + lane;
+    if (lim == V) {
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm) yr[32 * mm] = acc[mm];
+    } else {
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm)
+        if (32 * mm + lane < lim) yr[32 * mm] = acc[mm];
+    }
+    __syncwarp();  // staging reused by the next tile
+  }
+}
+
+template <int B, int kOp>
+int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st) {
+  using G = XGeo<B>;
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[3] = {32, (cuuint64_t)(length / 32), (cuuint64_t)batch};
+  cuuint64_t strides[2] = {128, (cuuint64_t)length * sizeof(float)};
+  cuuint32_t box[3] = {32, (cuuint32_t)G::kRows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "pool exact tensor map encode failed");
+  const int64_t out_len = length - k + 1;
+  const int64_t tiles_per_row = (out_len + kWarps * G::V - 1) / (kWarps * G::V);
+  const int64_t n_tiles = tiles_per_row * batch;
+  if (n_tiles >= 0x7fffffff) return 1;
+  const size_t smem = 1024 + kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
+  static uint64_t attr = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(pool_exact_sum_kernel<B, kOp>, smem, &attr));
+  const int tpc = 8;  // contiguous tiles per CTA
+  const int64_t grid = (n_tiles + tpc - 1) / tpc;
+  pool_exact_sum_kernel<B, kOp><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+      map, y, out_len, tiles_per_row, n_tiles, tpc, k);
+  SC_LAUNCH_CHECK("pool_exact_sum_kernel");
+  return SC_OK;
+}
+
+template <int kOp>
+int dispatch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st) {
+  if (k <= 64) return launch<64, kOp>(x, batch, length, k, y, st);
+  if (k <= 128) return launch<128, kOp>(x, batch, length, k, y, st);
+  if (k <= 256) return launch<256, kOp>(x, batch, length, k, y, st);
+  return launch<512, kOp>(x, batch, length, k, y, st);
+}
+
+}  // namespace
+
+// Bit-exact SUM / AVG for 32 < k <= 512 on 16-byte aligned signals whose
+// length is a multiple of 32 (>= 1,024).  Returns SC_OK / an error if it ran,
+// 1 if it does not apply.
+int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st) {
+  static const bool off = getenv("SC_POOL_NO_EXACT_BLOCK") != nullptr;
+  if (off || (op != SC_POOL_SUM && op != SC_POOL_AVG) || k <= 32 || k > 512 ||
+      reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || length < kWin ||
+      length / 32 > 0x7fffffff || batch > 0x7fffffff)
+    return 1;
+  return op == SC_POOL_SUM ? dispatch<SC_POOL_SUM>(x, batch, length, (int)k, y, st)
+                           : dispatch<SC_POOL_AVG>(x, batch, length, (int)k, y, st);
+}
+
+}  // namespace sc

@@ -85,6 +85,25 @@ def test_block_max_runtime_window(k):
     assert np.array_equal(sc.sliding_window_max(xd, k, exact=True)[0].cpu().numpy(), want)
 
 
+# pool_exact.cu: exact (bit-identical) sums / averages for 32 < k <= 512 on
+# aligned signals -- the reference's doubling + largest-bit-first fold per tile
+@pytest.mark.parametrize("k", [33, 37, 48, 63, 65, 100, 127, 128, 129, 200, 255, 256, 257, 300,
+                               383, 450, 511, 512])
+def test_exact_sum_block_kernel(k):
+    rng = np.random.default_rng(9000 + k)
+    x = rng.standard_normal((3, 32 * 1061), dtype=np.float32)
+    x[0, 5000] = np.inf
+    x[1, 7000:7003] = np.nan
+    x[2, ::13] = np.float32(1e30)               # large magnitudes: order matters
+    xd = torch.from_numpy(x).cuda()
+    for op in ("sum", "avg"):
+        want = O.pool_batched(x, k, op)
+        got = FNS[op](xd, k, exact=True)[0].cpu().numpy()
+        assert np.array_equal(np.isnan(got), np.isnan(want)), (op, k)
+        m = ~np.isnan(want)
+        assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32)), (op, k)
+
+
 def test_reference_kats():
     assert sc.sliding_window_sum([1, 2, 3, 4, 5], 3)[0].tolist() == [6, 9, 12]
     assert sc.sliding_window_max([3, 1, 4, 1, 5], 3)[0].tolist() == [4, 4, 5]
