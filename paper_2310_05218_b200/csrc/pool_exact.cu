@@ -13,10 +13,10 @@
 // A doubling level w is then register adds, with the w (w < 32) or all 32
 // (w >= 32) partners that sit in a later lane fetched by __shfl_down_sync.
 // The partials of the lower set bits are needed only after P_W, and keeping
-// them all would take up to 8 windows of shared memory per warp, so each is
-// RECOMPUTED from the tile (still in shared memory) when its turn comes:
-// k = 255 costs 28 levels instead of 7, ~40 adds per output, which the SMs
-// absorb next to the HBM stream.  Each partial passes through a
+// them all would take up to 8 windows of shared memory per warp: the largest
+// one is captured on the way up (lane-striped, in registers), the others are
+// RECOMPUTED from the tile (still in shared memory) when their turn comes --
+// k = 255 costs 22 doubling levels instead of 7.  Each partial passes through a
 // 33-float-pitch staging window (conflict-free blocked writes) and is read
 // lane-striped at the runtime offset width, which is a per-lane base plus
 // immediate row offsets; the running sums stay in registers lane-striped,
@@ -65,13 +65,14 @@ __device__ __forceinline__ void load_lane_row(const unsigned char* rowp, int swz
   }
 }
 
-// c = P_1 on entry, P_upto on exit (upto a power of two < 2 * kMaxW):
+// c = P_from on entry, P_upto on exit (powers of two, upto < 2 * kMaxW):
 // level w -> 2w is c(j) = c(j) + c(j + w), pooling.py:37-41
 template <int kMaxW>
-__device__ __forceinline__ void doubling(float (&c)[kT], int upto) {
+__device__ __forceinline__ void doubling(float (&c)[kT], int upto, int from = 1) {
 #pragma unroll
   for (int w = 1; w < kMaxW; w <<= 1) {
     if (w >= upto) break;  // warp-uniform
+    if (w < from) continue;
     if (w < kT) {
       // partners of the last w registers live in lane + 1; fetch them first
       float sh[kT];
@@ -121,6 +122,8 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
   __syncthreads();
 
   const int kw = 1 << (31 - __clz(k));     // W: the largest power of two <= k
+  const int low = k & (kw - 1);            // the set bits below W
+  const int bit1 = low ? 1 << (31 - __clz(low)) : 0;  // the largest of them
   const float fk = (float)k, rk = 1.0f / fk;
   const int row0 = (warp * V) / 32 + lane;  // this lane's 128-byte row in the tile
   float* stage = stage_all + warp * G::kStage;
@@ -131,18 +134,40 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     mbar_wait(&full_bar[b], (it / kNbuf) & 1);
     const unsigned char* rowp = base + b * G::kBuf + row0 * 128;
     float c[kT];
-    // acc = P_W(i), i = 32 mm + lane (lane-striped)
+    // The largest lower set bit's partial is captured on the way up to P_W
+    // (kept lane-striped in registers, at its fold offset kw): one partial
+    // fewer to recompute (k = 255: 22 doubling levels instead of 28).
+    float cap[G::kOutLanes];
     load_lane_row(rowp, row0 & 7, c);
-    doubling<B>(c, kw);
+    if (bit1) {
+      doubling<B>(c, bit1);
+#pragma unroll
+      for (int r = 0; r < kT; ++r) wrow[r] = c[r];
+      __syncwarp();
+      const int ld = lane + kw;
+      const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm) cap[mm] = sq[kPitch * mm];
+      __syncwarp();
+      doubling<B>(c, kw, bit1);
+    } else {
+      doubling<B>(c, kw);
+    }
+    // acc = P_W(i), i = 32 mm + lane (lane-striped)
 #pragma unroll
     for (int r = 0; r < kT; ++r) wrow[r] = c[r];
     __syncwarp();
     float acc[G::kOutLanes];
 #pragma unroll
     for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = stage[kPitch * mm + lane];
-    // the other set bits, largest first: acc = acc + P_bit(i + width)
     int width = kw;
-    for (int bit = kw >> 1; bit; bit >>= 1) {
+    if (bit1) {
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], cap[mm]);
+      width += bit1;
+    }
+    // the other set bits, largest first: acc = acc + P_bit(i + width)
+    for (int bit = (bit1 ? bit1 : kw) >> 1; bit; bit >>= 1) {
       if (!(k & bit)) continue;
       load_lane_row(rowp, row0 & 7, c);
       doubling<B>(c, bit);
