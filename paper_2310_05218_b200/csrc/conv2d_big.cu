@@ -42,7 +42,10 @@ constexpr int kMaxK = 64;
 // (conflict-free LDS.128 per group); a broadcast tap load feeds 16 kG FMAs.
 // kG = 2 (8 x 8 outputs per thread, ~120 registers) measured 10-25 % slower
 // than kG = 1 on the 11..63 sweep (fewer resident warps), so only kG = 1 is
-// instantiated.
+// instantiated.  Packed FFMA2 on column pairs (as the 7x7 kernel does) also
+// measured slower here (-9 %): the shifted input pairs of every 4-tap block
+// must be re-made from registers (~55 moves per 64 FFMA2) or re-loaded with
+// volatile scalar loads that sit on the block's critical path.
 __host__ __device__ constexpr int tile_cols(int g) { return 128 * g; }
 __host__ __device__ constexpr int tile_rows(int warps) { return kR * warps; }
 __host__ __device__ constexpr int pad4(int v) { return (v + 3) & ~3; }
