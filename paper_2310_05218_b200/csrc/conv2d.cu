@@ -246,6 +246,9 @@ constexpr int kC4Stages = SC_C4_STAGES;
 #ifndef SC_C4_PACKED
 #define SC_C4_PACKED 1
 #endif
+#ifndef SC_ROT4_PACKED
+#define SC_ROT4_PACKED 1
+#endif
 __host__ __device__ constexpr int c4_rs(int k) { return k >= 7 ? k : 2 * k; }
 __host__ __device__ constexpr int c4_box(int k) { return (kC4Cols + k - 1 + 3) / 4 * 4; }
 __host__ __device__ constexpr int c4_sub(int k) {  // one warp's box, 128-byte aligned
@@ -489,12 +492,22 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
   const int64_t gcol = (int64_t)c0 + col;
   float* ynext = y + ((int64_t)b * oh + r0 - (K - 1)) * ow + gcol;
   const OutCols nvc = out_cols<C>(y, ow, c0 + warp * 32 * C, gcol);
-  // acc[j]: output row t - (K - 1) + j for the input row t just consumed
+  // acc[j]: output row t - (K - 1) + j for the input row t just consumed.
+  // Fast mode with C = 4: packed FFMA2 on column pairs as in
+  // conv2d_cols4_kernel (aligned pairs by LDS.128, shifted pairs by volatile
+  // scalar loads, taps broadcast from uniform registers).
+  // (measured per K: 4 x 2048^2 k = 9 / 13 / 15 / 17: 33 / 37 / 36 / 35 -> 40 /
+  // 43 / 43 / 44 TFLOP/s, 32 x 512^2 even or better; K = 11 (spills) and 21
+  // lose 7-10 % on the small images, so they stay scalar)
+  constexpr bool kPk = !kExact && C == 4 && SC_ROT4_PACKED && K != 11 && K != 21;
   float acc[K][C];
+  float2 ap[K][2];
 #pragma unroll
-  for (int j = 0; j < K; ++j)
+  for (int j = 0; j < K; ++j) {
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[j][c] = 0.0f;
+    ap[j][0] = ap[j][1] = make_float2(0.0f, 0.0f);
+  }
 
   int t = 0;  // input row relative to r0
   for (int s = 0; s < n_stage; ++s) {
@@ -507,6 +520,46 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
       constexpr int NW = K + C - 1;  // the lane's input window
       float cur[NW];
       const float* p = buf + rr * BW;
+      if constexpr (kPk) {
+        constexpr int kPe = (K + 3) / 2, kPo = K / 2 + 1;  // (x0,x1).. / (x1,x2)..
+        float2 pe[kPe], po[kPo];
+#pragma unroll
+        for (int q = 0; q < kPe / 2; ++q) {
+          const float4 v = reinterpret_cast<const float4*>(p)[q];
+          pe[2 * q] = make_float2(v.x, v.y);
+          pe[2 * q + 1] = make_float2(v.z, v.w);
+        }
+        if constexpr (kPe % 2) pe[kPe - 1] = reinterpret_cast<const float2*>(p)[kPe - 1];
+#pragma unroll
+        for (int q = 0; q < kPo; ++q) {
+          float a, b2;
+          asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(a) : "r"(smem_u32(p + 2 * q + 1)));
+          asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(b2) : "r"(smem_u32(p + 2 * q + 2)));
+          po[q] = make_float2(a, b2);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+#pragma unroll
+          for (int pp = 0; pp < 2; ++pp) {
+            float2 a = ap[j][pp];
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              const float tv = taps.f[(K - 1 - j) * K + i];
+              a = __ffma2_rn(make_float2(tv, tv), (i & 1) ? po[pp + i / 2] : pe[pp + i / 2], a);
+            }
+            ap[j][pp] = a;
+          }
+        }
+        if ((unsigned)(t - (K - 1)) < (unsigned)rc) {
+          const float o[4] = {ap[0][0].x, ap[0][0].y, ap[0][1].x, ap[0][1].y};
+          store_cols<4>(ynext, nvc, o);
+        }
+        ynext += ow;
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) ap[j][0] = ap[j + 1][0], ap[j][1] = ap[j + 1][1];
+        ap[K - 1][0] = ap[K - 1][1] = make_float2(0.0f, 0.0f);
+        continue;
+      }
       if constexpr (C == 4) {
 #pragma unroll
         for (int q = 0; q < NW / 4; ++q) {
