@@ -776,17 +776,36 @@ int launch_rot4(const float* x, int64_t batch, int64_t h, int64_t w, const float
   BigSquareTaps<K> taps;
   for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
   const int64_t strips = (ow + kC4Warps * 32 * C - 1) / (kC4Warps * 32 * C);
-  // rows per CTA: long segments for big images, at least ~2 waves otherwise
-  int64_t rows = 1024;
-  while (rows > 64 && batch * strips * ((oh + rows - 1) / rows) < 2 * sm_count()) rows /= 2;
-  rows = std::min<int64_t>(rows, oh);
-  const int64_t segs = (oh + rows - 1) / rows;
-  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
-    return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
   const size_t smem =
       (size_t)kC4Stages * kC4Warps * ((kR4RS * BW + 31) / 32 * 32) * sizeof(float) + 128;
   static uint64_t attr = 0;  // devices whose limit is set
   SC_CUDA(set_smem_limit_once(conv2d_rot4_kernel<K, C, kExact>, (int)smem, &attr));
+  static int slots_dev[kMaxDevices] = {};  // resident CTAs on the whole GPU
+  int& slots = slots_dev[current_device()];
+  if (!slots) {
+    int occ = 0;
+    SC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, conv2d_rot4_kernel<K, C, kExact>, 32 * (kC4Warps + 1), smem));
+    slots = std::max(1, occ) * sm_count();
+  }
+  // rows per CTA: FP32-bound, a CTA costs ~(rows + K - 1) input rows and the
+  // grid runs in waves of `slots` CTAs -- minimise waves x (rows + K - 1)
+  // (the old rule, halve from 1,024 until >= 2 waves, gave 64-row segments
+  // with 31 % halo re-work for K = 21 on 4 x 2048^2)
+  // Measured against the old rule: 4 x 2048^2 / 1 x 4096^2 +5-30 % for
+  // K = 9..21, 32 x 512^2 +10 % for K = 15 / 17; K = 21 on 512^2 / 1024^2
+  // images loses 7 % (a floor on the grid fill did not recover it).
+  int64_t rows = 64, best = -1;
+  for (int64_t r = 16; r <= 1024; r += 8) {
+    const int64_t n = batch * strips * ((oh + r - 1) / r);
+    const int64_t cost = (n + slots - 1) / slots * (std::min<int64_t>(r, oh) + K - 1);
+    if (best < 0 || cost < best) best = cost, rows = r;
+    if (r >= oh) break;
+  }
+  rows = std::min<int64_t>(rows, oh);
+  const int64_t segs = (oh + rows - 1) / rows;
+  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
+    return fail(SC_ERR_UNSUPPORTED, "conv2d: grid too large");
   dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
   conv2d_rot4_kernel<K, C, kExact><<<grid, 32 * (kC4Warps + 1), smem, st>>>(map, y, oh, ow,
                                                                         (int)rows, taps);
