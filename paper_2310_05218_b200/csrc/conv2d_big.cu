@@ -27,6 +27,7 @@
 //     the reference's order (j ascending as q ascends, i ascending within a
 //     row, from 0): bit-identical to _accumulate_taps (reference.py:15-23).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -246,8 +247,13 @@ int dispatch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigT
                  int64_t kh, int64_t kw, float* y, cudaStream_t st) {
   const int64_t oh = h - kh + 1, ow = w - kw + 1;
   const int64_t ctas8 = batch * ((ow + 127) / 128) * ((oh + 63) / 64);
-  return ctas8 < 2 * sm_count() ? launch_big<kExact, 4, 1>(x, batch, h, w, taps, kh, kw, y, st)
-                                : launch_big<kExact, 8, 1>(x, batch, h, w, taps, kh, kw, y, st);
+  static const int env_warps = [] {
+    const char* e = std::getenv("SC_BIG_WARPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool four = env_warps ? env_warps == 4 : ctas8 < 2 * sm_count();
+  return four ? launch_big<kExact, 4, 1>(x, batch, h, w, taps, kh, kw, y, st)
+              : launch_big<kExact, 8, 1>(x, batch, h, w, taps, kh, kw, y, st);
 }
 
 }  // namespace
