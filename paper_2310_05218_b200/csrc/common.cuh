@@ -170,6 +170,19 @@ __device__ __forceinline__ void store_cols(float* p, const OutCols& m, const flo
   }
 }
 
+// The pair (p[0], p[1]) of a shared-memory row at an odd float offset, as a
+// register pair for packed FFMA2.  Volatile scalar loads: ptxas merges plain
+// ones with the neighbouring aligned vector loads and then rebuilds the pair
+// with moves at every use.
+__device__ __forceinline__ float2 lds_pair_unaligned(const float* p) {
+  float a, b;
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(a) : "r"(
+      static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+  asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(b) : "r"(
+      static_cast<uint32_t>(__cvta_generic_to_shared(p + 1))));
+  return make_float2(a, b);
+}
+
 // ------------------------------------------------------ mbarrier / TMA PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

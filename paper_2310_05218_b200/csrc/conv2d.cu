@@ -349,15 +349,8 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
         pe[bsel][2 * q + 1] = make_float2(t.z, t.w);
       }
       if constexpr (kPe % 2) pe[bsel][kPe - 1] = reinterpret_cast<const float2*>(p)[kPe - 1];
-      // volatile loads: plain ones are CSE'd with the pe loads and the pairs
-      // rebuilt with moves
 #pragma unroll
-      for (int q = 0; q < kPo; ++q) {
-        float a, b;
-        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(a) : "r"(smem_u32(p + 2 * q + 1)));
-        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(b) : "r"(smem_u32(p + 2 * q + 2)));
-        po[bsel][q] = make_float2(a, b);
-      }
+      for (int q = 0; q < kPo; ++q) po[bsel][q] = lds_pair_unaligned(p + 2 * q + 1);
     };
     float cur[K + 3];
     if constexpr (kPacked) loadp(0, 0);
@@ -531,12 +524,7 @@ __global__ void __launch_bounds__(32 * (kC4Warps + 1))
         }
         if constexpr (kPe % 2) pe[kPe - 1] = reinterpret_cast<const float2*>(p)[kPe - 1];
 #pragma unroll
-        for (int q = 0; q < kPo; ++q) {
-          float a, b2;
-          asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(a) : "r"(smem_u32(p + 2 * q + 1)));
-          asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(b2) : "r"(smem_u32(p + 2 * q + 2)));
-          po[q] = make_float2(a, b2);
-        }
+        for (int q = 0; q < kPo; ++q) po[q] = lds_pair_unaligned(p + 2 * q + 1);
 #pragma unroll
         for (int j = 0; j < K; ++j) {
 #pragma unroll
