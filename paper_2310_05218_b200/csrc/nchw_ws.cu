@@ -424,9 +424,20 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   const int co_tiles = (int)(cout / kCo);
   const int sms = sm_count();
   a.ctas_per_co = std::max(1, sms / co_tiles);
-  const int64_t rows_total = nb * a.col_tiles * h;
-  a.seg_rows = (int)std::max<int64_t>(4, (rows_total + a.ctas_per_co - 1) / a.ctas_per_co);
-  a.seg_rows = std::min<int>(a.seg_rows, (int)h);
+  // Segment length: the CTAs (one per SM) walk items of seg_rows output rows
+  // (one image, one column tile) in a grid-stride loop, so the kernel lasts
+  // ceil(items / ctas) items.  Pick seg_rows minimising that x (seg_rows + 2)
+  // (+2: the per-item pipeline fill).  Splitting rows_total evenly and
+  // rounding per image made 160 items for 148 CTAs at N = 32 (kernel 2.5x
+  // the N = 16 time instead of 2x).
+  const int64_t units = nb * a.col_tiles;
+  int64_t best = -1;
+  a.seg_rows = (int)h;
+  for (int64_t sr = 4; sr <= h; ++sr) {
+    const int64_t items = units * ((h + sr - 1) / sr);
+    const int64_t cost = (items + a.ctas_per_co - 1) / a.ctas_per_co * (sr + 2);
+    if (best < 0 || cost < best) best = cost, a.seg_rows = (int)sr;
+  }
   a.segs = (int)((h + a.seg_rows - 1) / a.seg_rows);
   a.items_per_co = (int)(nb * a.col_tiles * a.segs);
   a.ctas_per_co = std::min(a.ctas_per_co, a.items_per_co);
