@@ -345,7 +345,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) hv[i] = odd ? sum[8 + i] : sum[i];
           float* dst = yr + p0 + (odd ? 8 : 0);
-          if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          const int live = w - w0 - p0 - (odd ? 8 : 0);  // pixels of this half in the image
+          if (live < 8) {  // W % 16 != 0: the tile is padded to 16 pixels
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < live) dst[i] = hv[i];
+          } else if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
             reinterpret_cast<float4*>(dst)[0] = make_float4(hv[0], hv[1], hv[2], hv[3]);
             reinterpret_cast<float4*>(dst)[1] = make_float4(hv[4], hv[5], hv[6], hv[7]);
           } else {
@@ -410,17 +415,22 @@ int pick_tile_width(int64_t w) {
 // Returns SC_OK / an error if it ran, 1 if the shape is outside its range.
 int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
                int64_t cout, float* y, cudaStream_t st) {
-  if (cin > kMaxCin || cin % 32 != 0 || cout % kCo != 0 || w % 16 != 0 ||
+  // W % 16 != 0 (e.g. 56, 28): one column tile padded to the next multiple
+  // of 16 pixels (TMA zero-fills the columns past W, the epilogue masks
+  // them); the x rows must still be 16-byte aligned for TMA (W % 4 == 0)
+  const bool padded = w % 16 != 0;
+  if (cin > kMaxCin || cin % 32 != 0 || cout % kCo != 0 || w % 4 != 0 ||
+      (padded && w > kMaxWt) ||
       (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
       nb * cout * h * w >= ((int64_t)1 << 31) || h < 1)
     return 1;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const int tw = pick_tile_width(w);
+  const int tw = padded ? (int)((w + 15) / 16 * 16) : pick_tile_width(w);
   WsArgs a;
   a.nb = (int)nb, a.cin = (int)cin, a.h = (int)h, a.w = (int)w, a.cout = (int)cout;
   a.wt = tw;
-  a.col_tiles = (int)(w / tw);
+  a.col_tiles = padded ? 1 : (int)(w / tw);
   const int co_tiles = (int)(cout / kCo);
   const int sms = sm_count();
   a.ctas_per_co = std::max(1, sms / co_tiles);

@@ -38,6 +38,11 @@ def test_config4_exact_matches_composed_oracle():
                                                  # column tiles with halos, 3 co-tiles, H = 1, 2
                                                  (2, 32, 64, 30, 224, 3, 1), (2, 32, 192, 17, 160, 3, 1),
                                                  (1, 64, 64, 2, 48, 3, 1), (3, 64, 128, 5, 96, 3, 1),
+                                                 # weights-stationary, W % 16 != 0: one
+                                                 # column tile padded to 16 pixels
+                                                 (2, 64, 64, 20, 56, 3, 1), (3, 64, 128, 9, 28, 3, 1),
+                                                 (1, 32, 64, 7, 12, 3, 1), (2, 64, 64, 5, 100, 3, 1),
+                                                 (1, 32, 64, 3, 4, 3, 1),
                                                  # Cin % 64 != 0 -> CUDA-core kernel
                                                  (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1)])
 def test_nchw_shapes(n, cin, cout, h, w, k, p):
