@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* xbuf = b_ring + kStages * kBBytes;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int co_tiles = cout / kN, wtiles = w / kTileW, htiles = (h + kTileH - 1) / kTileH;
+  // W % 16 != 0: the last column tile is padded (TMA zero-fills the columns
+  // past W, the epilogue masks them)
+  const int co_tiles = cout / kN, wtiles = (w + kTileW - 1) / kTileW;
+  const int htiles = (h + kTileH - 1) / kTileH;
   const int cchunks = cin / kKB;
 
   if (threadIdx.x == 0) {
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         tmem_st16(taddr + ch0, zero16);  // re-arm the accumulator for tile it + 2
         tmem_st16(taddr + kN + ch0, zero16);
-        if (oh < h) {
+        if (oh < h && ow < w) {
 #pragma unroll
           for (int c = 0; c < 16; ++c)
             yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
@@ -431,11 +434,12 @@ __global__ void split_weights_kernel(const float* __restrict__ w, __nv_bfloat16*
 // Returns SC_OK / an error if the tensor-core path ran, 1 if it does not apply.
 int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
                int64_t cout, float* y, cudaStream_t st) {
-  if (cin % kKB != 0 || cout % kN != 0 || w % kTileW != 0 ||
+  if (cin % kKB != 0 || cout % kN != 0 || w % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
       nb * cout * h * w >= ((int64_t)1 << 31))
     return 1;
-  const int64_t ntiles = nb * (cout / kN) * (w / kTileW) * ((h + kTileH - 1) / kTileH);
+  const int64_t ntiles =
+      nb * (cout / kN) * ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH);
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   // dims (w, h, c, n): the box is [c][rows][cols] in shared memory

@@ -43,6 +43,10 @@ def test_config4_exact_matches_composed_oracle():
                                                  (2, 64, 64, 20, 56, 3, 1), (3, 64, 128, 9, 28, 3, 1),
                                                  (1, 32, 64, 7, 12, 3, 1), (2, 64, 64, 5, 100, 3, 1),
                                                  (1, 32, 64, 3, 4, 3, 1),
+                                                 # pixel-stationary (Cin 128 / 192), padded
+                                                 # last column tile
+                                                 (2, 128, 64, 11, 56, 3, 1), (1, 128, 128, 9, 28, 3, 1),
+                                                 (1, 192, 64, 5, 20, 3, 1), (2, 128, 64, 3, 4, 3, 1),
                                                  # Cin % 64 != 0 -> CUDA-core kernel
                                                  (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1)])
 def test_nchw_shapes(n, cin, cout, h, w, k, p):
