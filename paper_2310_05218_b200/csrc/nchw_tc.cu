@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // past W, the epilogue masks them)
   const int co_tiles = cout / kN, wtiles = (w + kTileW - 1) / kTileW;
   const int htiles = (h + kTileH - 1) / kTileH;
-  const int cchunks = cin / kKB;
+  // Cin % 64 != 0: the last chunk's channels past Cin are zero-filled by TMA in
+  // both the input box and the weight box (x 0 = 0: nothing to mask)
+  const int cchunks = (cin + kKB - 1) / kKB;
 
   if (threadIdx.x == 0) {
     zero_word = 0.0f;
@@ -434,7 +436,8 @@ __global__ void split_weights_kernel(const float* __restrict__ w, __nv_bfloat16*
 // Returns SC_OK / an error if the tensor-core path ran, 1 if it does not apply.
 int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
                int64_t cout, float* y, cudaStream_t st) {
-  if (cin % kKB != 0 || cout % kN != 0 || w % 4 != 0 ||
+  // weight rows (bf16 [tap][2 cout][cin]) must be 16-byte aligned for TMA
+  if (cin % 8 != 0 || cout % kN != 0 || w % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
       nb * cout * h * w >= ((int64_t)1 << 31))
     return 1;

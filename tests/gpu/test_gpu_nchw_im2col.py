@@ -47,8 +47,12 @@ def test_config4_exact_matches_composed_oracle():
                                                  # last column tile
                                                  (2, 128, 64, 11, 56, 3, 1), (1, 128, 128, 9, 28, 3, 1),
                                                  (1, 192, 64, 5, 20, 3, 1), (2, 128, 64, 3, 4, 3, 1),
-                                                 # Cin % 64 != 0 -> CUDA-core kernel
-                                                 (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1)])
+                                                 # Cin % 64 != 0: zero-padded channel chunk
+                                                 (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1),
+                                                 (2, 48, 64, 10, 56, 3, 1), (1, 160, 128, 6, 28, 3, 1),
+                                                 (1, 8, 64, 5, 16, 3, 1),
+                                                 # Cin % 8 != 0 -> CUDA-core kernel
+                                                 (2, 3, 64, 12, 32, 3, 1)])
 def test_nchw_shapes(n, cin, cout, h, w, k, p):
     rng = np.random.default_rng(n + cin + cout + h + w)
     x = rng.standard_normal((n, cin, h, w), dtype=np.float32)
