@@ -54,6 +54,26 @@ inline int sm_count() {
   return n[dev];
 }
 
+// Stream-ordered scratch for the few paths that need one (weight packing,
+// split partial planes, exact-mode passes).  The device's default memory
+// pool keeps up to 1 GiB of freed blocks (release threshold raised once per
+// device): with
+// the default threshold of 0 every synchronisation returns them to the
+// driver and the next call pays a fresh allocation (~tens of us).
+inline cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static bool pool_set[kMaxDevices] = {};
+  const int dev = current_device();
+  if (!pool_set[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 1ull << 30;  // keep up to 1 GiB (large exact-mode scratch is released)
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_set[dev] = true;
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
 // Raise a kernel's dynamic shared-memory limit once per device
 // (cudaFuncSetAttribute applies to the current device only); `done` is the
 // caller's per-kernel bit set of devices already configured.

@@ -824,7 +824,7 @@ int launch_generic(const T* x, int64_t batch, int64_t h, int64_t w, const T* f, 
   const int64_t oh = h - kh + 1, ow = w - kw + 1;
   T* fd = nullptr;
   const size_t fb = (size_t)(kh * kw) * sizeof(T);
-  SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&fd), fb, st));
+  SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&fd), fb, st));
   SC_CUDA(cudaMemcpyAsync(fd, f, fb, cudaMemcpyHostToDevice, st));
   const int64_t total = batch * oh * ow;
   const int64_t blocks = std::max<int64_t>(

@@ -77,11 +77,11 @@ struct BigTaps {
 
 // kWarps = 8 (64-row tiles, less halo, more warps per SM) for big grids;
 // 4 when a single image would leave SMs idle
-template <bool kExact, int kWarps, int kG>
+template <bool kExact, int kWarps, int kG, bool kSplit>
 __global__ void __launch_bounds__(32 * kWarps)
     conv2d_big_kernel(const float* __restrict__ x, int h, int w,
-                      const __grid_constant__ BigTaps ft, int kh, int kw, float* __restrict__ y,
-                      int oh, int ow) {
+                      const __grid_constant__ BigTaps ft, int kh_full, int kw,
+                      float* __restrict__ y, int oh, int ow, int nsplit, int jstep) {
   constexpr int kTileRows = tile_rows(kWarps);
   constexpr int kTileCols = tile_cols(kG);
   const float* f = ft.f;
@@ -92,16 +92,24 @@ __global__ void __launch_bounds__(32 * kWarps)
   // so the blocks of the (up to 8) filter rows one input row meets sit at
   // compile-time offsets -16 r bytes from one pointer (no per-row address
   // arithmetic in the inner loop); zero padded past kw
+  // nsplit > 1 (fast mode, small grids): CTA slice s convolves filter rows
+  // [s jstep, s jstep + kh) only -- the input shifted down by s jstep rows --
+  // into its own partial plane of y; a second kernel adds the planes in order
+  const int slice = kSplit ? blockIdx.z % nsplit : 0;
+  const int img = kSplit ? blockIdx.z / nsplit : blockIdx.z;
+  const int j0 = slice * jstep;
+  const int kh = kSplit ? min(kh_full, j0 + jstep) - j0 : kh_full;  // filter rows of this slice
   float* taps = smem;
   float* tile = smem + kh * kwp;             // [kTileRows + kh - 1][pitch]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = blockIdx.y * kTileRows, c0 = blockIdx.x * kTileCols;
-  const float* xi = x + (int64_t)blockIdx.z * h * w;
-  float* yi = y + (int64_t)blockIdx.z * oh * ow;
+  const float* xi = x + ((int64_t)img * h + j0) * w;
+  float* yi = y + (int64_t)blockIdx.z * oh * ow;  // [img][slice] planes (= img when unsplit)
+  if (kSplit) h -= j0;                       // input rows left below the shift
 
   for (int e = threadIdx.x; e < kh * kwp; e += blockDim.x) {
     const int j = e / kwp, i = e - j * kwp;
-    taps[((i >> 2) * kh + j) * 4 + (i & 3)] = i < kw ? f[j * kw + i] : 0.0f;
+    taps[((i >> 2) * kh + j) * 4 + (i & 3)] = i < kw ? f[(j0 + j) * kw + i] : 0.0f;
   }
   const int rows = kTileRows + kh - 1;
   for (int rr = warp; rr < rows; rr += kWarps) {
@@ -224,6 +232,20 @@ __global__ void __launch_bounds__(32 * kWarps)
   }
 }
 
+// y[b][i] = ((part[b][0][i] + part[b][1][i]) + ...) -- fixed order, deterministic
+__global__ void sum_planes_kernel(const float* __restrict__ part, int nsplit, int64_t plane,
+                                  int64_t batch, float* __restrict__ y) {
+  const int64_t n = batch * plane;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / plane, i = e - b * plane;
+    const float* p = part + b * nsplit * plane + i;
+    float acc = p[0];
+    for (int s = 1; s < nsplit; ++s) acc += p[s * plane];
+    y[e] = acc;
+  }
+}
+
 template <bool kExact, int kWarps, int kG>
 int launch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigTaps& taps,
                int64_t kh, int64_t kw, float* y, cudaStream_t st) {
@@ -232,13 +254,47 @@ int launch_big(const float* x, int64_t batch, int64_t h, int64_t w, const BigTap
   const int64_t oh = h - kh + 1, ow = w - kw + 1;
   const int64_t gx = (ow + kTileCols - 1) / kTileCols, gy = (oh + kTileRows - 1) / kTileRows;
   if (gy > 65535) return 1;
-  static uint64_t attr = 0;  // devices whose limit is set
-  SC_CUDA(set_smem_limit_once(conv2d_big_kernel<kExact, kWarps, kG>, (int)big_smem(kMaxK, kMaxK, kWarps, kG), &attr));
-  conv2d_big_kernel<kExact, kWarps, kG>
-      <<<dim3((unsigned)gx, (unsigned)gy, (unsigned)batch), 32 * kWarps,
-         big_smem((int)kh, (int)kw, kWarps, kG), st>>>(x, (int)h, (int)w, taps, (int)kh, (int)kw,
-                                                       y, (int)oh, (int)ow);
+  static uint64_t attr = 0, attr_split = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(conv2d_big_kernel<kExact, kWarps, kG, false>,
+                              big_smem(kMaxK, kMaxK, kWarps, kG), &attr));
+  // filter-row split for grids that leave SMs idle (fast mode only: the
+  // exact mode must accumulate every output in the reference's order)
+  // (only for grids under one wave; slices keep >= 8 filter rows so every
+  // warp still has a steady range of all-live rows)
+  int nsplit = 1, jstep = (int)kh;
+  const int64_t ctas = batch * gx * gy;
+  if (!kExact && kh >= 24 && ctas < sm_count()) {
+    const int64_t want = (3 * (int64_t)sm_count() / 2 + ctas - 1) / ctas;
+    const int n = (int)std::min<int64_t>(want, std::min<int64_t>(8, kh / 8));
+    if (n > 1) {
+      jstep = (int)((kh + n - 1) / n);
+      nsplit = (int)((kh + jstep - 1) / jstep);
+    }
+  }
+  if (batch * nsplit > 65535) nsplit = 1, jstep = (int)kh;
+  float* out = y;
+  if (nsplit > 1)
+    SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&out),
+                            (size_t)nsplit * batch * oh * ow * sizeof(float), st));
+  const dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)(batch * nsplit));
+  const size_t smem = big_smem(jstep, (int)kw, kWarps, kG);
+  if (nsplit > 1) {
+    SC_CUDA(set_smem_limit_once(conv2d_big_kernel<kExact, kWarps, kG, true>,
+                                big_smem(kMaxK, kMaxK, kWarps, kG), &attr_split));
+    conv2d_big_kernel<kExact, kWarps, kG, true><<<grid, 32 * kWarps, smem, st>>>(
+        x, (int)h, (int)w, taps, (int)kh, (int)kw, out, (int)oh, (int)ow, nsplit, jstep);
+  } else {
+    conv2d_big_kernel<kExact, kWarps, kG, false><<<grid, 32 * kWarps, smem, st>>>(
+        x, (int)h, (int)w, taps, (int)kh, (int)kw, out, (int)oh, (int)ow, 1, (int)kh);
+  }
   SC_LAUNCH_CHECK("conv2d_big_kernel");
+  if (nsplit > 1) {
+    const int64_t n = batch * oh * ow;
+    sum_planes_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4 * sm_count()), 256, 0,
+                        st>>>(out, nsplit, oh * ow, batch, y);
+    SC_LAUNCH_CHECK("sum_planes_kernel");
+    SC_CUDA(cudaFreeAsync(out, st));
+  }
   return SC_OK;
 }
 

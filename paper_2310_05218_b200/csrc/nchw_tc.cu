@@ -467,7 +467,7 @@ int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   }
   __nv_bfloat16* wsplit = nullptr;
   const size_t wbytes = (size_t)9 * 2 * cout * cin * sizeof(__nv_bfloat16);
-  SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wsplit), wbytes, st));
+  SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&wsplit), wbytes, st));
   split_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (9 * cout * cin + 255) / 256), 256, 0,
                          st>>>(wt, wsplit, (int)cin, (int)cout);
   SC_LAUNCH_CHECK("split_weights_kernel");

@@ -473,7 +473,7 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   }
   uint32_t* apack = nullptr;
   const size_t abytes = (size_t)co_tiles * 128 * (9 * cin / 2) * sizeof(uint32_t);
-  SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&apack), abytes, st));
+  SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&apack), abytes, st));
   pack_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (int64_t)(abytes / 4 + 255) / 256), 256,
                         0, st>>>(wt, apack, (int)cin, (int)cout);
   SC_LAUNCH_CHECK("pack_weights_kernel");

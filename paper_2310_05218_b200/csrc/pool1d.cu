@@ -346,7 +346,7 @@ int launch_passes(const float* x, int64_t batch, int64_t length, int64_t k, floa
   int nbuf = 2;
   if (kOp != SC_POOL_MAX) nbuf += __builtin_popcountll((unsigned long long)k) - 1;
   float* scratch = nullptr;
-  SC_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes * nbuf, st));
+  SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&scratch), bytes * nbuf, st));
   float* bufs[2] = {scratch, scratch + (size_t)batch * n};
   float* parts[64] = {nullptr};
   int next_part = 2;
