@@ -139,7 +139,7 @@ template <int B, int K>
 __global__ void __launch_bounds__(32 * kWarps, 2)
     pool_block_max_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
-                          int tiles_per_cta, int d) {
+                          int tiles_per_cta, int d, int64_t flat_L) {
   using G = Geo<B>;
   // d > 0: the window is K + d; the warp stages y_K (window K) and stores
   // max(y_K(i), y_K(i + d)) for Vd = floor32(V - d) outputs per warp
@@ -201,8 +201,61 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
         }
       }
     }
-    float* yr = y + (int64_t)row * out_len + o_in_row + lane;
     const float* sp = stage + lane;
+    if (flat_L) {
+      // flat-batch mode (signal length not a multiple of 32): the batch is one
+      // signal of B L samples; flat output p belongs to signal p / L and is
+      // kept iff p % L <= L - k, at y[p - (p / L)(k - 1)]
+      const int km1 = K + d - 1;
+      // a warp's <= 992 outputs cross at most one signal boundary (L >= 1024):
+      // warps entirely inside one signal's kept range (all but ~V / L of
+      // them) store exactly as in the aligned mode, from a shifted base
+      {
+        const int64_t w0 = (int64_t)o_in_row, wb = w0 / flat_L;
+        if (w0 + lim - 1 < wb * flat_L + flat_L - km1) {
+          float* yr = y + (w0 - wb * km1) + lane;
+          if (d == 0) {
+#pragma unroll
+            for (int mm = 0; mm < G::kOutLanes; ++mm)
+              if (32 * mm + lane < lim) yr[32 * mm] = sp[mm * kPitch];
+          } else {
+            const int ld = lane + d;
+            const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+#pragma unroll
+            for (int mm = 0; mm < G::kOutLanes; ++mm)
+              if (32 * mm + lane < lim)
+                yr[32 * mm] = zero ? mx<true>(sp[mm * kPitch], sq[mm * kPitch])
+                                   : mx<false>(sp[mm * kPitch], sq[mm * kPitch]);
+          }
+          __syncwarp();
+          continue;
+        }
+      }
+      // boundary warps: 32-bit position within the signal, pointer stepped
+      const int L32 = (int)flat_L, keep = L32 - km1;
+      const int64_t p0 = (int64_t)o_in_row + lane;
+      const int64_t bq = p0 / flat_L;
+      int rem = (int)(p0 - bq * flat_L);
+      float* yp = y + (p0 - bq * km1);
+      const int ld = lane + d;
+      const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+      const int nv = lim - lane;  // this lane's outputs: 32 mm < nv
+#pragma unroll
+      for (int mm = 0; mm < G::kOutLanes; ++mm) {
+        if (32 * mm < nv && rem < keep) {
+          const float v = d == 0 ? sp[mm * kPitch]
+                                 : (zero ? mx<true>(sp[mm * kPitch], sq[mm * kPitch])
+                                         : mx<false>(sp[mm * kPitch], sq[mm * kPitch]));
+          *yp = v;
+        }
+        rem += 32;
+        yp += 32;
+        if (rem >= L32) rem -= L32, yp -= km1;
+      }
+      __syncwarp();
+      continue;
+    }
+    float* yr = y + (int64_t)row * out_len + o_in_row + lane;
     if (d == 0) {
       if (lim == V) {
 #pragma unroll
@@ -234,9 +287,11 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
 }
 
 // k = K + d (d = 0: the plain window K)
+// flat_L > 0: x is batch signals of flat_L samples viewed as ONE signal of
+// `length` = batch * flat_L samples (batch = 1 here)
 template <int B, int K>
 int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
-           int d = 0) {
+           int d = 0, int64_t flat_L = 0) {
   using G = Geo<B>;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -267,7 +322,7 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   const int tpc = tpc_env ? tpc_env : B == 256 ? 6 : 8;
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   pool_block_max_kernel<B, K><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, d);
+      map, y, out_len, tiles_per_row, n_tiles, tpc, d, flat_L);
   SC_LAUNCH_CHECK("pool_block_max_kernel");
   return SC_OK;
 }
@@ -281,18 +336,27 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
 int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st) {
   static const bool off = getenv("SC_POOL_NO_BLOCK") != nullptr;
-  if (off || reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || length < kWin ||
-      length / 32 > 0x7fffffff || batch > 0x7fffffff)
+  if (off || reinterpret_cast<uintptr_t>(x) % 16 != 0 || length < kWin || batch > 0x7fffffff)
     return 1;
+  // signals not a multiple of 32 samples: the whole batch as one flat signal
+  // (needs B L % 32 == 0), outputs that straddle two signals dropped
+  int64_t flat_L = 0;
+  if (length % 32 != 0) {
+    if ((batch * length) % 32 != 0) return 1;
+    flat_L = length;
+    length *= batch;
+    batch = 1;
+  }
+  if (length / 32 > 0x7fffffff) return 1;
   switch (k) {
-    case 63: return launch<64, 63>(x, batch, length, y, st);
-    case 64: return launch<64, 64>(x, batch, length, y, st);
-    case 127: return launch<128, 127>(x, batch, length, y, st);
-    case 128: return launch<128, 128>(x, batch, length, y, st);
-    case 255: return launch<256, 255>(x, batch, length, y, st);
-    case 256: return launch<256, 256>(x, batch, length, y, st);
-    case 511: return launch<512, 511>(x, batch, length, y, st);
-    case 512: return launch<512, 512>(x, batch, length, y, st);
+    case 63: return launch<64, 63>(x, batch, length, y, st, 0, flat_L);
+    case 64: return launch<64, 64>(x, batch, length, y, st, 0, flat_L);
+    case 127: return launch<128, 127>(x, batch, length, y, st, 0, flat_L);
+    case 128: return launch<128, 128>(x, batch, length, y, st, 0, flat_L);
+    case 255: return launch<256, 255>(x, batch, length, y, st, 0, flat_L);
+    case 256: return launch<256, 256>(x, batch, length, y, st, 0, flat_L);
+    case 511: return launch<512, 511>(x, batch, length, y, st, 0, flat_L);
+    case 512: return launch<512, 512>(x, batch, length, y, st, 0, flat_L);
     default: break;
   }
   // any other window 34 .. 512: k = A + d with A = 32 / 64 / 128 / 256 the
@@ -301,10 +365,10 @@ int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, f
   // and cover [i, i + k - 1]; taking the later one on ties keeps the
   // rightmost maximal element, as the reference's doubling does)
   if (k > 33 && k <= 512) {  // k <= 33: pool_tma.cu is faster
-    if (k <= 64) return launch<32, 32>(x, batch, length, y, st, (int)k - 32);
-    if (k <= 128) return launch<64, 64>(x, batch, length, y, st, (int)k - 64);
-    if (k <= 256) return launch<128, 128>(x, batch, length, y, st, (int)k - 128);
-    return launch<256, 256>(x, batch, length, y, st, (int)k - 256);
+    if (k <= 64) return launch<32, 32>(x, batch, length, y, st, (int)k - 32, flat_L);
+    if (k <= 128) return launch<64, 64>(x, batch, length, y, st, (int)k - 64, flat_L);
+    if (k <= 256) return launch<128, 128>(x, batch, length, y, st, (int)k - 128, flat_L);
+    return launch<256, 256>(x, batch, length, y, st, (int)k - 256, flat_L);
   }
   return 1;
 }

@@ -104,6 +104,27 @@ def test_exact_sum_block_kernel(k):
         assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32)), (op, k)
 
 
+# signal length not a multiple of 32: the batch viewed as one flat signal
+# (B L % 32 == 0), outputs straddling two signals dropped
+@pytest.mark.parametrize("b,n", [(32, 4001), (64, 1031), (96, 2053)])
+@pytest.mark.parametrize("k", [34, 63, 64, 100, 127, 255, 256, 300, 511, 512])
+def test_flat_batch_unaligned_signals(b, n, k):
+    if k > n:
+        pytest.skip("window longer than the signal")
+    rng = np.random.default_rng(b * 7 + n + k)
+    x = rng.standard_normal((b, n), dtype=np.float32)
+    x[3, ::17] = np.float32(0.0)
+    x[5, ::19] = np.float32(-0.0)
+    xd = torch.from_numpy(x).cuda()
+    for op in ("max", "sum", "avg"):
+        want = O.pool_batched(x, k, op)
+        got = FNS[op](xd, k)[0].cpu().numpy()
+        if op == "max":
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (op, k)
+        else:
+            assert O.normwise_error(got, want) <= O.north_star_tol(k), (op, k)
+
+
 def test_reference_kats():
     assert sc.sliding_window_sum([1, 2, 3, 4, 5], 3)[0].tolist() == [6, 9, 12]
     assert sc.sliding_window_max([3, 1, 4, 1, 5], 3)[0].tolist() == [4, 4, 5]
