@@ -151,11 +151,11 @@ __device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int jb, 
   bar_consumers();
 }
 
-template <int kOp>
+template <int kOp, bool kFlat>
 __global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
     pool_wide_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y, int k,
                      int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
-                     int vt) {
+                     int vt, int64_t flat_L) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kNbuf];
   __shared__ __align__(8) uint64_t empty_bar[kNbuf];
@@ -308,17 +308,38 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
 #pragma unroll
         for (int m = 0; m < kT; ++m) o[m] *= inv_k;
       }
+      float* ys = yr;
+      if constexpr (kFlat) {
+        // flat-batch mode (SUM / AVG only): flat output p of signal p / L is
+        // kept iff p % L <= L - k, at y[p - (p / L)(k - 1)].  Tiles (3,840+
+        // outputs) inside one signal's kept range store from a shifted base;
+        // the few that straddle a boundary go element by element.
+        const int64_t tb = o0 / flat_L;
+        if (o0 + lim - 1 < tb * flat_L + flat_L - (k - 1)) {
+          ys = y + o0 - tb * (k - 1);
+        } else {
+#pragma unroll
+          for (int m = 0; m < kT; ++m) {
+            const int i = warp * (32 * kT) + 32 * m + lane;
+            const int64_t p = o0 + i, b = p / flat_L;
+            if (i < lim && p - b * flat_L < flat_L - (k - 1)) y[p - b * (k - 1)] = o[m];
+          }
+          continue;
+        }
+      }
 #pragma unroll
       for (int m = 0; m < kT; ++m) {
         const int i = warp * (32 * kT) + 32 * m + lane;
-        if (i < lim) yr[i] = o[m];
+        if (i < lim) ys[i] = o[m];
       }
     }
   }
 }
 
+// flat_L > 0: `batch` signals of flat_L samples viewed as one signal (batch = 1)
 template <int kOp>
-int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, cudaStream_t st) {
+int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, cudaStream_t st,
+           int64_t flat_L = 0) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
@@ -336,8 +357,9 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + (size_t)kNbuf * kBufBytes + (size_t)kArrBytes * 2;
-  static uint64_t attr = 0;  // devices whose limit is set
-  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp>, (int)smem, &attr));
+  static uint64_t attr = 0, attr_flat = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp, false>, (int)smem, &attr));
+  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp, true>, (int)smem, &attr_flat));
   static const int tpc = [] {  // contiguous tiles per CTA (SC_WIDE_TPC)
     const char* e = std::getenv("SC_WIDE_TPC");
     const int n = e ? std::atoi(e) : 0;
@@ -345,8 +367,12 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
   }();
   const int64_t grid = std::min<int64_t>((n_tiles + tpc - 1) / tpc,
                                          (int64_t)sm_count() * (kOp == SC_POOL_MAX ? 2 : 3));
-  pool_wide_kernel<kOp><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
-      map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt);
+  if (flat_L)
+    pool_wide_kernel<kOp, true><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
+        map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt, flat_L);
+  else
+    pool_wide_kernel<kOp, false><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
+        map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt, 0);
   SC_LAUNCH_CHECK("pool_wide_kernel");
   return SC_OK;
 }
@@ -356,12 +382,22 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
 // Returns SC_OK / an error if the wide path ran, or 1 if it does not apply.
 int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                 cudaStream_t st) {
-  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || k <= 32 || k > 2049 ||
-      length / 32 > 0x7fffffff || batch > 0x7fffffff || batch * length > (int64_t)1 << 40)
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || k <= 32 || k > 2049 ||
+      batch > 0x7fffffff || batch * length > (int64_t)1 << 40)
     return 1;
+  // signals not a multiple of 32 samples (sums / averages): the batch as one
+  // flat signal (B L % 32 == 0), outputs straddling two signals dropped
+  int64_t flat_L = 0;
+  if (length % 32 != 0) {
+    if (op == SC_POOL_MAX || (batch * length) % 32 != 0 || length < 4096) return 1;
+    flat_L = length;
+    length *= batch;
+    batch = 1;
+  }
+  if (length / 32 > 0x7fffffff) return 1;
   switch (op) {
-    case SC_POOL_SUM: return launch<SC_POOL_SUM>(x, batch, length, k, y, st);
-    case SC_POOL_AVG: return launch<SC_POOL_AVG>(x, batch, length, k, y, st);
+    case SC_POOL_SUM: return launch<SC_POOL_SUM>(x, batch, length, k, y, st, flat_L);
+    case SC_POOL_AVG: return launch<SC_POOL_AVG>(x, batch, length, k, y, st, flat_L);
     default: return launch<SC_POOL_MAX>(x, batch, length, k, y, st);
   }
 }
