@@ -91,7 +91,7 @@ template <int B, int kOp>
 __global__ void __launch_bounds__(32 * kWarps, 2)
     pool_exact_sum_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
-                          int tiles_per_cta, int k) {
+                          int tiles_per_cta, int k, int64_t flat_L) {
   using G = XGeo<B>;
   constexpr int V = G::V;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -197,6 +197,24 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     const unsigned o_in_row = (t - row * tpr) * (unsigned)(kWarps * V) + warp * V;
     const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
     float* yr = y + (int64_t)row * out_len + o_in_row + lane;
+    if (flat_L) {
+      // flat-batch mode (signal length not a multiple of 32, as in
+      // pool_block.cu): warps inside one signal's kept range store from a
+      // shifted base, boundary warps element by element
+      const int64_t w0 = (int64_t)o_in_row, wb = w0 / flat_L;
+      if (w0 + lim - 1 < wb * flat_L + flat_L - (k - 1)) {
+        yr = y + (w0 - wb * (k - 1)) + lane;
+      } else {
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm) {
+          const int64_t p = w0 + 32 * mm + lane, pb = p / flat_L;
+          if (32 * mm + lane < lim && p - pb * flat_L < flat_L - (k - 1))
+            y[p - pb * (k - 1)] = acc[mm];
+        }
+        __syncwarp();
+        continue;
+      }
+    }
     if (lim == V) {
 #pragma unroll
       for (int mm = 0; mm < G::kOutLanes; ++mm) yr[32 * mm] = acc[mm];
@@ -210,7 +228,8 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
 }
 
 template <int B, int kOp>
-int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st) {
+int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st,
+           int64_t flat_L) {
   using G = XGeo<B>;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -233,17 +252,18 @@ int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaS
   const int tpc = 8;  // contiguous tiles per CTA
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   pool_exact_sum_kernel<B, kOp><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, k);
+      map, y, out_len, tiles_per_row, n_tiles, tpc, k, flat_L);
   SC_LAUNCH_CHECK("pool_exact_sum_kernel");
   return SC_OK;
 }
 
 template <int kOp>
-int dispatch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st) {
-  if (k <= 64) return launch<64, kOp>(x, batch, length, k, y, st);
-  if (k <= 128) return launch<128, kOp>(x, batch, length, k, y, st);
-  if (k <= 256) return launch<256, kOp>(x, batch, length, k, y, st);
-  return launch<512, kOp>(x, batch, length, k, y, st);
+int dispatch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st,
+             int64_t flat_L) {
+  if (k <= 64) return launch<64, kOp>(x, batch, length, k, y, st, flat_L);
+  if (k <= 128) return launch<128, kOp>(x, batch, length, k, y, st, flat_L);
+  if (k <= 256) return launch<256, kOp>(x, batch, length, k, y, st, flat_L);
+  return launch<512, kOp>(x, batch, length, k, y, st, flat_L);
 }
 
 }  // namespace
@@ -255,11 +275,19 @@ int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int6
                      cudaStream_t st) {
   static const bool off = getenv("SC_POOL_NO_EXACT_BLOCK") != nullptr;
   if (off || (op != SC_POOL_SUM && op != SC_POOL_AVG) || k <= 32 || k > 512 ||
-      reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || length < kWin ||
-      length / 32 > 0x7fffffff || batch > 0x7fffffff)
+      reinterpret_cast<uintptr_t>(x) % 16 != 0 || length < kWin || batch > 0x7fffffff)
     return 1;
-  return op == SC_POOL_SUM ? dispatch<SC_POOL_SUM>(x, batch, length, (int)k, y, st)
-                           : dispatch<SC_POOL_AVG>(x, batch, length, (int)k, y, st);
+  // signals not a multiple of 32 samples: the batch as one flat signal
+  int64_t flat_L = 0;
+  if (length % 32 != 0) {
+    if ((batch * length) % 32 != 0) return 1;
+    flat_L = length;
+    length *= batch;
+    batch = 1;
+  }
+  if (length / 32 > 0x7fffffff) return 1;
+  return op == SC_POOL_SUM ? dispatch<SC_POOL_SUM>(x, batch, length, (int)k, y, st, flat_L)
+                           : dispatch<SC_POOL_AVG>(x, batch, length, (int)k, y, st, flat_L);
 }
 
 }  // namespace sc

@@ -123,6 +123,8 @@ def test_flat_batch_unaligned_signals(b, n, k):
             assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (op, k)
         else:
             assert O.normwise_error(got, want) <= O.north_star_tol(k), (op, k)
+            exact = FNS[op](xd, k, exact=True)[0].cpu().numpy()
+            assert np.array_equal(exact.view(np.uint32), want.view(np.uint32)), (op, k)
 
 
 def test_reference_kats():
