@@ -194,7 +194,7 @@ extern "C" int sc_conv2d_nchw_f32(const float* x, int64_t n, int64_t cin, int64_
   if (!x || !wt || !y) return fail(SC_ERR_ARG, "nchw: null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (mode == SC_MODE_FAST && kh == 3 && kw == 3 && pad == 1) {
-    // tensor cores (tcgen05 3xTF32) when the shape fits; CUDA-core FFMA otherwise
+    // tensor cores (tcgen05, bf16x3 split) when the shape fits; CUDA-core FFMA otherwise
     static const bool no_tc = [] {
       const char* e = getenv("SC_NCHW_NO_TC");
       return e && e[0] == '1';

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // W % 16 != 0: the last column tile is padded (TMA zero-fills the columns
   // past W, the epilogue masks them)
-  const int co_tiles = cout / kN, wtiles = (w + kTileW - 1) / kTileW;
+  const int co_tiles = (cout + kN - 1) / kN, wtiles = (w + kTileW - 1) / kTileW;
   const int htiles = (h + kTileH - 1) / kTileH;
   // Cin % 64 != 0: the last chunk's channels past Cin are zero-filled by TMA in
   // both the input box and the weight box (x 0 = 0: nothing to mask)
@@ -392,9 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st16(taddr + ch0, zero16);  // re-arm the accumulator for tile it + 2
         tmem_st16(taddr + kN + ch0, zero16);
         if (oh < h && ow < w) {
+          const int c_live = cout - tc.co0 - ch0;  // Cout % 64 != 0: padded channels dropped
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
+            if (c < c_live) yp[(ch0 + c) * plane] = __uint_as_float(r[c]) + __uint_as_float(rl[c]);
         }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -416,16 +417,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // w[co][ci][3][3] -> bf16 [tap][2*cout][ci]: for every 64-channel output tile,
 // rows 0..63 hold w1 = bf16(w), rows 64..127 w2 = bf16(w - w1) (the K-major
 // B operand [W1 | W2] of one N = 128 MMA per tap)
+// (cout_p = Cout rounded up to 64: the padded channels' weights are zero)
 __global__ void split_weights_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ out,
-                                     int cin, int cout) {
-  const int total = 9 * cout * cin;
+                                     int cin, int cout, int cout_p) {
+  const int total = 9 * cout_p * cin;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int ci = e % cin, co = (e / cin) % cout, tap = e / (cin * cout);
-    const float v = w[((int64_t)co * cin + ci) * 9 + tap];
+    const int ci = e % cin, co = (e / cin) % cout_p, tap = e / (cin * cout_p);
+    const float v = co < cout ? w[((int64_t)co * cin + ci) * 9 + tap] : 0.0f;
     const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
     const __nv_bfloat16 v2 = __float2bfloat16_rn(v - __bfloat162float(v1));
     const int tile = co / kN, cl = co % kN;
-    __nv_bfloat16* base = out + ((int64_t)tap * 2 * cout + (int64_t)tile * kNC) * cin;
+    __nv_bfloat16* base = out + ((int64_t)tap * 2 * cout_p + (int64_t)tile * kNC) * cin;
     base[(int64_t)cl * cin + ci] = v1;
     base[(int64_t)(kN + cl) * cin + ci] = v2;
   }
@@ -437,12 +439,13 @@ __global__ void split_weights_kernel(const float* __restrict__ w, __nv_bfloat16*
 int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, const float* wt,
                int64_t cout, float* y, cudaStream_t st) {
   // weight rows (bf16 [tap][2 cout][cin]) must be 16-byte aligned for TMA
-  if (cin % 8 != 0 || cout % kN != 0 || w % 4 != 0 ||
+  if (cin % 8 != 0 || cout < 1 || w % 4 != 0 ||
       (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
       nb * cout * h * w >= ((int64_t)1 << 31))
     return 1;
   const int64_t ntiles =
-      nb * (cout / kN) * ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH);
+      nb * ((cout + kN - 1) / kN) * ((w + kTileW - 1) / kTileW) * ((h + kTileH - 1) / kTileH);
+  const int64_t cout_p = (cout + kN - 1) / kN * kN;  // weight layout padded to 64 channels
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   // dims (w, h, c, n): the box is [c][rows][cols] in shared memory
@@ -466,14 +469,14 @@ int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
     if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "nchw tc: halo tensor map failed");
   }
   __nv_bfloat16* wsplit = nullptr;
-  const size_t wbytes = (size_t)9 * 2 * cout * cin * sizeof(__nv_bfloat16);
+  const size_t wbytes = (size_t)9 * 2 * cout_p * cin * sizeof(__nv_bfloat16);
   SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&wsplit), wbytes, st));
-  split_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (9 * cout * cin + 255) / 256), 256, 0,
-                         st>>>(wt, wsplit, (int)cin, (int)cout);
+  split_weights_kernel<<<(unsigned)std::min<int64_t>(1024, (9 * cout_p * cin + 255) / 256), 256,
+                         0, st>>>(wt, wsplit, (int)cin, (int)cout, (int)cout_p);
   SC_LAUNCH_CHECK("split_weights_kernel");
   {
-    cuuint64_t wdims[3] = {(cuuint64_t)cin, (cuuint64_t)(2 * cout), 9};
-    cuuint64_t wstrides[2] = {(cuuint64_t)(cin * 2), (cuuint64_t)(2 * cin * cout * 2)};
+    cuuint64_t wdims[3] = {(cuuint64_t)cin, (cuuint64_t)(2 * cout_p), 9};
+    cuuint64_t wstrides[2] = {(cuuint64_t)(cin * 2), (cuuint64_t)(2 * cin * cout_p * 2)};
     cuuint32_t box[3] = {kKB, kNC, 1};
     CUresult r = enc(&mw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wsplit, wdims, wstrides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

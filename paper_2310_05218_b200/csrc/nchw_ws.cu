@@ -86,8 +86,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cin = args.cin, h = args.h, w = args.w, wt = args.wt;
-  const int co_tile = blockIdx.x % (args.cout / kCo);
-  const int cta_in_co = blockIdx.x / (args.cout / kCo);
+  const int co_tiles = (args.cout + kCo - 1) / kCo;  // last tile zero-padded
+  const int co_tile = blockIdx.x % co_tiles;
+  const int cta_in_co = blockIdx.x / co_tiles;
   const int a_cols = 9 * cin / 2;
   const int ksteps = cin / 16;
   const uint32_t idesc128 = idesc_bf16(128, wt), idesc64 = idesc_bf16(64, wt);
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
       int n, w0, r0, nr;
       item_of(it, n, w0, r0, nr);
+      const bool c_live = co_tile * kCo + c < args.cout;  // padded channels are dropped
       float* ybase = y + ((int64_t)n * args.cout + co_tile * kCo + c) * plane + w0;
       for (int rr = 0; rr < nr; ++rr, ++o) {
         const int acc = o & 1;
@@ -345,8 +347,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 8; ++i) hv[i] = odd ? sum[8 + i] : sum[i];
           float* dst = yr + p0 + (odd ? 8 : 0);
-          const int live = w - w0 - p0 - (odd ? 8 : 0);  // pixels of this half in the image
-          if (live < 8) {  // W % 16 != 0: the tile is padded to 16 pixels
+          // pixels of this half in the image (W % 16 != 0 pads the tile to
+          // 16 pixels); none for a padded output channel
+          const int live = c_live ? w - w0 - p0 - (odd ? 8 : 0) : 0;
+          if (live < 8) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)
               if (i < live) dst[i] = hv[i];
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __restrict__ apack,
                                     int cin, int cout) {
   const int a_cols = 9 * cin / 2;
-  const int total = (cout / kCo) * 128 * a_cols;
+  const int total = (cout + kCo - 1) / kCo * 128 * a_cols;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int k2 = e % a_cols;
     const int m = (e / a_cols) % 128;
@@ -393,7 +397,7 @@ __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __re
     for (int t = 0; t < 2; ++t) {
       const int kidx = 2 * k2 + t;
       const int tap = kidx / cin, ci = kidx % cin;
-      const float v = wt[((int64_t)co * cin + ci) * 9 + tap];
+      const float v = co < cout ? wt[((int64_t)co * cin + ci) * 9 + tap] : 0.0f;
       const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
       const __nv_bfloat16 part = hlf ? __float2bfloat16_rn(v - __bfloat162float(v1)) : v1;
       packed |= (uint32_t)__bfloat16_as_ushort(part) << (16 * t);
@@ -419,7 +423,7 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   // of 16 pixels (TMA zero-fills the columns past W, the epilogue masks
   // them); the x rows must still be 16-byte aligned for TMA (W % 4 == 0)
   const bool padded = w % 16 != 0;
-  if (cin > kMaxCin || cin % 32 != 0 || cout % kCo != 0 || w % 4 != 0 ||
+  if (cin > kMaxCin || cin % 32 != 0 || cout < 1 || w % 4 != 0 ||
       (padded && w > kMaxWt) ||
       (reinterpret_cast<uintptr_t>(x) & 15) || nb * cin * h * w >= ((int64_t)1 << 31) ||
       nb * cout * h * w >= ((int64_t)1 << 31) || h < 1)
@@ -431,7 +435,7 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   a.nb = (int)nb, a.cin = (int)cin, a.h = (int)h, a.w = (int)w, a.cout = (int)cout;
   a.wt = tw;
   a.col_tiles = padded ? 1 : (int)(w / tw);
-  const int co_tiles = (int)(cout / kCo);
+  const int co_tiles = (int)((cout + kCo - 1) / kCo);
   const int sms = sm_count();
   a.ctas_per_co = std::max(1, sms / co_tiles);
   // Segment length: the CTAs (one per SM) walk items of seg_rows output rows

@@ -51,6 +51,9 @@ def test_config4_exact_matches_composed_oracle():
                                                  (2, 32, 64, 16, 32, 3, 1), (3, 96, 64, 9, 16, 3, 1),
                                                  (2, 48, 64, 10, 56, 3, 1), (1, 160, 128, 6, 28, 3, 1),
                                                  (1, 8, 64, 5, 16, 3, 1),
+                                                 # Cout % 64 != 0: zero-padded output tile
+                                                 (2, 64, 32, 9, 48, 3, 1), (1, 64, 96, 7, 56, 3, 1),
+                                                 (2, 128, 40, 5, 32, 3, 1), (1, 32, 8, 6, 16, 3, 1),
                                                  # Cin % 8 != 0 -> CUDA-core kernel
                                                  (2, 3, 64, 12, 32, 3, 1)])
 def test_nchw_shapes(n, cin, cout, h, w, k, p):
