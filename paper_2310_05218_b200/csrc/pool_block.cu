@@ -135,7 +135,7 @@ __device__ __forceinline__ bool block_max(const unsigned char* rowp, int swz, in
 // kNbuf-deep TMA ring without a producer warp: the first load of each slot
 // is issued up front, and the LAST warp to finish with a slot (a shared
 // counter) refills it with the CTA's next tile at once.
-template <int B, int K>
+template <int B, int K, bool kFlat>
 __global__ void __launch_bounds__(32 * kWarps, 2)
     pool_block_max_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
       }
     }
     const float* sp = stage + lane;
-    if (flat_L) {
+    if constexpr (kFlat) {
       // flat-batch mode (signal length not a multiple of 32): the batch is one
       // signal of B L samples; flat output p belongs to signal p / L and is
       // kept iff p % L <= L - k, at y[p - (p / L)(k - 1)]
@@ -310,8 +310,9 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + G::kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
-  static uint64_t attr = 0;  // devices whose limit is set
-  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<B, K>, (int)smem, &attr));
+  static uint64_t attr = 0, attr_flat = 0;  // devices whose limit is set
+  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<B, K, false>, (int)smem, &attr));
+  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<B, K, true>, (int)smem, &attr_flat));
   // contiguous runs of tiles per CTA (tools/pbcheck.py sweep on config 2:
   // 6 tiles for B = 256, 8 otherwise); env override
   static const int tpc_env = [] {
@@ -321,8 +322,12 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   }();
   const int tpc = tpc_env ? tpc_env : B == 256 ? 6 : 8;
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
-  pool_block_max_kernel<B, K><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, d, flat_L);
+  if (flat_L)
+    pool_block_max_kernel<B, K, true><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+        map, y, out_len, tiles_per_row, n_tiles, tpc, d, flat_L);
+  else
+    pool_block_max_kernel<B, K, false><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+        map, y, out_len, tiles_per_row, n_tiles, tpc, d, 0);
   SC_LAUNCH_CHECK("pool_block_max_kernel");
   return SC_OK;
 }
