@@ -344,7 +344,20 @@ def per_config(torch, sc, hbm_peak, args, traffic):
     o = 65530
     nb = 4 * (65536 * 65536 + o * o + 49)
     fl = 2 * o * o * 49
+    # contrast: im2col + cuBLAS over the whole image in chunks of 256 output
+    # rows (the full column matrix would be 784 GiB; one chunk is 3.3 GB)
+    yc = torch.empty((o, o), device=dev)
+    cols = torch.empty(256 * o * 49, device=dev)
+    fdk = torch.from_numpy(f7.reshape(-1)).to(dev)
+
+    def contrast5():
+        lib.sc_conv2d_im2col_f32(xb.data_ptr(), 65536, 65536, fdk.data_ptr(), 7, 7,
+                                 cols.data_ptr(), 256, yc.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream)
+    tc5 = time_launches(torch, contrast5, 1, 1)
+    del yc, cols
     out["cfg5_7x7_65536"] = {"ms": round(t * 1e3, 3), **roofline(nb, fl, t, hbm_peak),
+                             "im2col_cublas_ms": round(tc5 * 1e3, 1),
                              "cpu": cpu_rate("conv2d", {"cfg": 5, "h": 262, "w": 65536, "k": 7,
                                                         "lo": -1.0}, 8,
                                              4 * (262 * 65536 + 256 * 65530), 2 * 256 * 65530 * 49)}
