@@ -267,6 +267,15 @@ def per_config(torch, sc, hbm_peak, args, traffic):
             row[name] = {"ms": round(t * 1e3, 4), **roofline(nb, fl, t, hbm_peak)}
         row["cpu_sum"] = cpu_rate("pool", {"cfg": 2, "n": L, "k": k, "ops": ("sum",)}, 32,
                                   4 * (L + L - k + 1), 0)
+        # library contrast on the same GPU: PyTorch's avg / max pooling (cuDNN-
+        # free native kernels), stride 1, same input
+        import torch.nn.functional as F
+        x3 = xp.unsqueeze(1)
+        row["torch_pool_ms"] = {
+            "avg": round(time_launches(torch, lambda: F.avg_pool1d(x3, k, stride=1), reps,
+                                       warm) * 1e3, 4),
+            "max": round(time_launches(torch, lambda: F.max_pool1d(x3, k, stride=1), reps,
+                                       warm) * 1e3, 4)}
         out[f"cfg2_pool_k{k}"] = row
     del xp
 
