@@ -711,10 +711,12 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
     const char* e = getenv("SC_CONV_ROWS");
     return e ? atoi(e) : 0;
   }();
-  // long row segments (less halo re-reading; measured best at ~900 rows)
-  // measured (tools/conv_sweep.py): ~890 rows for the FP32-bound 7 x 7, ~450
-  // for the bandwidth-bound 5 x 5 (shorter segments keep streams adjacent)
-  const int64_t seg_rows = K >= 7 ? 896 : 450;
+  // measured (tools/conv_sweep.py): long segments for the FP32-bound 7 x 7
+  // (then refined by the wave model below); 96-row segments for the
+  // bandwidth-bound 5 x 5 (config 3: 446 rows 0.707 ms -> 96 rows 0.654 ms,
+  // i.e. 1.0 of the HBM copy peak: many short CTAs keep the streams adjacent
+  // and the last wave short)
+  const int64_t seg_rows = K >= 7 ? 896 : 100;
   int64_t rows = env_rows > 0 ? env_rows : (int64_t)c4_rs(K) * (seg_rows / c4_rs(K)) - (K - 1);
   const size_t smem = (size_t)kC4Stages * kC4Warps * c4_sub(K) * sizeof(float) + 128;
   static uint64_t attr = 0;  // devices whose limit is set
