@@ -679,7 +679,7 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
     // concurrently streamed rows adjacent in HBM for the bandwidth-bound
     // sizes; the FP32-bound 7x7 prefers long segments (less halo re-work).
     // Segment length = RS*m - (KH-1) so the last stage carries no waste.
-    const int m = KH >= 7 ? 64 : (KH == 1 ? 7 : (KH == 3 ? 5 : 6));
+    const int m = KH >= 7 ? 64 : (KH == 1 ? 7 : (KH == 3 ? 3 : 6));  // 3x3: 34 rows (58: +2.5 %)
     rows = (int64_t)RS * m - (KH - 1);
   }
   rows = std::min<int64_t>(rows, oh);
