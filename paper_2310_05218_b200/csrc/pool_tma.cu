@@ -297,7 +297,18 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
                       (size_t)kTmaWarps * 32 * kStageStride * sizeof(float);
   static uint64_t attr = 0;  // devices whose limit is set
   SC_CUDA(set_smem_limit_once(pool_tma_kernel<kOp, K, NBUF>, (int)smem, &attr));
-  const int tpc = env_int("SC_POOL_TPC", 4, 1, 64);
+  // contiguous tiles per CTA, measured per op / window on config 2 and 1
+  // (tools/pool_sweep.py, conv_sweep.py): light kernels (few doubling stages,
+  // no division) stream best with 2, heavier ones with 4 -- e.g. k = 16 avg
+  // 84.5 -> 82.4 us at 2, k = 16 max 88.2 at 2 vs 82.9 at 4, conv1d k = 7
+  // 86.0 -> 84.2 us at 2
+  constexpr bool kPow2 = (K & (K - 1)) == 0;
+  constexpr int kTpcDefault =
+      kOp == SC_POOL_SUM ? (K <= 24 ? 2 : 4)
+      : kOp == SC_POOL_AVG ? ((kPow2 && K <= 16) || K == 3 ? 2 : 4)
+      : kOp == SC_POOL_MAX ? (K <= 8 ? 2 : 4)
+      : 2;  // weighted (conv1d) windows
+  const int tpc = env_int("SC_POOL_TPC", kTpcDefault, 1, 64);
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   Taps1<K> taps{};
   if (w)
