@@ -27,6 +27,11 @@
 // case -- a +0/-0 tie -- where the two rules can differ) re-reads its window
 // and redoes it with np_max.
 //
+// Signals whose length is not a multiple of 32 (the 3-D tensor map needs
+// 128-byte rows) are processed as ONE flat signal of B L samples: windows
+// that straddle two signals are computed and dropped at the store
+// (kFlat instantiation).
+//
 // Tiles of 8 warps x (1024 - B) outputs arrive by one 2-D TMA box each in a
 // 2- or 3-deep ring (no producer warp: the last warp done with a slot refills
 // it), two 8-warp CTAs per SM, CTAs own contiguous runs of tiles; outputs are
