@@ -23,6 +23,10 @@
 //    The fast pass uses max.NaN; if any output of the tile is zero (the only
 //    case where the two rules can differ: a +0/-0 tie) the tile is redone
 //    with np.maximum semantics.
+//  * Persistent CTAs walk grid-strided pairs of contiguous tiles.  Sums on
+//    signals whose length is not a multiple of 32 view the batch as one flat
+//    signal (kFlat instantiation), dropping the windows that straddle two
+//    signals at the store.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
