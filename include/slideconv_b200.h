@@ -82,6 +82,14 @@ int sc_conv1d_f32(const float* x, int64_t batch, int64_t length, const float* w,
 int sc_conv2d_f32(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                   int64_t kh, int64_t kw, int mode, float* y, void* stream);
 
+/* Introspection (new; no reference counterpart): output rows per CTA row
+ * segment of the tiling sc_conv2d_f32 launches for this shape and mode, 0 when
+ * the chosen kernel does not tile rows that way (only the 5x5 / 7x7
+ * four-column kernels report one), -1 for invalid dims.  Tests use it to
+ * oracle-check windows that straddle segment boundaries. */
+int64_t sc_conv2d_segment_rows(int64_t batch, int64_t h, int64_t w, int64_t kh, int64_t kw,
+                               int mode);
+
 /* Same formula in float64 -- replaces oracle_conv2d (reference.py:42-47). */
 int sc_conv2d_f64(const double* x, int64_t batch, int64_t h, int64_t w, const double* f,
                   int64_t kh, int64_t kw, double* y, void* stream);

@@ -8,12 +8,19 @@ Methodology follows the reference benchmark (pkg/src/slideconv/bench.py:71-78,
 itself to a single core); work is sharded by unit (signal / image / band);
 inputs are generated inside the workers BEFORE a barrier, so generation is
 excluded from the timed region; wall time = last finish - first start.
+
+The worker processes are PERSISTENT (`CpuPool`): started once, pinned once,
+inputs generated once per task and kept; every timed step is then a barrier
+plus the compute, so consecutive steps measure the same thing (round 1 spawned
+fresh processes every step, and two arms of the same run disagreed by 2x).
 """
 
 from __future__ import annotations
 
+import atexit
 import multiprocessing as mp
 import os
+import statistics
 import time
 
 import numpy as np
@@ -40,7 +47,7 @@ def cpu_model() -> str:
 
 
 # --------------------------------------------------------------------- tasks
-# task = (kind, params); unit = integer index -> (inputs, bytes, flops)
+# task = (kind, params); unit = integer index -> inputs
 
 def _gen(kind, p, unit):
     rng = np.random.default_rng([0x5EED, p["cfg"], unit])
@@ -85,40 +92,102 @@ def _compute(kind, p, inputs, w):
         return
 
 
-def _worker(core, kind, p, units, barrier, q):
+def _task_key(kind, p, units):
+    return (kind, tuple(sorted((k, tuple(v) if isinstance(v, (list, tuple)) else v)
+                               for k, v in p.items())), tuple(units))
+
+
+def _pool_worker(core, conn, barrier):
     try:
         os.sched_setaffinity(0, {core})
     except (AttributeError, OSError):
         pass
-    w = _weights(kind, p)
-    data = [_gen(kind, p, u) for u in units]
-    barrier.wait()
-    t0 = time.perf_counter()
-    for inp in data:
-        _compute(kind, p, inp, w)
-    t1 = time.perf_counter()
-    q.put((t0, t1, len(units)))
+    cache = {}
+    while True:
+        msg = conn.recv()
+        if msg[0] == "stop":
+            return
+        _, kind, p, units = msg
+        key = _task_key(kind, p, units)
+        if key not in cache:
+            cache.clear()                      # one task's inputs resident at a time
+            cache[key] = (_weights(kind, p), [_gen(kind, p, u) for u in units])
+        w, data = cache[key]
+        conn.send("ready")
+        barrier.wait()
+        t0 = time.perf_counter()
+        for inp in data:
+            _compute(kind, p, inp, w)
+        t1 = time.perf_counter()
+        conn.send((t0, t1, len(units)))
+
+
+class CpuPool:
+    """One pinned process per host core, started once."""
+
+    def __init__(self, workers: int | None = None):
+        cores = host_cores()
+        self.workers = max(1, min(workers or len(cores), len(cores)))
+        ctx = mp.get_context("spawn")
+        self._barrier = ctx.Barrier(self.workers)
+        self._conns, self._procs = [], []
+        for i in range(self.workers):
+            a, b = ctx.Pipe()
+            pr = ctx.Process(target=_pool_worker, args=(cores[i], b, self._barrier), daemon=True)
+            pr.start()
+            self._conns.append(a)
+            self._procs.append(pr)
+
+    def run(self, kind: str, p: dict, n_units: int) -> dict:
+        """Time n_units of the task sharded over all workers (every worker
+        joins the barrier, idle ones with no units)."""
+        shards = [list(range(i, n_units, self.workers)) for i in range(self.workers)]
+        for c, s in zip(self._conns, shards):
+            c.send(("run", kind, p, s))
+        for c in self._conns:
+            assert c.recv() == "ready"
+        res = [c.recv() for c in self._conns]
+        busy = [r for r in res if r[2] > 0]
+        t0 = min(r[0] for r in busy)
+        t1 = max(r[1] for r in busy)
+        return {"seconds": t1 - t0, "units": n_units, "cores": len(busy)}
+
+    def close(self):
+        for c in self._conns:
+            try:
+                c.send(("stop",))
+            except (OSError, BrokenPipeError):
+                pass
+        for pr in self._procs:
+            pr.join(timeout=10)
+
+
+_POOL: CpuPool | None = None
+
+
+def get_pool() -> CpuPool:
+    global _POOL
+    if _POOL is None:
+        _POOL = CpuPool()
+        atexit.register(_POOL.close)
+    return _POOL
 
 
 def time_units(kind: str, p: dict, n_units: int, workers: int | None = None) -> dict:
-    """Run n_units of the task across `workers` pinned processes; return
-    {'seconds': wall, 'units': n_units, 'cores': workers}."""
-    cores = host_cores()
-    workers = max(1, min(workers or len(cores), n_units))
-    ctx = mp.get_context("spawn")
-    barrier = ctx.Barrier(workers)
-    q = ctx.Queue()
-    shards = [list(range(i, n_units, workers)) for i in range(workers)]
-    procs = [ctx.Process(target=_worker, args=(cores[i % len(cores)], kind, p, shards[i], barrier, q))
-             for i in range(workers)]
-    for pr in procs:
-        pr.start()
-    res = [q.get() for _ in procs]
-    for pr in procs:
-        pr.join()
-    t0 = min(r[0] for r in res)
-    t1 = max(r[1] for r in res)
-    return {"seconds": t1 - t0, "units": n_units, "cores": workers}
+    """One timed run of n_units across the persistent pinned pool (`workers`
+    is accepted for compatibility; the pool always uses every host core)."""
+    return get_pool().run(kind, p, n_units)
+
+
+def time_steps(kind: str, p: dict, n_units: int, steps: int, warmup: int = 1) -> dict:
+    """The estimator both bench arms use: median over `steps` timed runs
+    after `warmup` untimed ones, on the persistent pool."""
+    pool = get_pool()
+    for _ in range(warmup):
+        pool.run(kind, p, n_units)
+    secs = [pool.run(kind, p, n_units)["seconds"] for _ in range(steps)]
+    return {"seconds": statistics.median(secs), "all": secs, "units": n_units,
+            "cores": pool.workers}
 
 
 def time_one_core(kind: str, p: dict, n_units: int) -> float:

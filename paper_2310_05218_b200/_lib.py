@@ -36,6 +36,7 @@ SIGNATURES = {
     "sc_pool1d_stages": (_i64, [_int, _i64]),
     "sc_conv1d_f32": (_int, [_vp, _i64, _i64, _vp, _i64, _int, _vp, _vp]),
     "sc_conv2d_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _vp]),
+    "sc_conv2d_segment_rows": (_i64, [_i64, _i64, _i64, _i64, _i64, _int]),
     "sc_conv2d_f64": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "sc_conv2d_nchw_f32": (_int, [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64,
                                   _int, _vp, _vp]),

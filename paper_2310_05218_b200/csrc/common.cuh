@@ -78,11 +78,16 @@ inline cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
 // (cudaFuncSetAttribute applies to the current device only); `done` is the
 // caller's per-kernel bit set of devices already configured.
 template <typename F>
-cudaError_t set_smem_limit_once(F* func, size_t bytes, uint64_t* done) {
+cudaError_t set_smem_limit_once(F* func, size_t bytes, uint64_t* done, int carveout = -1) {
   const uint64_t bit = 1ull << current_device();
   if (__atomic_load_n(done, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
-  const cudaError_t e =
+  cudaError_t e =
       cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  // carveout (percent of the unified L1 / shared array given to shared
+  // memory): the driver otherwise may pick a configuration that fits only
+  // one CTA per SM (a 100 KB carveout for two 85 KB CTAs, say)
+  if (e == cudaSuccess && carveout >= 0)
+    e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
   if (e == cudaSuccess) __atomic_fetch_or(done, bit, __ATOMIC_RELEASE);
   return e;
 }

@@ -696,16 +696,12 @@ int launch_tma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   return SC_OK;
 }
 
+// Row-segment length (output rows per CTA) of the 4-column kernel for this
+// grid; shared by the launch and by sc_conv2d_segment_rows (test / tooling
+// introspection of where CTA segment boundaries fall).
 template <int K, bool kExact>
-int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, float* y,
-                 cudaStream_t st) {
-  constexpr int BW = c4_box(K);
+int cols4_rows(int64_t batch, int64_t h, int64_t w, int64_t* rows_out) {
   const int64_t oh = h - K + 1, ow = w - K + 1;
-  CUtensorMap map;
-  int rc = make_tmap(&map, x, batch, h, w, BW, c4_rs(K));
-  if (rc) return rc;
-  Taps<K, K> taps;
-  for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
   const int64_t strips = (ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols);
   static const int env_rows = [] {
     const char* e = getenv("SC_CONV_ROWS");
@@ -744,6 +740,25 @@ int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const floa
       if (best < 0 || cost < best) best = cost, rows = r;
     }
   }
+  *rows_out = std::min<int64_t>(rows, oh);
+  return SC_OK;
+}
+
+
+template <int K, bool kExact>
+int launch_cols4(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, float* y,
+                 cudaStream_t st) {
+  constexpr int BW = c4_box(K);
+  const int64_t oh = h - K + 1, ow = w - K + 1;
+  CUtensorMap map;
+  int rc = make_tmap(&map, x, batch, h, w, BW, c4_rs(K));
+  if (rc) return rc;
+  Taps<K, K> taps;
+  for (int i = 0; i < K * K; ++i) taps.f[i] = f[i];
+  const int64_t strips = (ow + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols);
+  const size_t smem = (size_t)kC4Stages * kC4Warps * c4_sub(K) * sizeof(float) + 128;
+  int64_t rows = 0;
+  if ((rc = cols4_rows<K, kExact>(batch, h, w, &rows))) return rc;
   rows = std::min<int64_t>(rows, oh);
   const int64_t segs = (oh + rows - 1) / rows;
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
@@ -930,6 +945,28 @@ extern "C" int sc_conv2d_f32(const float* x, int64_t batch, int64_t h, int64_t w
   if (rc || batch == 0) return rc;
   return sc::conv2d_f32_dispatch(x, batch, h, w, f, kh, kw, mode == SC_MODE_EXACT, y,
                                  static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t sc_conv2d_segment_rows(int64_t batch, int64_t h, int64_t w, int64_t kh,
+                                          int64_t kw, int mode) {
+  // mirrors try_tma's choice of the 4-column kernel (16-byte aligned input)
+  using namespace sc;
+  if (batch < 1 || kh < 1 || kw < 1 || kh > h || kw > w) return -1;
+  if (kh != kw || (kh != 5 && kh != 7) || w % 4 != 0 || h * w >= (int64_t)1 << 40) return 0;
+  const bool pairs = getenv(kh == 7 ? "SC_CONV7_PAIRS" : "SC_CONV5_PAIRS") &&
+                     getenv(kh == 7 ? "SC_CONV7_PAIRS" : "SC_CONV5_PAIRS")[0] == '1';
+  const int64_t ctas = batch * ((w - kw + 1 + kC4Warps * kC4Cols - 1) / (kC4Warps * kC4Cols)) *
+                       ((h - kh + 1 + 255) / 256);
+  if (pairs || w < c4_box((int)kh) || ctas < 2 * sm_count() ||
+      h < (kh == 7 ? RowsPerStage<7>::value : RowsPerStage<5>::value))
+    return 0;
+  int64_t rows = 0;
+  const bool exact = mode == SC_MODE_EXACT;
+  int rc = kh == 7 ? (exact ? cols4_rows<7, true>(batch, h, w, &rows)
+                            : cols4_rows<7, false>(batch, h, w, &rows))
+                   : (exact ? cols4_rows<5, true>(batch, h, w, &rows)
+                            : cols4_rows<5, false>(batch, h, w, &rows));
+  return rc ? -1 : rows;
 }
 
 extern "C" int sc_conv1d_f32(const float* x, int64_t batch, int64_t length, const float* wt,

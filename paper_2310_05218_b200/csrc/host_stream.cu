@@ -258,8 +258,12 @@ extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t
                         }});
     }
   } else {
-    // one signal is larger than a chunk: segments with a k-1 sample overlap
-    const int64_t seg = std::max<int64_t>(1, (int64_t)(kChunkBytes / sizeof(float)) - (k - 1));
+    // one signal is larger than a chunk: segments with a k-1 sample overlap.
+    // Each segment carries at least 3 (k - 1) outputs (the chunk grows with
+    // k), so the re-sent overlap stays under a quarter of the traffic even
+    // when k - 1 exceeds the nominal chunk.
+    const int64_t seg = std::max<int64_t>(
+        {1, (int64_t)(kChunkBytes / sizeof(float)) - (k - 1), 3 * (k - 1)});
     for (int64_t r = 0; r < batch; ++r)
       for (int64_t o = 0; o < out_len; o += seg) {
         const int64_t no = std::min(seg, out_len - o);
@@ -304,9 +308,11 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
                         }});
     }
   } else {
-    // row bands with a kh-1 row halo (bit-identical to the whole image)
-    const int64_t band = std::max<int64_t>(1, (int64_t)kChunkBytes / (w * (int64_t)sizeof(float)) -
-                                                  (kh - 1));
+    // row bands with a kh-1 row halo (bit-identical to the whole image); at
+    // least 3 (kh - 1) output rows per band so the re-sent halo stays under a
+    // quarter of the traffic for tall filters on wide images
+    const int64_t band = std::max<int64_t>(
+        {1, (int64_t)kChunkBytes / (w * (int64_t)sizeof(float)) - (kh - 1), 3 * (kh - 1)});
     for (int64_t b = 0; b < batch; ++b) {
       int64_t o_next = 0;
       for (const int64_t no : ramp_sizes(oh, band, std::max<int64_t>(1, band / 8))) {

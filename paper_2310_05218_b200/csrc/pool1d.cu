@@ -11,8 +11,9 @@
 //    rotation by r, so shifts by multiples of 32 are free.  Operation order is
 //    the reference's, hence sums are bit-exact; max uses np.maximum's
 //    operand order (pooling.py:70,75), hence bit-exact including NaN and +-0.
-//  * pool_prefix_kernel -- FAST-mode window sums for wide windows: O(1) work
-//    per output from a tile-local float64 prefix staged in shared memory.
+//  * pool_prefix_kernel -- FAST-mode window sums for very wide windows: O(1)
+//    work per output from two float64 scans (backward / forward) that meet at
+//    a split point inside every window of the tile, staged in shared memory.
 //  * pool_pass_kernel -- one doubling / combine pass over global memory, the
 //    reference's numpy pass verbatim; used for EXACT sums with many set bits
 //    and for very wide windows.
@@ -194,10 +195,49 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock)
 }
 
 // ------------------------------------------------------------ prefix kernel
-// FAST window sums: y(i) = float(Q(i+k-1) - Q(i-1)) with Q the float64
-// inclusive prefix of the tile's input, anchored at the tile start.
+// FAST window sums (very wide windows, and wide windows the TMA kernel cannot
+// take: unaligned pointers / ragged batches).  Every window i of a chunk of
+// at most k - 1 outputs [c0, c) contains the split point c, so
+//   y(i) = float(S(i) + P(i + k - 1)),  S(i) = sum x[i .. c),  P(m) = sum x[c .. m]
+// with S a backward and P a forward float64 inclusive scan.  Each output only
+// ever sums samples of its own window: a non-finite or huge sample outside it
+// cannot leak in (a prefix difference Q(i + k) - Q(i) would turn every later
+// output of the tile into NaN after one inf).
 constexpr int kPrefixThreads = 256;
 constexpr int kPrefixTile = 2048;
+
+// inclusive scan of xs[lo_g, hi_g) into q[] at the same indices; backward
+// (q[i] = sum_{j >= i} x[j]) when kRev
+template <bool kRev>
+__device__ __forceinline__ void block_scan_f64(const float* xs, double* q, int lo_g, int hi_g,
+                                               double* warp_tot) {
+  const int n = hi_g - lo_g;
+  const int E = (n + kPrefixThreads - 1) / kPrefixThreads;
+  const int lo = threadIdx.x * E;
+  const int hi = min(lo + E, n);
+  auto at = [&](int j) { return kRev ? hi_g - 1 - j : lo_g + j; };
+  double run = 0.0;
+  for (int j = lo; j < hi; ++j) run += (double)xs[at(j)];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double inc = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  // exclusive prefix of this thread from the lane to its left (inc - run
+  // would turn an inf in this thread's own run into inf - inf = NaN)
+  double acc = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) acc = 0.0;
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) acc += warp_tot[w];
+  for (int j = lo; j < hi; ++j) {
+    acc += (double)xs[at(j)];
+    q[at(j)] = acc;
+  }
+  __syncthreads();  // q complete; warp_tot free for the next scan
+}
 
 template <int kOp>
 __global__ void __launch_bounds__(kPrefixThreads)
@@ -209,44 +249,27 @@ __global__ void __launch_bounds__(kPrefixThreads)
   const int64_t out_len = length - k + 1;
   const int n_out = (int)min((int64_t)kPrefixTile, out_len - t0);
   const int n_in = n_out + k - 1;
-  double* q = reinterpret_cast<double*>(smem_raw);  // [n_in + 1], q[0] = 0
+  double* q = reinterpret_cast<double*>(smem_raw);  // [n_in]
   float* xs = reinterpret_cast<float*>(q + (kPrefixTile + k));
   const float* xr = x + row * length + t0;
   for (int i = threadIdx.x; i < n_in; i += kPrefixThreads) xs[i] = __ldg(xr + i);
-  __syncthreads();
-
-  // blocked scan: thread t owns elements [t*E, (t+1)*E)
-  const int E = (n_in + kPrefixThreads - 1) / kPrefixThreads;
-  const int lo = threadIdx.x * E;
-  const int hi = min(lo + E, n_in);
-  double run = 0.0;
-  for (int i = lo; i < hi; ++i) run += (double)xs[i];
-  // warp inclusive scan of thread totals
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double inc = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    double t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
   __shared__ double warp_tot[kPrefixThreads / 32];
-  if (lane == 31) warp_tot[warp] = inc;
-  __syncthreads();
-  double off = 0.0;
-  for (int w = 0; w < warp; ++w) off += warp_tot[w];
-  double acc = off + inc - run;  // exclusive prefix of this thread
-  if (threadIdx.x == 0) q[0] = 0.0;
-  for (int i = lo; i < hi; ++i) {
-    acc += (double)xs[i];
-    q[i + 1] = acc;
-  }
   __syncthreads();
   float* yr = y + row * out_len + t0;
   const float fk = (float)k;
-  for (int i = threadIdx.x; i < n_out; i += kPrefixThreads) {
-    float v = (float)(q[i + k] - q[i]);
-    if (kOp == SC_POOL_AVG) v = __fdiv_rn(v, fk);
-    yr[i] = v;
+  // chunks of at most k - 1 outputs, so one split point lies in every window
+  // of a chunk (one chunk for the k > 2,048 windows this kernel is tuned for)
+  const int C = min(n_out, k - 1);
+  for (int c0 = 0; c0 < n_out; c0 += C) {
+    const int cn = min(C, n_out - c0), c = c0 + cn;
+    block_scan_f64<true>(xs, q, c0, c, warp_tot);         // S over [c0, c)
+    block_scan_f64<false>(xs, q, c, c + k - 1, warp_tot);  // P over [c, c + k - 1)
+    for (int i = c0 + threadIdx.x; i < c; i += kPrefixThreads) {
+      float v = (float)(q[i] + q[i + k - 1]);
+      if (kOp == SC_POOL_AVG) v = __fdiv_rn(v, fk);
+      yr[i] = v;
+    }
+    __syncthreads();  // q is rewritten by the next chunk
   }
 }
 

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
   const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
   auto issue = [&](unsigned t, int b) {
     const unsigned row = t / tpr;
-    const unsigned s0 = (t - row * tpr) * (unsigned)(kWarps * V);
+    const int64_t s0 = (int64_t)(t - row * tpr) * (kWarps * V);  // 64-bit: flat batches exceed 2^32 samples
     mbar_arrive_expect_tx(&full_bar[b], G::kRows * 128);
     tma_load_3d(base + b * G::kBuf, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
   };
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     mbar_wait(&full_bar[b], (it / kNbuf) & 1);
     const unsigned char* rowp = base + b * G::kBuf + row0 * 128;
     const unsigned row = t / tpr;
-    const unsigned o_in_row = (t - row * tpr) * (unsigned)(kWarps * V) + warp * V;
+    const int64_t o_in_row = (int64_t)(t - row * tpr) * (kWarps * V) + warp * V;
     const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
     float* srow = stage + lane * kPitch;
     const int lim_k = d ? G::V : lim;  // y_K outputs the combine reads

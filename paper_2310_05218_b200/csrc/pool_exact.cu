@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
   const unsigned nt = (unsigned)min(n_tiles, (int64_t)t_begin + tiles_per_cta);
   auto issue = [&](unsigned t, int b) {
     const unsigned row = t / tpr;
-    const unsigned s0 = (t - row * tpr) * (unsigned)(kWarps * V);
+    const int64_t s0 = (int64_t)(t - row * tpr) * (kWarps * V);  // 64-bit: flat batches exceed 2^32 samples
     mbar_arrive_expect_tx(&full_bar[b], G::kRows * 128);
     tma_load_3d(base + b * G::kBuf, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
   };
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     }
     if constexpr (kOp == SC_POOL_AVG) div_all_by_k<G::kOutLanes>(acc, fk, rk);
     const unsigned row = t / tpr;
-    const unsigned o_in_row = (t - row * tpr) * (unsigned)(kWarps * V) + warp * V;
+    const int64_t o_in_row = (int64_t)(t - row * tpr) * (kWarps * V) + warp * V;
     const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
     float* yr = y + (int64_t)row * out_len + o_in_row + lane;
     if (flat_L) {

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
         const int b = i % NBUF;
         if (i >= NBUF) mbar_wait_sleep(&empty_bar[b], ((i / NBUF) - 1) & 1);
         const unsigned row = t / tpr;
-        const unsigned s0 = (t - row * tpr) * (unsigned)(kTmaWarps * V);
+        const int64_t s0 = (int64_t)(t - row * tpr) * (kTmaWarps * V);  // 64-bit: flat batches exceed 2^32 samples
         mbar_arrive_expect_tx(&full_bar[b], tma_rows(K) * 128);
         tma_load_3d(base + b * BUF, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
       }
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
           make_float4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
     __syncwarp();
     const unsigned row = t / tpr;
-    const unsigned o_in_row = (t - row * tpr) * (unsigned)(kTmaWarps * V) + warp * V;
+    const int64_t o_in_row = (int64_t)(t - row * tpr) * (kTmaWarps * V) + warp * V;
     const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
     float* yr = y + (int64_t)row * out_len + o_in_row + lane;
     const float* sp = stage + (lane / T) * kStageStride + (lane % T);

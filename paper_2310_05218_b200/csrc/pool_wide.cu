@@ -3,17 +3,24 @@
 // Replaces the doubling of pooling.py:28-78 for wide windows (BASELINE config
 // 2 sweep, k = 64 / 255), where log2(k) register-doubling stages or a global
 // pass per stage would cost far more than the 8 bytes of HBM traffic per
-// output.  Same TMA / warp-specialised skeleton as pool_tma.cu: a producer
-// warp streams tiles of 4,096 samples (128 swizzled rows of 32 floats) into a
-// 2-deep ring, CTAs own contiguous runs of tiles; 8 consumer warps hold the
+// output.  TMA streams tiles of 4,096 samples (128 swizzled rows of 32
+// floats) into a 3-deep ring (thread 0 refills a slot after the CTA barrier
+// that shows it consumed), two persistent CTAs per SM own contiguous runs of
+// tiles; 8 warps hold the
 // tile blocked in registers (16 samples per lane).  Each tile yields
 // vt = 4096 - roundup32(k - 1) outputs.
 //
-//  * SUM / AVG (fast mode): tile-anchored exclusive prefix E (lane-local scan,
-//    warp shuffle scan, cross-warp offsets) written to shared memory, then
-//    y(i) = E(i + k) - E(i) read lane-striped -> coalesced stores.  Anchoring
-//    every 4,096 samples bounds |E| and the cancellation error (measured
-//    ~1e-7 normwise vs the reference for N(0,1); tolerance 1e-5 k).
+//  * SUM / AVG (fast mode): van Herk / Gil-Werman with '+' -- segments of k
+//    samples anchored at the tile start, P = running sum from the segment
+//    start, S = running sum to the segment end, y(i) = S(i) + P(i + k - 1)
+//    (P is stored as 0 at segment ends, which is what the window that starts
+//    ON a segment start needs: S(i) alone).  Every output is a sum over its
+//    own window's samples only, so an inf / NaN / huge value elsewhere in
+//    the tile (or in the neighbouring signal in flat-batch mode) cannot leak
+//    into it, and the rounding error scales with the window's own magnitude
+//    (measured 2.6e-7 normwise at k = 255 on N(0,1) data; tolerance 1e-5 k).
+//    A tile-anchored prefix difference E(i + k) - E(i) was used before: it
+//    let one non-finite sample turn every later output of the tile into NaN.
 //  * MAX (always bit-exact): van Herk / Gil-Werman -- segments of k samples
 //    anchored at the tile start; P = running max from the segment start,
 //    S = running max to the segment end (segmented lane / warp / CTA scans),
@@ -44,8 +51,10 @@ constexpr int kT = 16;                 // samples per lane
 constexpr int kRows = 128;             // TMA box rows of 32 floats
 constexpr int kTile = kRows * 32;      // 4096 samples per tile
 constexpr int kBufBytes = kTile * 4;   // 16 KiB
-constexpr int kNbuf = 2;
-constexpr int kArrBytes = kBufBytes + 1024;  // one spare swizzle row (E[4096])
+constexpr int kNbuf = 3;
+// X reads at i + k - 1 run up to 2,048 floats past the tile for outputs
+// beyond vt (never stored): they land inside arr_s, which follows arr_x
+constexpr int kArrBytes = kBufBytes;
 
 // float position -> byte offset in a 128-byte-swizzled array of 32-float rows
 __device__ __forceinline__ int swz(int p) {
@@ -70,151 +79,214 @@ __device__ __forceinline__ bool bar_consumers_or(bool pred) {
   return r != 0;
 }
 
-template <bool kExact>
-__device__ __forceinline__ float mx(float a, float b) {  // a earlier, b later
-  if constexpr (kExact) return np_max(a, b);
+// combine ops of the segmented scans (a earlier, b later)
+constexpr int kCombMaxFast = 0, kCombMaxExact = 1, kCombAdd = 2;
+template <int kComb>
+__device__ __forceinline__ float mx(float a, float b) {
+  if constexpr (kComb == kCombMaxExact) return np_max(a, b);
+  else if constexpr (kComb == kCombAdd) return a + b;
   else return max_nan(a, b);
 }
 
-// van Herk / Gil-Werman max over a tile: segments of k samples anchored at
-// the tile start (k > kT, so a lane's 16 samples hold at most one segment
-// start jb and at most one segment end e).  P(p) = running max from the
-// segment start, S(p) = running max to the segment end, as segmented scans:
-// lane-local, then across lanes (shuffles) and warps (shared memory).  Every
-// combine is mx(earlier, later), so ties keep the rightmost maximal element.
-// Writes P and S to shared memory (swizzled like the tile).
-template <bool kExact>
-__device__ __forceinline__ void vhgw_tile(const float (&s)[kT], int p0, int jb, int e, int warp,
-                                          int lane, unsigned char* arr_p, unsigned char* arr_s,
-                                          float* wv, int* wf) {
-  const float kId = -__int_as_float(0x7f800000);  // -inf: identity of max
-  float P[kT], S[kT];
-  // ---- lane-local segmented scans: prefix (reset at the segment start jb),
-  // suffix (reset at the segment end e)
-  P[0] = s[0];
+// Window op over a tile, every output from its own window's samples only.
+// Output i (lane a = i / 16 of the tile, offset r = i % 16) covers
+//   [i, end of lane a] + c full lanes + [start of lane b, i + k - 1],
+// c = c0 or c0 + 1 with c0 = (k - 1) / 16 - 1 (c = c0 + 1 iff r + (k - 1) % 16
+// >= 16).  So with LANE-LOCAL suffix Sf / prefix Pf (no
+// segment resets inside a lane: plain register scans) and, per lane L, the op
+// of the c0 (G0) or c0 + 1 (G1) lane totals just before L,
+//   X(q) = op(G_sel(lane(q)), Pf(q)),   y(i) = op(Sf(i), X(i + k - 1)),
+// where the choice sel depends only on q % 16 (j < (k - 1) % 16 -> G1).  G0 / G1
+// are sliding windows over the 256 lane totals of the tile: van Herk /
+// Gil-Werman at lane granularity (segments of c0 lanes, segmented shuffle
+// scans + one cross-warp carry), G0(L) = op(S_T(L - c0), P_T(L - 1)).  Every
+// combine is op(earlier, later), so for max ties keep the rightmost maximal
+// element (np.maximum's order, pooling.py:70-76) and sums add only window
+// samples.  Writes Sf and X to shared memory (swizzled like the tile).
+struct WideLane {   // per-lane constants (same for every tile)
+  int lg;           // lane index in the tile, 0..255
+  int c0;           // full lanes in the shorter window middle
+  int km;           // (k - 1) % 16: positions j < km of a lane take G1
+  bool seg_start;   // lg % c0 == 0   (lane-total segments of c0 lanes)
+  bool seg_end;     // lg % c0 == c0 - 1
+  int u;            // lg - c0: first lane of this lane's c0-lane window
+  bool u_start;     // u >= 0 and u starts a segment (the window IS a segment)
+};
+
+template <int kComb>
+__device__ __forceinline__ void wide_tile(const float (&s)[kT], const WideLane& wl, int warp,
+                                          int lane, unsigned char* arr_x, unsigned char* arr_s,
+                                          float* tot, float* pt, float* st_, float* wagg,
+                                          int* wflag) {
+  const float kId = kComb == kCombAdd ? 0.0f : -__int_as_float(0x7f800000);  // identity
+  // ---- lane-local prefix / suffix (plain scans: no resets inside a lane)
+  float pf[kT], sf[kT];
+  pf[0] = s[0];
 #pragma unroll
-  for (int j = 1; j < kT; ++j) P[j] = (j == jb) ? s[j] : mx<kExact>(P[j - 1], s[j]);
-  S[kT - 1] = s[kT - 1];
+  for (int j = 1; j < kT; ++j) pf[j] = mx<kComb>(pf[j - 1], s[j]);
+  sf[kT - 1] = s[kT - 1];
 #pragma unroll
-  for (int j = kT - 2; j >= 0; --j) S[j] = (j == e) ? s[j] : mx<kExact>(s[j], S[j + 1]);
-  // ---- across lanes (shuffles): inclusive segmented scans of the lane
-  // aggregates, left to right for P, right to left for S
-  float pv = P[kT - 1], sv = S[0];
-  int pf = jb < kT, sf = e >= 0;
+  for (int j = kT - 2; j >= 0; --j) sf[j] = mx<kComb>(s[j], sf[j + 1]);
+  const float T = pf[kT - 1];
+  // ---- segmented scans of the lane totals across the warp (segments of c0
+  // lanes in tile lane space): P_T from the segment start, S_T to its end
+  float pv = T, sv = T;
+  int pfl = wl.seg_start, sfl = wl.seg_end;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const float upv = __shfl_up_sync(0xffffffffu, pv, d);
-    const int upf = __shfl_up_sync(0xffffffffu, pf, d);
+    const int upf = __shfl_up_sync(0xffffffffu, pfl, d);
     const float dnv = __shfl_down_sync(0xffffffffu, sv, d);
-    const int dnf = __shfl_down_sync(0xffffffffu, sf, d);
-    if (lane >= d) {
-      if (!pf) pv = mx<kExact>(upv, pv);
-      pf |= upf;
+    const int dnf = __shfl_down_sync(0xffffffffu, sfl, d);
+    if (lane >= d && !pfl) {
+      pv = mx<kComb>(upv, pv);
+      pfl = upf;
     }
-    if (lane + d < 32) {
-      if (!sf) sv = mx<kExact>(sv, dnv);
-      sf |= dnf;
+    if (lane + d < 32 && !sfl) {
+      sv = mx<kComb>(sv, dnv);
+      sfl = dnf;
     }
   }
-  // ---- across warps (one barrier): warp totals to shared memory
+  // ---- across warps: warp aggregates, then a segmented 8-lane scan
   if (lane == 31) {
-    wv[warp] = pv;
-    wf[warp] = pf;
+    wagg[warp] = pv;
+    wflag[warp] = pfl;
   }
   if (lane == 0) {
-    wv[kWarps + warp] = sv;
-    wf[kWarps + warp] = sf;
+    wagg[kWarps + warp] = sv;
+    wflag[kWarps + warp] = sfl;
   }
-  float cpv = __shfl_up_sync(0xffffffffu, pv, 1);    // exclusive, from the left
-  const int cpf = __shfl_up_sync(0xffffffffu, pf, 1);
-  float csv = __shfl_down_sync(0xffffffffu, sv, 1);  // exclusive, from the right
-  const int csf = __shfl_down_sync(0xffffffffu, sf, 1);
   bar_consumers();
-  float wl = kId, wr = kId;
-  for (int w = 0; w < warp; ++w) wl = wf[w] ? wv[w] : mx<kExact>(wl, wv[w]);
-  for (int w = kWarps - 1; w > warp; --w)
-    wr = wf[kWarps + w] ? wv[kWarps + w] : mx<kExact>(wv[kWarps + w], wr);
-  if (lane == 0) cpv = wl;
-  else if (!cpf) cpv = mx<kExact>(wl, cpv);
-  if (lane == 31) csv = wr;
-  else if (!csf) csv = mx<kExact>(csv, wr);
+  {
+    // lanes 0..7: P aggregates of warps 0..7 (left to right); lanes 8..15: S
+    // aggregates of warps 7..0 (right to left) -- one segmented scan each
+    const int w = lane & 7;
+    const bool is_s = lane >= 8 && lane < 16;
+    float av = kId;
+    int af = 0;
+    if (lane < 16) {
+      av = wagg[is_s ? kWarps + (kWarps - 1 - w) : w];
+      af = wflag[is_s ? kWarps + (kWarps - 1 - w) : w];
+    }
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) {
+      const float uv = __shfl_up_sync(0xffffffffu, av, d);
+      const int uf = __shfl_up_sync(0xffffffffu, af, d);
+      if (w >= d && !af) {
+        av = is_s ? mx<kComb>(av, uv) : mx<kComb>(uv, av);
+        af = uf;
+      }
+    }
+    // carry into this warp: inclusive scan at warp - 1 (from the left) and
+    // at the mirrored lane of warp + 1 (from the right)
+    const float cl = __shfl_sync(0xffffffffu, av, warp > 0 ? warp - 1 : 0);
+    const float cr = __shfl_sync(0xffffffffu, av, warp < kWarps - 1 ? 8 + (kWarps - 2 - warp) : 8);
+    if (warp > 0 && !pfl) pv = mx<kComb>(cl, pv);
+    if (warp < kWarps - 1 && !sfl) sv = mx<kComb>(sv, cr);
+  }
+  tot[wl.lg] = T;
+  pt[wl.lg] = pv;
+  st_[wl.lg] = sv;
+  bar_consumers();
+  // ---- G0 / G1 for this lane: op of the c0 / c0 + 1 lane totals before it
+  float g0 = kId, g1 = kId;
+  {
+    const int u = wl.u;
+    if (u >= 0) {
+      const float sfx = st_[u];
+      g0 = wl.u_start ? sfx : mx<kComb>(sfx, pt[wl.lg - 1]);
+      g1 = (u >= 1) ? mx<kComb>(tot[u - 1], g0) : g0;
+    }
+  }
+  // ---- X = op(G_sel, Pf) and Sf to shared memory (swizzled, 16-byte stores)
+  const int p0 = wl.lg * kT;
 #pragma unroll
   for (int q = 0; q < kT / 4; ++q) {
-    float4 p4, s4;
-    p4.x = (4 * q + 0 < jb) ? mx<kExact>(cpv, P[4 * q + 0]) : P[4 * q + 0];
-    p4.y = (4 * q + 1 < jb) ? mx<kExact>(cpv, P[4 * q + 1]) : P[4 * q + 1];
-    p4.z = (4 * q + 2 < jb) ? mx<kExact>(cpv, P[4 * q + 2]) : P[4 * q + 2];
-    p4.w = (4 * q + 3 < jb) ? mx<kExact>(cpv, P[4 * q + 3]) : P[4 * q + 3];
-    s4.x = (4 * q + 0 > e) ? mx<kExact>(S[4 * q + 0], csv) : S[4 * q + 0];
-    s4.y = (4 * q + 1 > e) ? mx<kExact>(S[4 * q + 1], csv) : S[4 * q + 1];
-    s4.z = (4 * q + 2 > e) ? mx<kExact>(S[4 * q + 2], csv) : S[4 * q + 2];
-    s4.w = (4 * q + 3 > e) ? mx<kExact>(S[4 * q + 3], csv) : S[4 * q + 3];
-    *reinterpret_cast<float4*>(arr_p + swz(p0 + 4 * q)) = p4;
+    float4 x4, s4;
+    x4.x = mx<kComb>((4 * q + 0 < wl.km) ? g1 : g0, pf[4 * q + 0]);
+    x4.y = mx<kComb>((4 * q + 1 < wl.km) ? g1 : g0, pf[4 * q + 1]);
+    x4.z = mx<kComb>((4 * q + 2 < wl.km) ? g1 : g0, pf[4 * q + 2]);
+    x4.w = mx<kComb>((4 * q + 3 < wl.km) ? g1 : g0, pf[4 * q + 3]);
+    s4 = make_float4(sf[4 * q], sf[4 * q + 1], sf[4 * q + 2], sf[4 * q + 3]);
+    *reinterpret_cast<float4*>(arr_x + swz(p0 + 4 * q)) = x4;
     *reinterpret_cast<float4*>(arr_s + swz(p0 + 4 * q)) = s4;
   }
   bar_consumers();
 }
 
 template <int kOp, bool kFlat>
-__global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
+__global__ void __launch_bounds__(32 * kWarps, 2)
     pool_wide_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y, int k,
                      int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
                      int vt, int64_t flat_L) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kNbuf];
-  __shared__ __align__(8) uint64_t empty_bar[kNbuf];
-  __shared__ float wv[kWarps];
+  __shared__ float tot[kWarps * 32], pt[kWarps * 32], st_[kWarps * 32];
+  __shared__ float wagg[2 * kWarps];
+  __shared__ int wflag[2 * kWarps];
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  unsigned char* arr_a = base + kNbuf * kBufBytes;   // E (sum) or P (max)
-  unsigned char* arr_b = arr_a + kArrBytes;         // S (max)
+  unsigned char* arr_x = base + kNbuf * kBufBytes;   // X (op of window middle + lane prefix)
+  unsigned char* arr_s = arr_x + kArrBytes;         // Sf (lane-local suffix)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) {
-    for (int i = 0; i < kNbuf; ++i) {
-      mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], kWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
   const unsigned tpr = (unsigned)tiles_per_row;
   // persistent CTAs: groups of tiles_per_cta contiguous tiles, grid-strided
   // (a CTA per group paid a pipeline fill -- the first tile's full load
-  // latency -- every few tiles)
+  // latency -- every few tiles).  Iteration i of this CTA handles tile
+  // tile_of(i) while it < n_tiles (only the last group can be short).
   const unsigned n_t = (unsigned)n_tiles, tpc = (unsigned)tiles_per_cta;
   const unsigned g_stride = gridDim.x * tpc;
-
-  if (warp == kWarps) {
-    if (lane == 0) {
-      prefetch_tmap(&tmap);
-      int i = 0;
-      for (unsigned g0 = blockIdx.x * tpc; g0 < n_t; g0 += g_stride)
-      for (unsigned t = g0; t < min(n_t, g0 + tpc); ++t, ++i) {
-        const int b = i % kNbuf;
-        if (i >= kNbuf) mbar_wait_sleep(&empty_bar[b], ((i / kNbuf) - 1) & 1);
-        const unsigned row = t / tpr;
-        const unsigned s0 = (t - row * tpr) * (unsigned)vt;
-        mbar_arrive_expect_tx(&full_bar[b], kBufBytes);
-        tma_load_3d(base + b * kBufBytes, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
-      }
+  auto tile_of = [&](unsigned i) { return blockIdx.x * tpc + (i / tpc) * g_stride + i % tpc; };
+  // No producer warp (a 9th warp would cap the CTA at 96 registers for two
+  // CTAs per SM: 5 warps on one SM sub-partition): thread 0 refills a ring
+  // slot once a CTA barrier shows every warp has its tile in registers.
+  auto issue = [&](unsigned i) {
+    const unsigned t = tile_of(i);
+    if (t >= n_t) return;
+    const int b = i % kNbuf;
+    const unsigned row = t / tpr;
+    const int64_t s0 = (int64_t)(t - row * tpr) * vt;  // 64-bit: flat batches exceed 2^32 samples
+    mbar_arrive_expect_tx(&full_bar[b], kBufBytes);
+    tma_load_3d(base + b * kBufBytes, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
+  };
+  if (tid == 0) {
+    prefetch_tmap(&tmap);
+    for (int i = 0; i < kNbuf; ++i) mbar_init(&full_bar[i], 1);
+    fence_mbar_init();
+    for (int i = 0; i < kNbuf; ++i) issue(i);
+  }
+  __syncthreads();
+  auto refill = [&](unsigned i) {  // after a CTA barrier: slot i % kNbuf is free
+    if (tid == 0) {
+      fence_proxy_async();
+      issue(i + kNbuf);
     }
-    return;
+  };
+
+  WideLane wl;
+  wl.lg = warp * 32 + lane;
+  wl.c0 = (k - 1) / kT - 1;  // >= 1 for k > 32
+  wl.km = (k - 1) % kT;
+  wl.seg_start = wl.lg % wl.c0 == 0;
+  wl.seg_end = wl.lg % wl.c0 == wl.c0 - 1;
+  wl.u = wl.lg - wl.c0;
+  wl.u_start = wl.u >= 0 && wl.u % wl.c0 == 0;
+  const int p0 = wl.lg * kT;
+  const float inv_k = 1.0f / (float)k;
+  // output loop addresses: output m of this lane is i = warp*512 + 32 m + lane;
+  // swz() repeats every 8 rows, so 8 byte offsets per array (+1024 B per 8 m)
+  // serve all 16 reads of Sf(i) and of X(i + k - 1)
+  int off_s[8], off_x[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int i = warp * (32 * kT) + 32 * m + lane;
+    off_s[m] = swz(i);
+    off_x[m] = swz(i + k - 1);
   }
 
-  const int p0 = warp * (32 * kT) + kT * lane;
-  const float fk = (float)k;
-  const float inv_k = 1.0f / fk;
-  // vHGW segment start / end inside this lane (same for every tile)
-  const int first_start = (p0 + k - 1) / k * k;  // first multiple of k >= p0
-  const int jb = first_start - p0 < kT ? first_start - p0 : kT;
-  const int end_pos = (p0 / k + 1) * k - 1;      // end of p0's segment
-  const int e = end_pos - p0 < kT ? end_pos - p0 : -1;
-  __shared__ float seg_v[2 * kWarps];
-  __shared__ int seg_f[2 * kWarps];
-  int it = 0;
-  for (unsigned g0 = blockIdx.x * tpc; g0 < n_t; g0 += g_stride)
-  for (unsigned t = g0; t < min(n_t, g0 + tpc); ++t, ++it) {
+  for (unsigned it = 0;; ++it) {
+    const unsigned t = tile_of(it);
+    if (t >= n_t) break;
     const int b = it % kNbuf;
     mbar_wait(&full_bar[b], (it / kNbuf) & 1);
     const unsigned char* buf = base + b * kBufBytes;
@@ -229,86 +301,54 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
         s[4 * q + 3] = v4.w;
       }
     };
-    auto release = [&]() {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[b]);
-    };
     load();
 
     const unsigned row = t / tpr;
     const int64_t o0 = (int64_t)(t - row * tpr) * vt;
     float* yr = y + (int64_t)row * out_len + o0;
     const int lim = (int)min((int64_t)vt, out_len - o0);
+    auto out_at = [&](int m) {  // y(i) read back from shared memory
+      return mx<kOp == SC_POOL_MAX ? kCombMaxFast : kCombAdd>(
+          *reinterpret_cast<const float*>(arr_s + off_s[m & 7] + (m >> 3) * 1024),
+          *reinterpret_cast<const float*>(arr_x + off_x[m & 7] + (m >> 3) * 1024));
+    };
 
     if constexpr (kOp == SC_POOL_MAX) {
-      release();  // the window stays in registers for a possible exact redo
       // fast pass (max.NaN), stored at once; if any output of the tile is zero
-      // (a +0/-0 tie may resolve differently) the tile is redone exactly
-      vhgw_tile<false>(s, p0, jb, e, warp, lane, arr_a, arr_b, seg_v, seg_f);
+      // (a +0/-0 tie may resolve differently) the tile -- still in registers --
+      // is redone with np.maximum semantics
+      wide_tile<kCombMaxFast>(s, wl, warp, lane, arr_x, arr_s, tot, pt, st_, wagg, wflag);
+      refill(it);  // wide_tile's barriers: every warp has its samples in registers
       bool zero = false;
 #pragma unroll
       for (int m = 0; m < kT; ++m) {
         const int i = warp * (32 * kT) + 32 * m + lane;
         if (i < lim) {
-          const float o = mx<false>(*reinterpret_cast<const float*>(arr_b + swz(i)),
-                                    *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
+          const float o = out_at(m);
           zero |= (o == 0.0f);
           yr[i] = o;
         }
       }
       if (bar_consumers_or(zero)) {
-        vhgw_tile<true>(s, p0, jb, e, warp, lane, arr_a, arr_b, seg_v, seg_f);
+        wide_tile<kCombMaxExact>(s, wl, warp, lane, arr_x, arr_s, tot, pt, st_, wagg, wflag);
 #pragma unroll
         for (int m = 0; m < kT; ++m) {
           const int i = warp * (32 * kT) + 32 * m + lane;
           if (i < lim)
-            yr[i] = mx<true>(*reinterpret_cast<const float*>(arr_b + swz(i)),
-                             *reinterpret_cast<const float*>(arr_a + swz(i + k - 1)));
+            yr[i] = np_max(*reinterpret_cast<const float*>(arr_s + off_s[m & 7] + (m >> 3) * 1024),
+                           *reinterpret_cast<const float*>(arr_x + off_x[m & 7] + (m >> 3) * 1024));
         }
         bar_consumers();
       }
     } else {
-      release();  // window in registers: hand the ring slot back at once
-      // exclusive prefix, tile-anchored: lane-local, warp shuffle, warp offsets
-      float e[kT];
-      float acc = 0.0f;
-#pragma unroll
-      for (int j = 0; j < kT; ++j) {
-        e[j] = acc;
-        acc += s[j];
-      }
-      float inc = acc;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const float o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-      }
-      float excl = __shfl_up_sync(0xffffffffu, inc, 1);
-      if (lane == 0) excl = 0.0f;
-      if (lane == 31) wv[warp] = inc;
-      bar_consumers();
-      float off = 0.0f;
-      for (int w = 0; w < warp; ++w) off += wv[w];
-      const float base_e = off + excl;
-#pragma unroll
-      for (int q = 0; q < kT / 4; ++q)
-        *reinterpret_cast<float4*>(arr_a + swz(p0 + 4 * q)) =
-            make_float4(base_e + e[4 * q], base_e + e[4 * q + 1], base_e + e[4 * q + 2],
-                        base_e + e[4 * q + 3]);
-      if (warp == kWarps - 1 && lane == 31)
-        *reinterpret_cast<float*>(arr_a + swz(kTile)) = off + inc;  // E(4096)
-      bar_consumers();
+      wide_tile<kCombAdd>(s, wl, warp, lane, arr_x, arr_s, tot, pt, st_, wagg, wflag);
+      refill(it);  // wide_tile's barriers: every warp has its samples in registers
       float o[kT];
 #pragma unroll
-      for (int m = 0; m < kT; ++m) {
-        int i = warp * (32 * kT) + 32 * m + lane;
-        i = (i < vt) ? i : 0;  // keep the E(i + k) read inside the tile
-        o[m] = *reinterpret_cast<const float*>(arr_a + swz(i + k)) -
-               *reinterpret_cast<const float*>(arr_a + swz(i));
-      }
+      for (int m = 0; m < kT; ++m) o[m] = out_at(m);  // reads past the tile: unused
       if constexpr (kOp == SC_POOL_AVG) {
-        // fast mode only (the prefix difference is already not bit-exact):
-        // multiply by the reciprocal; exact mode never reaches this kernel
+        // fast mode only (exact mode never reaches this kernel): multiply by
+        // the reciprocal
 #pragma unroll
         for (int m = 0; m < kT; ++m) o[m] *= inv_k;
       }
@@ -325,8 +365,8 @@ __global__ void __launch_bounds__(32 * (kWarps + 1), kOp == SC_POOL_MAX ? 2 : 3)
 #pragma unroll
           for (int m = 0; m < kT; ++m) {
             const int i = warp * (32 * kT) + 32 * m + lane;
-            const int64_t p = o0 + i, b = p / flat_L;
-            if (i < lim && p - b * flat_L < flat_L - (k - 1)) y[p - b * (k - 1)] = o[m];
+            const int64_t p = o0 + i, b2 = p / flat_L;
+            if (i < lim && p - b2 * flat_L < flat_L - (k - 1)) y[p - b2 * (k - 1)] = o[m];
           }
           continue;
         }
@@ -362,20 +402,25 @@ int launch(const float* x, int64_t batch, int64_t length, int64_t k, float* y, c
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + (size_t)kNbuf * kBufBytes + (size_t)kArrBytes * 2;
   static uint64_t attr = 0, attr_flat = 0;  // devices whose limit is set
-  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp, false>, (int)smem, &attr));
-  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp, true>, (int)smem, &attr_flat));
+  SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp, false>, (int)smem, &attr, 100));
+  if constexpr (kOp != SC_POOL_MAX)
+    SC_CUDA(set_smem_limit_once(pool_wide_kernel<kOp, true>, (int)smem, &attr_flat, 100));
   static const int tpc = [] {  // contiguous tiles per CTA (SC_WIDE_TPC)
     const char* e = std::getenv("SC_WIDE_TPC");
     const int n = e ? std::atoi(e) : 0;
     return (n >= 1 && n <= 1024) ? n : 2;
   }();
   const int64_t grid = std::min<int64_t>((n_tiles + tpc - 1) / tpc,
-                                         (int64_t)sm_count() * (kOp == SC_POOL_MAX ? 2 : 3));
-  if (flat_L)
-    pool_wide_kernel<kOp, true><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
-        map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt, flat_L);
-  else
-    pool_wide_kernel<kOp, false><<<(unsigned)grid, 32 * (kWarps + 1), smem, st>>>(
+                                         (int64_t)sm_count() * 2);
+  if constexpr (kOp != SC_POOL_MAX) {  // flat-batch mode: sums / averages only
+    if (flat_L) {
+      pool_wide_kernel<kOp, true><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+          map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt, flat_L);
+      SC_LAUNCH_CHECK("pool_wide_kernel");
+      return SC_OK;
+    }
+  }
+  pool_wide_kernel<kOp, false><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
         map, y, (int)k, out_len, tiles_per_row, n_tiles, tpc, vt, 0);
   SC_LAUNCH_CHECK("pool_wide_kernel");
   return SC_OK;

@@ -81,6 +81,8 @@ def exchange_halo(x_local, halo: int, group=None, recv=None):
     import torch.distributed as dist
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
+    if x_local.is_cuda and dist.get_backend(group) != "nccl":
+        return _exchange_halo_staged(x_local, halo, group, recv)
     ops = []
     if halo > 0 and world > 1:
         if rank > 0:
@@ -99,6 +101,48 @@ def exchange_halo(x_local, halo: int, group=None, recv=None):
         recv = None
     works = dist.batch_isend_irecv(ops) if ops else []
     return recv, works
+
+
+class _StagedWork:
+    """Completion handle of a host-staged exchange: wait() finishes the CPU
+    P2P ops, then copies the received rows into the caller's device buffer."""
+
+    def __init__(self, works, host_recv, recv):
+        self._works, self._host_recv, self._recv = works, host_recv, recv
+
+    def wait(self):
+        for wk in self._works:
+            wk.wait()
+        if self._recv is not None:
+            self._recv.copy_(self._host_recv)
+            self._recv = None
+        return True
+
+
+def _exchange_halo_staged(x_local, halo, group, recv):
+    """The same exchange for backends without device P2P (gloo): the halo
+    rows travel through host memory; the band compute stays on the GPU."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    if halo <= 0 or world <= 1:
+        return None, []
+    peer = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    ops, host_recv = [], None
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, x_local[:halo].to("cpu").contiguous(), peer(rank - 1),
+                              group))
+    if rank < world - 1:
+        if recv is None:
+            recv = torch.empty((halo,) + tuple(x_local.shape[1:]), dtype=x_local.dtype,
+                               device=x_local.device)
+        host_recv = torch.empty(tuple(recv.shape), dtype=recv.dtype)
+        ops.append(dist.P2POp(dist.irecv, host_recv, peer(rank + 1), group))
+    else:
+        recv = None
+    works = dist.batch_isend_irecv(ops) if ops else []
+    return recv, [_StagedWork(works, host_recv, recv)]
 
 
 def alloc_band(rows: int, w: int, kh: int, device=None):

@@ -184,6 +184,16 @@ def test_host_pipeline_band_path_large_image():
     assert np.array_equal(got, O.conv2d_batched(x, f))
 
 
+def test_host_pipeline_tall_filter_on_wide_rows(monkeypatch):
+    """kh - 1 >= the rows one host chunk holds: bands carry >= 3 (kh - 1)
+    output rows (host_stream.cu) and stay bit-identical to the whole image."""
+    monkeypatch.setenv("SC_HOST_CHUNK_MB", "1")        # 1 MiB chunks = one 262,144-wide row
+    x = rand(79, (1, 64, 262144))
+    f = rand(80, (9, 9))
+    got = sc.conv2d_reference(x, f, exact=True)
+    assert np.array_equal(got, O.conv2d_batched(x, f))
+
+
 def test_unaligned_device_pointer_uses_generic_path():
     x = torch.from_numpy(rand(3, (1, 200 * 400 + 1))).cuda()
     view = x[0, 1:].reshape(200, 400)                 # 4-byte aligned only

@@ -27,6 +27,19 @@ def test_config4_exact_matches_composed_oracle():
     assert np.array_equal(got, O.conv2d_nchw(x, w, 1))
 
 
+def test_config4_full_size_exact_bit_identical():
+    """Config 4 at full size (N 16, Cin = Cout = 64, 112^2, 3x3, pad 1) in
+    exact mode against the composed oracle (per (n, co): sum over ci ascending
+    of the reference's single-channel conv of the padded plane)."""
+    rng = np.random.default_rng([0x5EED, 4])
+    x = rng.standard_normal((16, 64, 112, 112), dtype=np.float32)
+    w = (rng.standard_normal((64, 64, 3, 3), dtype=np.float32) / np.float32(24.0)).astype(np.float32)
+    got = sc.conv2d_nchw(torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), 1,
+                         exact=True).cpu().numpy()
+    want = O.conv2d_nchw(x, w, 1)
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("n,cin,cout,h,w,k,p", [(1, 3, 5, 17, 23, 3, 1), (2, 7, 70, 33, 9, 3, 1),
                                                  (1, 4, 4, 10, 10, 5, 2), (1, 2, 3, 8, 8, 3, 0),
                                                  # tcgen05 bf16x3 path (Cin % 64, Cout % 64, W % 16):

@@ -175,6 +175,18 @@ def test_host_pipeline_single_signal_larger_than_a_chunk():
     assert np.array_equal(sc.sliding_window_sum(x, 16)[0], want)
 
 
+def test_host_pipeline_window_wider_than_a_chunk():
+    """k - 1 larger than the host pipeline's chunk: segments grow with k (at
+    least 3 (k - 1) outputs each) instead of degenerating to one output per
+    chunk (host_stream.cu)."""
+    rng = np.random.default_rng(61)
+    x = rng.standard_normal(4_000_000, dtype=np.float32)       # 16 MB, chunk 8 MB
+    k = 3_000_000
+    assert np.array_equal(sc.sliding_window_max(x, k)[0], O.sliding_window_max(x, k)[0])
+    got = sc.sliding_window_sum(x, k, exact=True)[0]
+    assert np.array_equal(got, O.sliding_window_sum(x, k)[0])
+
+
 def test_batch_leading_dims_and_empty_batch():
     x = np.random.default_rng(1).standard_normal((2, 3, 100), dtype=np.float32)
     y, _ = sc.sliding_window_sum(x, 5)
