@@ -2,15 +2,24 @@
 the reference CPU path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--dry-run]
 
 Headline workload (BASELINE.json configs[1]): 256 signals x 262,144 samples
 N(0,1), window 16; one STEP = average pooling + max pooling of the batch
 through the drop-in API on HBM-resident inputs.  value = algorithmic bytes
 (4 * (|x| + |y|) per op) / device time, summed over ranks (weak scaling: every
 rank pools its own 256-signal batch; no collective on the data path).
-`per_config` adds every other BASELINE config (1-D conv, k sweep, 2-D 3x3 /
-5x5, NCHW, 65536^2 7x7 row bands) with GB/s, GFLOP/s, roofline fraction and
-the im2col + cuBLAS contrast on the same GPU.  Rank 0 prints ONE JSON line.
+
+N = 1 adds `per_config` (every other BASELINE config with ms, GB/s, roofline
+fraction and the im2col + cuBLAS contrast on the same GPU; compact, printed
+last so the driver's stdout tail keeps it; the long form goes to stderr).
+N > 1 (`--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset) adds `rowband_cfg5` (config 5 in G row bands with the
+NCCL halo, efficiency E(G) = T(1) / (G T(G)) with T(1) the whole image on one
+GPU in the same run) and `sharded` (configs 1-3 split across the ranks, no
+collective, same efficiency).  `--dry-run` exercises the multi-rank plumbing
+(launch, barriers, max-over-ranks, the real halo exchange over gloo) on CPU
+with no kernels -- a CI check, not a measurement.  Rank 0 prints ONE JSON line.
 """
 
 from __future__ import annotations
@@ -49,6 +58,14 @@ def load_traffic():
             return json.load(fh)
     except (OSError, ValueError):
         return {}
+
+
+def bench_config(world: int) -> dict:
+    """The headline workload's config -- identical in both arms."""
+    return {"workload": "cfg2 pool1d avg+max k=16 (BASELINE configs[1])",
+            "signals_per_rank": B, "length": L, "window": K,
+            "l2": "inputs (268 MB) larger than L2 (126 MB), no flush",
+            "parallelism": f"signals sharded, {world} rank(s), no collective"}
 
 
 # ----------------------------------------------------------------- clocks
@@ -152,22 +169,46 @@ def time_launches(torch, fn, reps, warmup, flush=None):
     return statistics.median(times)
 
 
+def time_sustained(torch, fn, reps=20, sustain_s=1.0, clock_index=None):
+    """Median device time per call after `sustain_s` seconds of back-to-back
+    calls (so the power-capped clock has settled), one event pair per call,
+    nvidia-smi clocks sampled over the timed calls."""
+    t_end = time.time() + sustain_s
+    n = 0
+    while time.time() < t_end or n < 3:
+        fn()
+        n += 1
+        if n % 8 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(clock_index) if clock_index is not None else None
+    if sampler:
+        sampler.start()
+    st = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(reps)]
+    for a, b in ev:
+        a.record(st)
+        fn()
+        b.record(st)
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    times = [a.elapsed_time(b) / 1e3 for a, b in ev]
+    return statistics.median(times), clocks
+
+
 # ------------------------------------------------------------ reference arm
 def run_reference(args, rank, world):
     """`--impl reference`: the reference's algorithm (oracle port, pinned to
-    the reference's outputs) on all host cores, same workload / metric."""
+    the reference's outputs) on all host cores, same workload / metric /
+    config; median over K timed steps of the full batch on a persistent pool
+    of pinned processes -- the same estimator as our arm's cpu_baseline."""
     if rank != 0:
         return
     from oracle import cpu_runner
     p = {"cfg": 2, "n": L, "k": K, "ops": ("avg", "max")}
-    cores = len(cpu_runner.host_cores())
-    units = B  # the full 256-signal batch per step
-    times = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_runner.time_units("pool", p, units, cores)
-        if i >= args.warmup:
-            times.append(r["seconds"])
-    sec = statistics.median(times)
+    r = cpu_runner.time_steps("pool", p, B, args.steps, args.warmup)
+    sec = r["seconds"]
     alg = 2 * 4 * (B * L + B * (L - K + 1))
     val = alg / sec / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s",
@@ -175,36 +216,33 @@ def run_reference(args, rank, world):
             "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic N(0,1) signals, seeded per signal",
-            "config": {"workload": "cfg2 pool1d avg+max k=16, 256 x 262144 fp32",
-                       "signals": B, "length": L, "window": K},
-            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": cores,
+            "config": bench_config(world),
+            "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": r["cores"],
                              "kind": "port", "cpu": cpu_runner.cpu_model(),
-                             "sample": f"full batch ({B} signals) per step, numpy restatement of "
-                                       "pooling.py:28-78 (avg = sum / float32(k)), one pinned "
-                                       "process per core"},
+                             "sample": f"full batch ({B} signals, avg+max k={K}) per step, "
+                                       f"median of {args.steps} steps after {args.warmup} warm-up, "
+                                       "numpy restatement of pooling.py:28-78 (avg = sum / "
+                                       "float32(k)), persistent pool of one pinned process per "
+                                       "core"},
             "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
-def cpu_baseline_main():
+def cpu_baseline_main(steps=20, warmup=2):
+    """The reference arm's estimator on the same pool: median of `steps`
+    full-batch steps (~65 ms each on 16 cores), plus the 1-core figure."""
     from oracle import cpu_runner
     p = {"cfg": 2, "n": L, "k": K, "ops": ("avg", "max")}
-    cores = len(cpu_runner.host_cores())
-    secs = []
-    t_end = time.time() + 10.0
-    while time.time() < t_end or len(secs) < 3:
-        secs.append(cpu_runner.time_units("pool", p, B, cores)["seconds"])
-        if len(secs) >= 20:
-            break
-    sec = statistics.median(secs)
+    r = cpu_runner.time_steps("pool", p, B, steps, warmup)
     alg = 2 * 4 * (B * L + B * (L - K + 1))
     one = cpu_runner.time_one_core("pool", p, 16) * (B / 16)
-    return {"value": round(alg / sec / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "port",
-            "cpu": cpu_runner.cpu_model(),
-            "sample": f"{len(secs)} x full {B}-signal batch (avg+max, k=16) on {cores} pinned "
-                      f"processes, median; oracle = numpy restatement of pooling.py:28-78",
+    return {"value": round(alg / r["seconds"] / 1e9, 3), "unit": "GB/s", "cores": r["cores"],
+            "kind": "port", "cpu": cpu_runner.cpu_model(),
+            "sample": f"{steps} x full {B}-signal batch (avg+max, k={K}) on {r['cores']} pinned "
+                      "persistent processes, median (the reference arm's estimator); oracle = "
+                      "numpy restatement of pooling.py:28-78",
             "one_core_value": round(alg / one / 1e9, 3)}
 
 
@@ -349,7 +387,11 @@ def per_config(torch, sc, hbm_peak, args, traffic):
         xb[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
     f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
           / np.float32(7)).astype(np.float32)
-    t = time_launches(torch, lambda: sc.conv2d_slide_generic(xb, f7, vm), 3, 1)
+    y5 = torch.empty((65530, 65530), device=dev)
+    from paper_2310_05218_b200 import _ops
+    t, clk5 = time_sustained(torch, lambda: _ops.conv2d_into(xb, f7, y5), reps=20,
+                             sustain_s=1.0, clock_index=torch.cuda.current_device())
+    del y5
     o = 65530
     nb = 4 * (65536 * 65536 + o * o + 49)
     fl = 2 * o * o * 49
@@ -366,6 +408,8 @@ def per_config(torch, sc, hbm_peak, args, traffic):
     tc5 = time_launches(torch, contrast5, 1, 1)
     del yc, cols
     out["cfg5_7x7_65536"] = {"ms": round(t * 1e3, 3), **roofline(nb, fl, t, hbm_peak),
+                             "timing": "median of 20 launches after 1 s of sustained load",
+                             "clocks": clk5,
                              "im2col_cublas_ms": round(tc5 * 1e3, 1),
                              "cpu": cpu_rate("conv2d", {"cfg": 5, "h": 262, "w": 65536, "k": 7,
                                                         "lo": -1.0}, 8,
@@ -375,53 +419,145 @@ def per_config(torch, sc, hbm_peak, args, traffic):
     return out
 
 
-def rowband_bench(torch, sc, rank, world, hbm_peak, reps=3):
-    """BASELINE config 5 split into `world` row bands (one per rank) with the
-    6-row NCCL halo exchange of paper_2310_05218_b200.rowband; device time,
-    max over ranks (strong scaling of one 65,536^2 image)."""
+def _max_over_ranks(torch, dev, t):
     import torch.distributed as dist
-    H = W = 65536
-    plan = sc.plan_row_bands(H, 7, world)[rank]
-    rows = plan.in_stop - plan.in_start
-    dev = torch.device("cuda", torch.cuda.current_device())
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(5000 + rank)
-    # the band plus kh - 1 spare rows: the halo is received in place and the
-    # band is one conv launch (rowband.alloc_band)
-    band = sc.alloc_band(rows, W, 7, device=dev)
-    for r0 in range(0, rows, 8192):
-        band[r0:min(rows, r0 + 8192)].uniform_(-1, 1, generator=gen)
-    f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
-          / np.float32(7)).astype(np.float32)
-    group = dist.group.WORLD if world > 1 else None
-    for _ in range(2):
-        if world > 1:
-            sc.conv2d_rowband(band, f7, group=group, halo_in_place=True)
-        else:
-            sc.conv2d_reference(band[:rows], f7)
+    tt = torch.tensor([t], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def _timed_mean(torch, fn, reps, warmup=3):
+    """Mean device time per call of `reps` back-to-back calls (CUDA events on
+    the current stream)."""
+    for _ in range(warmup):
+        fn()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(reps):
-        y = (sc.conv2d_rowband(band, f7, group=group, halo_in_place=True)[0] if world > 1
-             else sc.conv2d_reference(band[:rows], f7))
+        fn()
     b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / 1e3 / reps
+
+
+def rowband_bench(torch, sc, rank, world, hbm_peak, reps=10):
+    """BASELINE config 5 split into `world` row bands (one per rank) with the
+    6-row NCCL halo exchange of paper_2310_05218_b200.rowband (received in
+    place, one launch per band): device time per step, max over ranks, and
+    E(G) = T(1) / (G T(G)) with T(1) the whole image in one launch on rank 0
+    measured the same way in this run while the other ranks wait."""
+    import torch.distributed as dist
+    from paper_2310_05218_b200 import _ops
+    H = W = 65536
+    plan = sc.plan_row_bands(H, 7, world)[rank]
+    rows = plan.in_stop - plan.in_start
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f7 = (np.random.default_rng([0x5EED, 5, 0xFFFF]).standard_normal((7, 7), dtype=np.float32)
+          / np.float32(7)).astype(np.float32)
+    gen = torch.Generator(device=dev)
+    # ---- T(1): rank 0 alone, whole image, one launch per step
+    t1 = None
+    if rank == 0:
+        gen.manual_seed(5000)
+        x = torch.empty((H, W), device=dev)
+        for r0 in range(0, H, 8192):
+            x[r0:r0 + 8192].uniform_(-1, 1, generator=gen)
+        y = torch.empty((H - 6, W - 6), device=dev)
+        t1 = _timed_mean(torch, lambda: _ops.conv2d_into(x, f7, y), reps)
+        del x, y
+        torch.cuda.empty_cache()
+    dist.barrier()
+    # ---- T(G): every rank its band (+6 spare rows for the halo), exchange +
+    # one launch per step
+    gen.manual_seed(5000 + rank)
+    band = sc.alloc_band(rows, W, 7, device=dev)
+    for r0 in range(0, rows, 8192):
+        band[r0:min(rows, r0 + 8192)].uniform_(-1, 1, generator=gen)
+
+    def step():
+        sc.conv2d_rowband(band, f7, halo_in_place=True)
+
+    for _ in range(3):
+        step()
     torch.cuda.synchronize()
-    t = a.elapsed_time(b) / 1e3 / reps
-    if world > 1:
-        tt = torch.tensor([t], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t = float(tt.item())
-    del band, y
+    dist.barrier()
+    tg = _timed_mean(torch, step, reps, warmup=0)
+    tg = _max_over_ranks(torch, dev, tg)
+    # the exchange alone (1.5 MiB per neighbour pair), for the breakdown
+    spare = band[rows:] if rank < world - 1 else None
+
+    def xchg():
+        _, works = sc.rowband.exchange_halo(band[:rows], 6, None, recv=spare)
+        for wk in works:
+            wk.wait()
+
+    dist.barrier()
+    tx = _max_over_ranks(torch, dev, _timed_mean(torch, xchg, reps))
+    del band
     torch.cuda.empty_cache()
     o = H - 6
     nb = 4 * (H * W + o * o + 49)
     fl = 2 * o * o * 49
-    return {"ms": round(t * 1e3, 3), "ranks": world, **roofline(nb, fl, t, hbm_peak * world),
-            "halo_bytes_per_pair": 6 * W * 4, "note": "one 65536^2 image, row bands + NCCL halo"}
+    out = {"ms": round(tg * 1e3, 3), "ranks": world, **roofline(nb, fl, tg, hbm_peak * world),
+           "halo_exchange_ms": round(tx * 1e3, 4), "halo_bytes_per_pair": 6 * W * 4,
+           "note": "one 65536^2 image, row bands + NCCL halo received in place; T1 = whole "
+                   "image on rank 0 in this run; mean of 10 steps, max over ranks"}
+    if rank == 0:
+        out["t1_ms"] = round(t1 * 1e3, 3)
+        out["efficiency"] = round(t1 / (world * tg), 4)
+    return out
+
+
+def sharded_bench(torch, sc, rank, world, hbm_peak, reps=10):
+    """Configs 1-3 with the BASELINE batch split across the ranks (no
+    collective): T(G) max over ranks vs T(1) = the whole batch on rank 0 in
+    this run; E(G) = T(1) / (G T(G))."""
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device())
+    gen = torch.Generator(device=dev)
+    vm = sc.VectorModel(16)
+    f1 = np.random.default_rng([0x5EED, 1, 0xFFFF]).standard_normal((1, 7), dtype=np.float32)
+    f3 = {k: (np.random.default_rng([0x5EED, 3, k]).standard_normal((k, k), dtype=np.float32)
+              / np.float32(k)).astype(np.float32) for k in (3, 5)}
+    cases = {
+        "cfg1_conv1d_k7": (64, lambda n: torch.rand((n, 1 << 20), generator=gen, device=dev) * 2 - 1,
+                           lambda x: sc.conv2d_slide_generic(x, f1, vm),
+                           lambda n: 4 * (n * (1 << 20) + n * ((1 << 20) - 6) + 7)),
+        "cfg2_pool_avgmax_k16": (256, lambda n: torch.randn((n, L), generator=gen, device=dev),
+                                 lambda x: (sc.sliding_window_mean(x, K), sc.sliding_window_max(x, K)),
+                                 lambda n: 2 * 4 * (n * L + n * (L - K + 1))),
+        "cfg3_conv2d_3x3": (32, lambda n: torch.rand((n, 4096, 4096), generator=gen, device=dev),
+                            lambda x: sc.conv2d_custom3(x, f3[3], vm),
+                            lambda n: 4 * (n * 4096 * 4096 + n * 4094 * 4094 + 9)),
+        "cfg3_conv2d_5x5": (32, lambda n: torch.rand((n, 4096, 4096), generator=gen, device=dev),
+                            lambda x: sc.conv2d_custom5(x, f3[5], vm),
+                            lambda n: 4 * (n * 4096 * 4096 + n * 4092 * 4092 + 25)),
+    }
+    out = {}
+    for name, (units, make, run, nbytes) in cases.items():
+        gen.manual_seed(sum(map(ord, name)) + rank)
+        t1 = None
+        if rank == 0:
+            x = make(units)
+            t1 = _timed_mean(torch, lambda: run(x), reps)
+            del x
+        dist.barrier()
+        per = units // world + (1 if rank < units % world else 0)
+        x = make(per)
+        for _ in range(3):
+            run(x)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tg = _max_over_ranks(torch, dev, _timed_mean(torch, lambda: run(x), reps, warmup=0))
+        del x
+        torch.cuda.empty_cache()
+        if rank == 0:
+            out[name] = {"units": units, "t1_ms": round(t1 * 1e3, 4), "tg_ms": round(tg * 1e3, 4),
+                         "gbs_total": round(nbytes(units) / tg / 1e9, 1),
+                         "efficiency": round(t1 / (world * tg), 4)}
+    return out
 
 
 def rowband_projection(torch, sc, rounds=3):
@@ -595,9 +731,10 @@ def run_ours(args, rank, world, local_rank):
         e2e_sec = float(tt.item())
     e2e_val = world * e2e_steps * 2 * alg_bytes_op / e2e_sec / 1e9
 
-    rb = None
+    rb = sh = None
     if world > 1 and not args.no_extras:
         rb = rowband_bench(torch, sc, rank, world, hbm_peak)
+        sh = sharded_bench(torch, sc, rank, world, hbm_peak)
     if rank != 0:
         return
     # the step is two launches of the same kernel template (AVG and MAX, equal
@@ -614,10 +751,7 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: torch.randn N(0,1) signals on device, seed 0x5EED+rank",
-        "config": {"workload": "cfg2 pool1d avg+max k=16 (BASELINE configs[1])",
-                   "signals_per_rank": B, "length": L, "window": K,
-                   "l2": "inputs (268 MB) larger than L2 (126 MB), no flush",
-                   "parallelism": f"signals sharded, {world} rank(s), no collective"},
+        "config": bench_config(world),
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 1),
                      "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                      "traffic": tr, "alg_bytes_per_launch": alg_bytes_op,
@@ -637,13 +771,101 @@ def run_ours(args, rank, world, local_rank):
     }
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_main()
-    if world == 1 and not args.no_extras:
-        line["per_config"] = per_config(torch, sc, hbm_peak, args, traffic)
     if rb is not None:
         line["rowband_cfg5"] = rb
+        line["sharded"] = sh
     if world == 1 and not args.no_extras:
-        line["rowband_cfg5_projection"] = rowband_projection(torch, sc)
+        detail = per_config(torch, sc, hbm_peak, args, traffic)
+        detail["rowband_cfg5_projection"] = rowband_projection(torch, sc)
+        # long form to stderr; the compact table goes LAST on the JSON line so
+        # the driver's stdout tail keeps it
+        print(json.dumps({"per_config_detail": detail}), file=sys.stderr, flush=True)
+        line["per_config"] = compact_per_config(detail)
     print(json.dumps(line), flush=True)
+
+
+def compact_per_config(detail: dict) -> dict:
+    """ms / GB/s / fraction of the bounding roofline / contrast per config."""
+    out = {}
+    for name, d in detail.items():
+        if name.startswith("cfg2_pool"):
+            out[name] = {op: [d[op]["ms"], d[op]["gbs"], d[op]["frac_of_bound"]]
+                         for op in ("avg", "max", "sum")}
+            out[name]["torch_ms"] = [d["torch_pool_ms"]["avg"], d["torch_pool_ms"]["max"]]
+        elif name == "rowband_cfg5_projection":
+            out[name] = {"whole_ms": d["whole_ms"],
+                         **{g: d[g]["proj_eff"] for g in ("G2", "G4", "G8")}}
+        else:
+            c = {"ms": d["ms"], "gbs": d["gbs"], "frac": d["frac_of_bound"], "bound": d["bound"],
+                 "im2col_ms": d.get("im2col_cublas_ms")}
+            if "tensor_roofline" in d:
+                c["tc_frac"] = d["tensor_roofline"]["frac"]
+            if "clocks" in d and d["clocks"]:
+                c["sm_mhz"] = d["clocks"].get("sm_mhz")
+            out[name] = c
+    out["key"] = "cfg2: op -> [ms, GB/s, frac]; others frac of max(t_hbm, t_fp32) roofline"
+    return out
+
+
+def relaunch(args) -> int:
+    """`--gpus N` without a torchrun environment: start N ranks on this node
+    (one per GPU) with torch.distributed.run, NCCL_DEBUG=INFO so the
+    communicator lines show nranks = N."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    if not args.dry_run:
+        env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """CPU-only plumbing check (CI): gloo group, barriers, the real halo
+    exchange of rowband.py on a small band, max-over-ranks, the same JSON
+    keys.  No kernel runs, so the numbers are not measurements."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2310_05218_b200 as sc
+    dist.init_process_group("gloo")
+    try:
+        h, w = 64 * world, 256
+        plan = sc.plan_row_bands(h, 7, world)[rank]
+        rows = plan.in_stop - plan.in_start
+        x = torch.arange(h * w, dtype=torch.float32).reshape(h, w)
+        band = sc.alloc_band(rows, w, 7)
+        band[:rows] = x[plan.in_start:plan.in_stop]
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _, works = sc.rowband.exchange_halo(band[:rows], 6, None,
+                                                recv=band[rows:] if rank < world - 1 else None)
+            for wk in works:
+                wk.wait()
+        t = (time.perf_counter() - t0) / args.steps
+        tt = torch.tensor([t], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        halo_ok = torch.tensor([1 if rank == world - 1 else
+                                int(torch.equal(band[rows:], x[plan.in_stop:plan.in_stop + 6]))])
+        dist.all_reduce(halo_ok, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(json.dumps({
+                "metric": METRIC, "value": 0.0, "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 0.0,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "dry run: no kernels", "dry_run": True,
+                "config": bench_config(world),
+                "rowband_cfg5": {"ranks": world, "halo_exchange_ms": round(float(tt) * 1e3, 4),
+                                 "halo_ok": bool(halo_ok.item()), "efficiency": None}}),
+                  flush=True)
+    finally:
+        dist.destroy_process_group()
 
 
 def main():
@@ -656,11 +878,18 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     ap.add_argument("--no-sustain", action="store_true",
                     help="skip the 1 s pre-load phase (for ncu launch lists)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing on CPU (gloo), no kernels (CI)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
