@@ -119,6 +119,29 @@ int sc_gemm_f32(const float* a, const float* b, float* c, int64_t m, int64_t n, 
 int sc_conv2d_im2col_f32(const float* x, int64_t h, int64_t w, const float* f_dev, int64_t kh,
                          int64_t kw, float* cols, int64_t chunk_rows, float* y, void* stream);
 
+/* ---- row bands across GPUs (new, BASELINE config 5) ----
+ * One host thread drives G GPUs; the context owns one NCCL communicator per
+ * device (ncclCommInitAll; NCCL is dlopen'ed) plus a comm stream and events.
+ * Band g (device devs[g]) is a DEVICE buffer of rows[g] + kh - 1 rows of w
+ * floats: its first rows[g] rows hold input rows of band g, the kh - 1 spare
+ * rows receive the first kh - 1 rows of band g + 1 (the halo, NCCL send/recv
+ * over NVLink).  ys[g] (DEVICE, on devs[g]) receives rows[g] output rows of
+ * w - kw + 1 (the last band: rows[g] - kh + 1).  Concatenating ys over g gives
+ * the valid conv of the whole image -- bit-identical, since output row r reads
+ * input rows r .. r + kh - 1 only (reference.py:15-23, _accumulate_taps).
+ * Per device the interior rows are convolved on streams[g] (NULL = legacy
+ * default stream) while the halo is in flight; the kh - 1 boundary rows run
+ * after it lands.  timeout_ms > 0: wait for completion, polling
+ * ncclCommGetAsyncError; on an NCCL error or timeout return SC_ERR_CUDA and
+ * mark the context aborted (destroy then aborts the communicators).
+ * timeout_ms <= 0: enqueue only. */
+typedef struct sc_rowband sc_rowband;
+int sc_rowband_create(int ndev, const int* devs, sc_rowband** ctx);
+int sc_rowband_destroy(sc_rowband* ctx);
+int sc_rowband_conv2d_f32(sc_rowband* ctx, float* const* bands, const int64_t* rows, int64_t w,
+                          const float* f, int64_t kh, int64_t kw, int mode, float* const* ys,
+                          void* const* streams, int timeout_ms);
+
 /* ---- host-buffer entry points (chunked H2D / compute / D2H pipeline) -------
  * Same semantics as the device entry points; x and y are HOST pointers. */
 int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t length, int64_t k,

@@ -11,11 +11,11 @@ from .kernels import (KernelVariant, analytic_counters, applicable_variants, com
                       conv1d_slide, conv2d_custom3, conv2d_custom5, conv2d_slide_compound,
                       conv2d_slide_generic, counted_offsets, run_variant, select_kernel,
                       variant_applicable)
-from .lanes import VectorModel
+from .lanes import VectorModel, slide
 from .nchw import conv2d_nchw
 from .pooling import sliding_window_max, sliding_window_mean, sliding_window_sum
 from .reference import conv1d_reference, conv2d_reference, oracle_conv2d, relative_error
-from .rowband import RowBandPlan, alloc_band, conv2d_rowband, plan_row_bands
+from .rowband import RowBandGroup, RowBandPlan, alloc_band, conv2d_rowband, plan_row_bands
 from .verify import PropertyResult, VerifyReport, verify_suite
 from .tensor import (ConvShape, CostCounters, FilterSizeError, FilterWidthError, ShapeError,
                      mac_count)
@@ -25,7 +25,7 @@ __version__ = "0.1.0"
 __all__ = [
     # reference hot-path subset (slideconv/__init__.py:39-49)
     "ConvShape", "CostCounters", "FilterSizeError", "FilterWidthError", "KernelVariant",
-    "ShapeError", "VectorModel", "applicable_variants", "bloat_ratio", "conv1d_reference",
+    "ShapeError", "VectorModel", "slide", "applicable_variants", "bloat_ratio", "conv1d_reference",
     "conv1d_slide", "conv2d_custom3", "conv2d_custom5", "conv2d_im2col", "conv2d_reference",
     "conv2d_slide_compound", "conv2d_slide_generic", "gemm", "im2col_2d", "mac_count",
     "oracle_conv2d", "run_variant", "select_kernel", "sliding_window_max", "sliding_window_sum",
@@ -34,5 +34,6 @@ __all__ = [
     "relative_error", "verify_suite", "VerifyReport", "PropertyResult",
     # B200 extensions (BASELINE configs)
     "sliding_window_mean", "conv2d_nchw", "conv2d_rowband", "plan_row_bands", "RowBandPlan", "alloc_band",
+    "RowBandGroup",
     "pinned_empty", "set_default_mode",
 ]

@@ -43,6 +43,11 @@ SIGNATURES = {
     "sc_im2col_f32": (_int, [_vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "sc_gemm_f32": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "sc_conv2d_im2col_f32": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _vp]),
+    "sc_rowband_create": (_int, [_int, ctypes.POINTER(_int), ctypes.POINTER(_vp)]),
+    "sc_rowband_destroy": (_int, [_vp]),
+    "sc_rowband_conv2d_f32": (_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64), _i64, _vp,
+                                     _i64, _i64, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                     _int]),
     "sc_pool1d_f32_host": (_int, [_int, _vp, _i64, _i64, _i64, _int, _vp, _int]),
     "sc_conv2d_f32_host": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _int]),
 }

@@ -32,13 +32,17 @@ def conv2d(x, f, exact=None):
     return _unbatch(y, lead) if lead else y[0]
 
 
-def conv2d_reference(x, f, *, exact=None):
-    """reference.py:26-30: 2-D valid convolution, float32, tap order (j, i)."""
+def conv2d_reference(x, f, *, exact=True):
+    """reference.py:26-30: 2-D valid convolution, float32, tap order (j, i).
+    Upstream documents this entry point as the bit-for-bit multiply-then-add
+    baseline, so it defaults to exact mode (bit-identical to the reference);
+    exact=False / None selects the FFMA kernels (module default)."""
     return conv2d(x, f, exact)
 
 
-def conv1d_reference(x, f, *, exact=None):
-    """reference.py:33-39: height-1 input and filter."""
+def conv1d_reference(x, f, *, exact=True):
+    """reference.py:33-39: height-1 input and filter (exact by default, as
+    conv2d_reference)."""
     x = as_tensor2d(x)
     f = as_filter2d(f)
     if x.shape[0] != 1 or f.shape[0] != 1:

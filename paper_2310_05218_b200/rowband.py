@@ -222,3 +222,84 @@ def conv2d_rowband(x_local, f, *, group=None, exact=None, conv=None, halo_in_pla
             parts.append(conv(edge, f))
         y = torch.cat(parts, dim=0) if len(parts) > 1 else parts[0]
     return y, CostCounters(macs=mac_count(s))
+
+
+class RowBandGroup:
+    """Row bands on several GPUs of this process, one host thread, through
+    the C ABI (include/slideconv_b200.h, sc_rowband_*): the context owns one
+    NCCL communicator per device; each call exchanges the kh-1 halo rows with
+    grouped ncclSend/ncclRecv on a comm stream while the interior rows are
+    convolved, then runs the boundary rows (no copy, no concatenation).
+
+        grp = RowBandGroup([0, 1, 2, 3])
+        bufs = [alloc_band(rows, W, kh, device=f"cuda:{d}") ...]   # fill [:rows]
+        ys = grp.conv2d(bufs, f)          # list of per-band outputs
+    """
+
+    def __init__(self, devices):
+        import ctypes
+
+        from . import _lib
+        self._lib = _lib.load()
+        self.devices = [int(d) for d in devices]
+        arr = (ctypes.c_int * len(self.devices))(*self.devices)
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.sc_rowband_create(len(self.devices), arr, ctypes.byref(h)))
+        self._h = h
+
+    def conv2d(self, bands, f, *, exact=None, timeout_ms: int = 120_000):
+        """bands[g]: contiguous float32 CUDA tensor (rows_g + kh - 1, W) on
+        devices[g], rows [:rows_g] filled; returns the per-band outputs
+        (rows_g, W - kw + 1), the last band rows_g - kh + 1."""
+        import ctypes
+
+        import torch
+
+        from . import _lib
+        from ._device import mode_flag
+        if self._h is None:
+            raise RuntimeError("RowBandGroup is closed")
+        f = as_filter2d(f)
+        kh, kw = f.shape
+        G = len(self.devices)
+        if len(bands) != G:
+            raise ValueError(f"expected {G} bands, got {len(bands)}")
+        w = int(bands[0].shape[1])
+        rows, ys = [], []
+        for g, b in enumerate(bands):
+            if (not b.is_cuda or b.device.index != self.devices[g] or b.dtype != torch.float32
+                    or not b.is_contiguous() or int(b.shape[1]) != w):
+                raise ValueError(f"band {g}: contiguous float32 CUDA tensor on cuda:"
+                                 f"{self.devices[g]} with {w} columns required")
+            r = int(b.shape[0]) - (kh - 1)
+            rows.append(r)
+            n_out = r if g < G - 1 else r - kh + 1
+            ys.append(torch.empty((max(n_out, 0), w - kw + 1), dtype=torch.float32,
+                                  device=b.device))
+        vp = ctypes.c_void_p
+        c_bands = (vp * G)(*[b.data_ptr() for b in bands])
+        c_rows = (ctypes.c_int64 * G)(*rows)
+        c_ys = (vp * G)(*[y.data_ptr() for y in ys])
+        c_streams = (vp * G)(*[torch.cuda.current_stream(b.device).cuda_stream for b in bands])
+        fc = np.ascontiguousarray(f, dtype=np.float32)
+        _lib.check(self._lib.sc_rowband_conv2d_f32(self._h, c_bands, c_rows, w, fc.ctypes.data,
+                                                   kh, kw, mode_flag(exact), c_ys, c_streams,
+                                                   int(timeout_ms)))
+        return ys
+
+    def close(self):
+        if self._h is not None:
+            self._lib.sc_rowband_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):  # pragma: no cover -- best effort
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

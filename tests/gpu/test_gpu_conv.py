@@ -30,7 +30,7 @@ def test_shapes_exact_and_fast(kh, kw, h, w):
     xd = torch.from_numpy(x).cuda()
     got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
     assert np.array_equal(got, want)
-    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    fast = sc.conv2d_reference(xd, f, exact=False).cpu().numpy()
     ref64 = np.stack([O.oracle_conv2d(img, f) for img in x])
     assert O.normwise_error(fast, ref64) <= O.north_star_tol(max(kh, kw))
     assert sc.relative_error(fast, ref64) <= 1e-5 * max(1, kh * kw / 64)
@@ -48,7 +48,7 @@ def test_runtime_k_register_blocked_kernel(kh, kw, n, h, w):
     xd = torch.from_numpy(x).cuda()
     got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
     assert np.array_equal(got, O.conv2d_batched(x, f))
-    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    fast = sc.conv2d_reference(xd, f, exact=False).cpu().numpy()
     ref64 = np.stack([O.oracle_conv2d(img, f) for img in x])
     assert O.normwise_error(fast, ref64) <= O.north_star_tol(max(kh, kw))
 
@@ -66,7 +66,7 @@ def test_four_column_kernels_on_large_grids(k, n, h, w):
     xd = torch.from_numpy(x).cuda()
     got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
     assert np.array_equal(got, O.conv2d_batched(x, f))
-    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    fast = sc.conv2d_reference(xd, f, exact=False).cpu().numpy()
     ref64 = np.stack([O.oracle_conv2d(img, f) for img in x[:2]])
     assert O.normwise_error(fast[:2], ref64) <= O.north_star_tol(k)
 
@@ -79,7 +79,7 @@ def test_rotating_4col_kernels(k):
     xd = torch.from_numpy(x).cuda()
     got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
     assert np.array_equal(got, O.conv2d_batched(x, f))
-    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    fast = sc.conv2d_reference(xd, f, exact=False).cpu().numpy()
     ref64 = np.stack([O.oracle_conv2d(img, f) for img in x[:3]])
     assert O.normwise_error(fast[:3], ref64) <= O.north_star_tol(k)
 
@@ -138,7 +138,7 @@ def test_config5_band_and_properties():
     xd = torch.from_numpy(x).cuda()
     got = sc.conv2d_reference(xd, f, exact=True).cpu().numpy()
     assert np.array_equal(got, want)
-    fast = sc.conv2d_reference(xd, f).cpu().numpy()
+    fast = sc.conv2d_reference(xd, f, exact=False).cpu().numpy()
     assert O.normwise_error(fast, want) <= O.north_star_tol(7)
     # banded on the GPU == whole on the GPU (exact), 4 virtual bands
     plans = sc.plan_row_bands(1030, 7, 4)

@@ -83,7 +83,7 @@ def _run(world, backend, h, w, kh, kw, tmp_path):
              join=True)
     x, f = _image(h, w, kh, kw)
     want = O.conv2d(x, f)
-    whole_fast = sc.conv2d_reference(torch.from_numpy(x).cuda(), f).cpu().numpy()
+    whole_fast = sc.conv2d_reference(torch.from_numpy(x).cuda(), f, exact=False).cpu().numpy()
     for exact in (1, 0):
         for in_place in (0, 1):
             parts = [np.load(tmp_path / f"r{r}_e{exact}_p{in_place}.npy") for r in range(world)]

@@ -62,3 +62,17 @@ def test_validation_happens_before_any_device_work(lib):
     assert lib.sc_im2col_f32(None, 3, 3, 4, 1, 0, 0, None, None) == _lib.SC_ERR_SHAPE
     # empty batches are a no-op
     assert lib.sc_pool1d_f32(0, None, 0, 8, 3, 0, None, None) == 0
+
+
+def test_rowband_abi_validates_before_touching_devices(lib):
+    import ctypes
+
+    from paper_2310_05218_b200 import _lib
+    h = ctypes.c_void_p()
+    devs = (ctypes.c_int * 1)(0)
+    assert lib.sc_rowband_create(0, devs, ctypes.byref(h)) == _lib.SC_ERR_ARG
+    assert h.value is None
+    assert lib.sc_rowband_create(1, devs, None) == _lib.SC_ERR_ARG
+    assert lib.sc_rowband_conv2d_f32(None, None, None, 8, None, 3, 3, 0, None, None, 0) == \
+        _lib.SC_ERR_ARG
+    assert lib.sc_rowband_destroy(None) == 0
