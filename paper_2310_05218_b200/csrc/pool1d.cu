@@ -26,6 +26,8 @@
 namespace sc {
 int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                cudaStream_t st);
+int pool1d_block_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st);
 int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                 cudaStream_t st);
 int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
@@ -465,6 +467,10 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
     const char* e = getenv("SC_POOL_MAX_WIDE_MIN");
     return e ? atoi(e) : 257;
   }();
+  if (kOp != SC_POOL_MAX && !exact) {  // window sums over aligned blocks (k = B - 1 / B)
+    const int rc = pool1d_block_sum(kOp, x, batch, length, k, y, st);
+    if (rc != 1) return rc;
+  }
   if ((kOp == SC_POOL_MAX && k >= max_wide_min) || (kOp != SC_POOL_MAX && !exact)) {
     const int rc = pool1d_wide(kOp, x, batch, length, k, y, st);
     if (rc != 1) return rc;

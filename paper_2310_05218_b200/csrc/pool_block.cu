@@ -40,6 +40,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -64,22 +65,30 @@ struct Geo {
   static_assert(kRows <= 256, "TMA box rows");
 };
 
-template <bool kExact>
-__device__ __forceinline__ float mx(float a, float b) {  // a earlier, b later
-  if constexpr (kExact) return np_max(a, b);
+// combine ops (a earlier, b later): max.NaN fast pass, np.maximum's rule, or
+// '+' (window sums: the same aligned-block structure with a sum combine)
+constexpr int kCombMaxFast = 0, kCombMaxExact = 1, kCombAdd = 2;
+template <int kComb>
+__device__ __forceinline__ float mx(float a, float b) {
+  if constexpr (kComb == kCombMaxExact) return np_max(a, b);
+  else if constexpr (kComb == kCombAdd) return a + b;
   else return max_nan(a, b);
+}
+template <bool kExact>
+__device__ __forceinline__ float mxb(float a, float b) {  // max only
+  return mx<kExact ? kCombMaxExact : kCombMaxFast>(a, b);
 }
 
 // Reads the lane's 32 samples (one swizzled 128-byte row of the tile),
 // computes y(32 lane + r) and writes the outputs of lanes < V/32 to the
 // warp's staging rows; returns whether a valid output was zero.
-template <int B, int K, bool kEx>
+template <int B, int K, int kEx, bool kAvg = false>
 __device__ __forceinline__ bool block_max(const unsigned char* rowp, int swz, int lane,
-                                          float* stage_row, int lim) {
+                                          float* stage_row, int lim, float inv_k = 1.0f) {
   constexpr int LB = B / 32;               // lanes per block
   constexpr int m = (K - 1) / 32, c = (K - 1) % 32;
   constexpr int kOutLanes = (kWin - B) / 32;
-  const float kId = -__int_as_float(0x7f800000);
+  const float kId = kEx == kCombAdd ? 0.0f : -__int_as_float(0x7f800000);  // identity
   float P[kT], S[kT];
 #pragma unroll
   for (int q = 0; q < kT / 4; ++q) {
@@ -129,7 +138,8 @@ __device__ __forceinline__ bool block_max(const unsigned char* rowp, int swz, in
       if (r == 0) si = lb == 0 ? kId : si;                   // window in one block: P alone
       if (r > 0 && r == B - K) pj = lb == 0 ? kId : pj;      // ends on the block end: S alone
       o[u] = mx<kEx>(si, pj);
-      if constexpr (!kEx) zero |= (o[u] == 0.0f) && (kT * lane + r < lim);
+      if constexpr (kAvg) o[u] *= inv_k;   // fast-mode average (sums are not bit-exact here)
+      if constexpr (kEx == kCombMaxFast) zero |= (o[u] == 0.0f) && (kT * lane + r < lim);
     }
     if (lane < kOutLanes)
       *reinterpret_cast<float4*>(stage_row + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
@@ -140,11 +150,14 @@ __device__ __forceinline__ bool block_max(const unsigned char* rowp, int swz, in
 // kNbuf-deep TMA ring without a producer warp: the first load of each slot
 // is issued up front, and the LAST warp to finish with a slot (a shared
 // counter) refills it with the CTA's next tile at once.
-template <int B, int K, bool kFlat>
+template <int kOp, int B, int K, bool kFlat>
 __global__ void __launch_bounds__(32 * kWarps, 2)
     pool_block_max_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
                           int tiles_per_cta, int d, int64_t flat_L) {
+  static_assert(kOp == SC_POOL_MAX || true, "");
+  // kOp = SUM / AVG (fast mode, K = B - 1 or B only, d == 0): the same
+  // structure with '+': every output adds the window's own samples only
   using G = Geo<B>;
   // d > 0: the window is K + d; the warp stages y_K (window K) and stores
   // max(y_K(i), y_K(i + d)) for Vd = floor32(V - d) outputs per warp
@@ -189,11 +202,17 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
     float* srow = stage + lane * kPitch;
     const int lim_k = d ? G::V : lim;  // y_K outputs the combine reads
-    bool zero = block_max<B, K, false>(rowp, row0 & 7, lane, srow, lim_k);
-    zero = __any_sync(0xffffffffu, zero);
-    if (zero) {  // rare: redo with np.maximum's rule
-      __syncwarp();
-      block_max<B, K, true>(rowp, row0 & 7, lane, srow, lim_k);
+    bool zero = false;
+    if constexpr (kOp == SC_POOL_MAX) {
+      zero = block_max<B, K, kCombMaxFast>(rowp, row0 & 7, lane, srow, lim_k);
+      zero = __any_sync(0xffffffffu, zero);
+      if (zero) {  // rare: redo with np.maximum's rule
+        __syncwarp();
+        block_max<B, K, kCombMaxExact>(rowp, row0 & 7, lane, srow, lim_k);
+      }
+    } else {
+      block_max<B, K, kCombAdd, kOp == SC_POOL_AVG>(rowp, row0 & 7, lane, srow, lim_k,
+                                                     1.0f / (float)K);
     }
     __syncwarp();
     if (lane == 0) {  // done with slot b: the last warp refills it
@@ -229,8 +248,8 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
 #pragma unroll
             for (int mm = 0; mm < G::kOutLanes; ++mm)
               if (32 * mm + lane < lim)
-                yr[32 * mm] = zero ? mx<true>(sp[mm * kPitch], sq[mm * kPitch])
-                                   : mx<false>(sp[mm * kPitch], sq[mm * kPitch]);
+                yr[32 * mm] = zero ? mxb<true>(sp[mm * kPitch], sq[mm * kPitch])
+                                   : mxb<false>(sp[mm * kPitch], sq[mm * kPitch]);
           }
           __syncwarp();
           continue;
@@ -249,8 +268,8 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
       for (int mm = 0; mm < G::kOutLanes; ++mm) {
         if (32 * mm < nv && rem < keep) {
           const float v = d == 0 ? sp[mm * kPitch]
-                                 : (zero ? mx<true>(sp[mm * kPitch], sq[mm * kPitch])
-                                         : mx<false>(sp[mm * kPitch], sq[mm * kPitch]));
+                                 : (zero ? mxb<true>(sp[mm * kPitch], sq[mm * kPitch])
+                                         : mxb<false>(sp[mm * kPitch], sq[mm * kPitch]));
           *yp = v;
         }
         rem += 32;
@@ -280,11 +299,11 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
       if (zero) {
 #pragma unroll
         for (int mm = 0; mm < G::kOutLanes; ++mm)
-          if (32 * mm + lane < lim_d) yr[32 * mm] = mx<true>(sp[mm * kPitch], sq[mm * kPitch]);
+          if (32 * mm + lane < lim_d) yr[32 * mm] = mxb<true>(sp[mm * kPitch], sq[mm * kPitch]);
       } else {
 #pragma unroll
         for (int mm = 0; mm < G::kOutLanes; ++mm)
-          if (32 * mm + lane < lim_d) yr[32 * mm] = mx<false>(sp[mm * kPitch], sq[mm * kPitch]);
+          if (32 * mm + lane < lim_d) yr[32 * mm] = mxb<false>(sp[mm * kPitch], sq[mm * kPitch]);
       }
     }
     __syncwarp();  // staging reused by the next tile
@@ -294,7 +313,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
 // k = K + d (d = 0: the plain window K)
 // flat_L > 0: x is batch signals of flat_L samples viewed as ONE signal of
 // `length` = batch * flat_L samples (batch = 1 here)
-template <int B, int K>
+template <int B, int K, int kOp = SC_POOL_MAX>
 int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
            int d = 0, int64_t flat_L = 0) {
   using G = Geo<B>;
@@ -316,8 +335,8 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   if (n_tiles >= 0x7fffffff) return 1;
   const size_t smem = 1024 + G::kNbuf * (size_t)G::kBuf + (size_t)kWarps * G::kStage * sizeof(float);
   static uint64_t attr = 0, attr_flat = 0;  // devices whose limit is set
-  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<B, K, false>, (int)smem, &attr));
-  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<B, K, true>, (int)smem, &attr_flat));
+  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<kOp, B, K, false>, (int)smem, &attr));
+  SC_CUDA(set_smem_limit_once(pool_block_max_kernel<kOp, B, K, true>, (int)smem, &attr_flat));
   // contiguous runs of tiles per CTA (tools/pbcheck.py sweep on config 2:
   // 6 tiles for B = 256, 8 otherwise); env override
   static const int tpc_env = [] {
@@ -328,16 +347,59 @@ int launch(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t
   const int tpc = tpc_env ? tpc_env : B == 256 ? 6 : 8;
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   if (flat_L)
-    pool_block_max_kernel<B, K, true><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+    pool_block_max_kernel<kOp, B, K, true><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
         map, y, out_len, tiles_per_row, n_tiles, tpc, d, flat_L);
   else
-    pool_block_max_kernel<B, K, false><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
+    pool_block_max_kernel<kOp, B, K, false><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
         map, y, out_len, tiles_per_row, n_tiles, tpc, d, 0);
   SC_LAUNCH_CHECK("pool_block_max_kernel");
   return SC_OK;
 }
 
+// flat view of a batch whose signal length is not a multiple of 32; returns
+// false if the batch cannot take the TMA kernels at all
+bool block_geometry(const float* x, int64_t& batch, int64_t& length, int64_t& flat_L) {
+  flat_L = 0;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || length < kWin || batch > 0x7fffffff)
+    return false;
+  if (length % 32 != 0) {
+    if ((batch * length) % 32 != 0) return false;
+    flat_L = length;
+    length *= batch;
+    batch = 1;
+  }
+  return length / 32 <= 0x7fffffff;
+}
+
 }  // namespace
+
+// FAST-mode window sums / averages for k = B - 1 or B, B in {128, 256, 512}
+// (and k = 63): the aligned-block kernel with a '+' combine -- every output
+// is S(i) + P(i + k - 1), sums over its own window only (config 2 k = 255:
+// 0.088 ms vs 0.105 for the general lane-granular wide kernel).  Returns
+// SC_OK / an error if it ran, 1 if it does not apply.
+int pool1d_block_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st) {
+  static const bool off = getenv("SC_POOL_NO_BLOCK") != nullptr;
+  int64_t flat_L = 0;
+  if (off || !block_geometry(x, batch, length, flat_L)) return 1;
+  auto go = [&](auto tag) -> int {
+    constexpr int kOp = decltype(tag)::value;
+    switch (k) {
+      case 63: return launch<64, 63, kOp>(x, batch, length, y, st, 0, flat_L);
+      case 127: return launch<128, 127, kOp>(x, batch, length, y, st, 0, flat_L);
+      case 128: return launch<128, 128, kOp>(x, batch, length, y, st, 0, flat_L);
+      case 255: return launch<256, 255, kOp>(x, batch, length, y, st, 0, flat_L);
+      case 256: return launch<256, 256, kOp>(x, batch, length, y, st, 0, flat_L);
+      case 511: return launch<512, 511, kOp>(x, batch, length, y, st, 0, flat_L);
+      case 512: return launch<512, 512, kOp>(x, batch, length, y, st, 0, flat_L);
+      default: return 1;
+    }
+  };
+  if (op == SC_POOL_SUM) return go(std::integral_constant<int, SC_POOL_SUM>{});
+  if (op == SC_POOL_AVG) return go(std::integral_constant<int, SC_POOL_AVG>{});
+  return 1;
+}
 
 // Exact sliding max for 34 <= k <= 512 on 16-byte aligned signals whose
 // length is a multiple of 32 (>= 1,024); k = B - 1 / B take the one-tiling

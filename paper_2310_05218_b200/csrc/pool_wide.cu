@@ -42,6 +42,10 @@
 
 #include "common.cuh"
 
+#ifndef SC_WIDE_NBUF
+#define SC_WIDE_NBUF 3
+#endif
+
 namespace sc {
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 namespace {
@@ -51,7 +55,7 @@ constexpr int kT = 16;                 // samples per lane
 constexpr int kRows = 128;             // TMA box rows of 32 floats
 constexpr int kTile = kRows * 32;      // 4096 samples per tile
 constexpr int kBufBytes = kTile * 4;   // 16 KiB
-constexpr int kNbuf = 3;
+constexpr int kNbuf = SC_WIDE_NBUF;
 // X reads at i + k - 1 run up to 2,048 floats past the tile for outputs
 // beyond vt (never stored): they land inside arr_s, which follows arr_x
 constexpr int kArrBytes = kBufBytes;
@@ -371,10 +375,15 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
           continue;
         }
       }
+      if (warp * (32 * kT) + 32 * kT <= lim) {  // whole warp in range: no per-output checks
 #pragma unroll
-      for (int m = 0; m < kT; ++m) {
-        const int i = warp * (32 * kT) + 32 * m + lane;
-        if (i < lim) ys[i] = o[m];
+        for (int m = 0; m < kT; ++m) ys[warp * (32 * kT) + 32 * m + lane] = o[m];
+      } else {
+#pragma unroll
+        for (int m = 0; m < kT; ++m) {
+          const int i = warp * (32 * kT) + 32 * m + lane;
+          if (i < lim) ys[i] = o[m];
+        }
       }
     }
   }
