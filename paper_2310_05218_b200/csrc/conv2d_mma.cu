@@ -1,0 +1,635 @@
+// Single-channel 2-D convolution on the 5th-generation tensor cores (fast
+// mode): the slide-MMA formulation of _accumulate_taps (reference.py:15-23)
+// for filters with kw <= 9 and kh <= 15 -- BASELINE config 5 (7x7 on a
+// 65,536^2 image) and the mid-size square filters of the paper's sweep.
+//
+// Why: the FFMA kernels (conv2d.cu) need kh*kw FMAs per output; for 7x7 that
+// is 49 FMA-pipe cycles per 128 outputs, which under the board's power cap
+// (~1.65 GHz sustained) is slower than streaming the image (config 5: 7.9 ms
+// against a 5.25 ms HBM floor).  As an MMA, with
+//   M = 128 "lanes" m, each the 8 output columns c0 + 8m + s (s = 0..7),
+//   K = 16 consecutive input samples x[rho][c0 + 8m + k] (k = 0..15),
+//   N = (output row r, shift s) for the 8 (= kh + 1, even) output rows an
+//       input row rho can touch,
+// one input row contributes D[m][(r, s)] += sum_k x[rho][c0+8m+k] * f[rho-r][k-s]
+// -- the whole 7x7 tap set of 1,024 columns x 8 rows in ONE M128 N64 K16
+// MMA.  The B operand (the taps, placed by shift and filter row) is a
+// constant of the filter; the A operand is the input row itself: a plain
+// bf16 row read through a no-swizzle K-major descriptor with LBO = 16 B and
+// SBO = 128 B makes A[m][k] = x[8m + k] (core matrices overlap by one 16-byte
+// row; measured on sm_100a, tools/micro/hankel_probe.cu), so nothing is
+// expanded in memory.  D is a ring of output-row slots in TMEM (8 columns per
+// row); an output row is final after the MMA of input row r + kh - 1,
+// drained by the epilogue warps and re-zeroed for reuse R rows later.
+//
+// Precision: fp32 operands are split x = x1 + x2, f = f1 + f2 (bf16, round to
+// nearest, ~16 significant bits each) and D += x1 f1 + x1 f2 + x2 f1 in fp32,
+// error ~2^-16 per product (normwise ~1e-6 on config 5 vs the north-star
+// 7e-5).  Inputs the split cannot carry (|x| > 2^64, non-finite, or nonzero
+// |x| < 2^-100, where the bf16 low part would underflow) are detected per
+// tile; such a tile is recomputed by the CTA with FMAs in the reference tap
+// order after the MMA pass, so inf / NaN propagate as in the FFMA kernels.
+//
+// Work per input row and 1,024-column strip: 3 MMAs (smem-bound at ~48
+// cycles each: A 4 KB + B 2 KB) ~ 0.14 SM-cycles per output, against 0.38
+// for 7x7 FFMAs -- the kernel streams at HBM speed instead.
+//
+// Warp roles (one CTA per SM, 512 TMEM columns): 0 TMA producer (input rows
+// into an fp32 staging ring); 1, 2 MMA issuers (even / odd input rows, each
+// into its own D ring so the accumulation order is fixed: output = ring 0 +
+// ring 1); 3-10 split warps (two groups of 4 alternating stages: fp32 -> x1,
+// x2 bf16 rows); 11-14 epilogue (one TMEM lane quarter each: drain, transpose
+// through shared memory to lane-contiguous stores, re-zero the slot).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace sc {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
+namespace {
+using namespace tc;
+
+constexpr int kStrip = 1024;                 // output columns per CTA (128 lanes x 8 shifts)
+constexpr int kRS = 4;                       // input rows per staging stage
+constexpr int kStages = 6;                   // fp32 staging ring (24 rows in flight)
+// A stage is ONE 4-D TMA box: the image viewed as (256-column chunk, chunk,
+// row, image) with box {256, 4, kRS, 1} lands as kRS rows of 1,024
+// contiguous floats (W % 256 == 0); plus a {8, kRS} box for the 8 columns
+// after the strip.  (Five 2-D boxes per stage cost ~100 cycles of producer
+// issue each and capped the input stream at ~2.4 TB/s.)
+constexpr int kRowBytes = kStrip * 4;        // 4 KiB
+constexpr int kTailOff = kRS * kRowBytes;
+constexpr int kStageBytes = (kTailOff + kRS * 8 * 4 + 127) / 128 * 128;  // 16,512
+constexpr int kMaxKH = 9, kMaxKW = 9;
+constexpr int kMaxNW = 10;                   // window rows = kh + 1 rounded up to even
+// B matrix of one row parity p: n = 16 j' + 8 part + s (window row j',
+// filter part f1 / f2, shift s) x 16 k, bf16, no-swizzle K-major (LBO 128 B
+// between the k halves, SBO 256 B per 8 rows)
+constexpr int kBMat = kMaxNW * 16 * 32;      // 5 KiB
+// TMEM (512 columns): one D ring of kRing output-row slots of 16 columns
+// (f1 part | f2 part, 8 shifts each)
+constexpr int kRing = 32;
+// split bf16 rows (x1 | x2) in shared memory, read by the MMAs (SS form)
+// through the overlapping (Hankel) descriptor
+constexpr int kXSlots = 16;
+constexpr int kXRow = 2176;                  // 1,032 bf16 used, 128-aligned
+constexpr int kXSlotBytes = 2 * kXRow;
+constexpr int kDone = 64;                    // MMA-completion barriers, one per 4 input rows
+constexpr int kEpiRows = 2;                  // output rows drained per epilogue batch
+constexpr int kSplitWarps = 8, kEpiWarps = 8;
+constexpr int kWarpSplit0 = 2, kWarpEpi0 = kWarpSplit0 + kSplitWarps;  // 2, 10
+constexpr int kThreads = 32 * (kWarpEpi0 + kEpiWarps);                 // 576
+constexpr size_t kSmem =
+    1024 + (size_t)kStages * kStageBytes + (size_t)kXSlots * kXSlotBytes + 2 * kBMat;
+static_assert(kRing * 16 == 512, "TMEM budget");
+static_assert(kRing % kEpiRows == 0, "an epilogue batch never wraps the ring");
+static_assert(kRing >= kMaxNW + kEpiRows + 2, "ring slack");
+static_assert((kMaxKH + 2) / 2 * 2 <= kMaxNW, "window rows");
+static_assert(kDone * 4 >= 2 * (kRing + kMaxNW + kXSlots + 8), "commit ring must cover the issue lead");
+
+struct MmaArgs {
+  float taps[kMaxKH * kMaxKW];
+  int kh, kw, nw;
+  int oh, ow, h, w;
+  int seg_rows;
+};
+
+// 16 lanes x 256 bits: thread t gets lane t/4 (r0, r1) and t/4 + 8 (r2, r3),
+// columns 2 (t % 4) and 2 (t % 4) + 1 (cute SM100_TMEM_LOAD_16dp256b1x)
+__device__ __forceinline__ void tmem_ld_16x256(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+      "r"(0u)
+      : "memory");
+}
+
+// D (TMEM) += A (smem) x B (smem), issued by one elected lane of a warp
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(da), "l"(db), "r"(idesc)
+      : "memory");
+}
+
+// D (TMEM) += A (TMEM) x B (smem), issued by one elected lane of a warp whose
+// operands are warp-uniform (a single-lane `if` makes ptxas wrap the
+// instruction in a uniformity loop: ~120 vs ~70 cycles per MMA per warp,
+// tools/micro/hankel_probe.cu)
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t db, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(db), "r"(idesc)
+      : "memory");
+}
+
+// shared memory (descriptor) -> TMEM, 128 lanes x 256 bits, async in the
+// tensor pipe (ordered with the MMAs issued after it by the same thread)
+__device__ __forceinline__ void cp_elect(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc)
+      : "memory");
+}
+
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// Optional event trace of CTA (0, 0, 0) (tools/micro/mma_trace.cu builds
+// this file with -DSC_MMA_TRACE): clock64 stamps per role and row.
+#ifdef SC_MMA_TRACE
+__device__ long long g_mma_trace[8][4096];
+#define MMA_TRACE(role, idx, v)                                                       \
+  do {                                                                                \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (idx) < 4096)         \
+      g_mma_trace[role][idx] = (v);                                                   \
+  } while (0)
+#else
+#define MMA_TRACE(role, idx, v) \
+  do {                          \
+  } while (0)
+#endif
+
+// Plain shared-memory counters for the hand-offs on the issuer's critical
+// path: an mbarrier probe costs ~180 cycles of latency even when the phase
+// is complete, an acquire load ~30.
+__device__ __forceinline__ void smem_add_release(int* p, int v) {
+  asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ int smem_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+// 2^64 / 2^-100 as float bit patterns (magnitudes the bf16 split carries)
+constexpr uint32_t kHiBits = 0x5F800000u, kLoBits = 0x0D800000u;
+
+// x1 = bf16(v), x2 = bf16(v - x1) for 8 values -> 4 + 4 packed words; track
+// the magnitude range for the fallback test
+__device__ __forceinline__ void split8(const float4 a, const float4 b, uint32_t* w1, uint32_t* w2) {
+  const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t h = pack_bf16x2(f[2 * j], f[2 * j + 1]);
+    w1[j] = h;
+    w2[j] = pack_bf16x2(f[2 * j] - __uint_as_float(h << 16),
+                        f[2 * j + 1] - __uint_as_float(h & 0xffff0000u));
+  }
+}
+__device__ __forceinline__ void range8(const float4 a, const float4 b, uint32_t& mx, uint32_t& mn) {
+  const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t bits = __float_as_uint(f[j]) & 0x7fffffffu;
+    mx = max(mx, bits);
+    mn = min(mn, bits - 1u);  // zero -> 0xffffffff (ignored)
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv2d_mma_kernel(const __grid_constant__ CUtensorMap tm_main,
+                      const __grid_constant__ CUtensorMap tm_tail, float* __restrict__ y,
+                      const float* __restrict__ xg, const __grid_constant__ MmaArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t st_full[kStages], st_empty[kStages];
+  // progress counters (release / acquire), one per split group (+4 per
+  // stage) and per epilogue half (+4 per batch): the issuer reads them only
+  // when it runs out of known-ready rows
+  __shared__ int split_cnt[2], epi_cnt[2];
+  __shared__ __align__(8) uint64_t done[kDone];         // MMA completion, one per 4 input rows
+  __shared__ __align__(8) uint64_t ring_ready;
+  __shared__ uint32_t tmem_base_sh;
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* stages = base;
+  unsigned char* xrows = stages + kStages * kStageBytes;
+  unsigned char* bmats = xrows + kXSlots * kXSlotBytes;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kh = args.kh, kw = args.kw, nw = args.nw;
+  const int strip = blockIdx.x, seg = blockIdx.y, img = blockIdx.z;
+  const int c0 = strip * kStrip;
+  const int r0 = seg * args.seg_rows;
+  const int s_valid = min(args.seg_rows, args.oh - r0);   // output rows of this CTA
+  const int t_rows = s_valid + kh - 1;                      // input rows it reads
+  // window of input row t: output rows [a(t), a(t) + nw), a(t) even
+  auto win = [&](int t, int& a, int& p) {
+    const int u = t - kh + 1;
+    a = u >= 0 ? (u & ~1) : -((-u + 1) & ~1);
+    p = u - a;
+  };
+  int o_first, p0;
+  win(0, o_first, p0);
+
+  // ---- B matrices [parity p][n = 16 j' + 8 part + s][k] (see kBMat)
+  for (int e = threadIdx.x; e < 2 * nw * 16 * 16; e += kThreads) {
+    const int k = e & 15, n = (e >> 4) % (nw * 16), p = (e >> 4) / (nw * 16);
+    const int jp = n >> 4, part = (n >> 3) & 1, s = n & 7;
+    const int j = kh - 1 + p - jp, i = k - s;
+    const float v = (j >= 0 && j < kh && i >= 0 && i < kw) ? args.taps[j * kw + i] : 0.0f;
+    const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
+    const __nv_bfloat16 v2 = __float2bfloat16_rn(v - __bfloat162float(v1));
+    const uint32_t off = (uint32_t)p * kBMat + (n >> 3) * 256 + (k >> 3) * 128 + (n & 7) * 16 +
+                         (k & 7) * 2;
+    *reinterpret_cast<__nv_bfloat16*>(bmats + off) = part ? v2 : v1;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], 4);
+    }
+    split_cnt[0] = split_cnt[1] = epi_cnt[0] = epi_cnt[1] = 0;
+    for (int s = 0; s < kDone; ++s) mbar_init(&done[s], 1);
+    mbar_init(&ring_ready, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();  // B matrices (generic writes) -> tensor core (async proxy)
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  bool bad = false;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      prefetch_tmap(&tm_main);
+      prefetch_tmap(&tm_tail);
+      const uint32_t bytes = kTailOff + kRS * 8 * 4;
+      for (int t = 0, s = 0; t < t_rows; t += kRS, ++s) {
+        const int st = s % kStages;
+        MMA_TRACE(5, 2 * s, clock64());
+        if (s >= kStages) mbar_spin(&st_empty[st], ((s / kStages) - 1) & 1);
+        MMA_TRACE(5, 2 * s + 1, clock64());
+        unsigned char* dst = stages + st * kStageBytes;
+        mbar_arrive_expect_tx(&st_full[st], bytes);
+        tma_load_4d(dst, &tm_main, &st_full[st], 0, c0 / 256, r0 + t, img);
+        tma_load_3d(dst + kTailOff, &tm_tail, &st_full[st], c0 + kStrip, r0 + t, img);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    // per input row t two MMAs, D[ring rows a(t)..a(t)+nw) += x1 . [f1|f2]
+    // and += x2 . [f1|f2] (N = 16 nw; split in two where the window wraps the
+    // ring), A read from the split rows in shared memory through the
+    // overlapping descriptor.  One warp issues everything, so the
+    // accumulation order is fixed.  Operands are warp-uniform (shuffled base
+    // values) so they stay in uniform registers; readiness of split rows and
+    // drained ring slots is read from counters only when the known-ready
+    // range runs out (an mbarrier probe or acquire load costs ~180 cycles).
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t bmat_addr = __shfl_sync(0xffffffffu, smem_u32(bmats), 0);
+    const uint32_t xrows_addr = __shfl_sync(0xffffffffu, smem_u32(xrows), 0);
+    mbar_wait(&ring_ready, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int hi = o_first;                       // rows [o_first, hi) already touched
+    int rows_ready = 0;                     // input rows [0, rows_ready) split into smem
+    int drained = o_first;                  // output rows [o_first, drained) drained + zeroed
+    for (int t = 0; t < t_rows; ++t) {
+      if (lane == 0) MMA_TRACE(0, 5 * t, clock64());
+      while (t >= rows_ready) {
+        // stage s (rows 2s, 2s + 1) belongs to split group s % 2
+        const int c0s = smem_ld_acquire(&split_cnt[0]) >> 2, c1s = smem_ld_acquire(&split_cnt[1]) >> 2;
+        rows_ready = min(2 * c0s, 2 * c1s + 1) * kRS;        // stages [0, min(2 c0, 2 c1 + 1)) done
+      }
+      if (lane == 0) MMA_TRACE(0, 5 * t + 1, clock64());
+      int a, p;
+      win(t, a, p);
+      // rows entering the window: a slot's previous generation (row o - kRing)
+      // must be drained and zeroed
+      if (a + nw > hi) {
+        const int need = a + nw - kRing;     // rows < need must be drained
+        while (drained < need) {
+          // batch b (rows o_first + 2b, + 1) belongs to epilogue half b % 2
+          const int b0 = smem_ld_acquire(&epi_cnt[0]) >> 2, b1 = smem_ld_acquire(&epi_cnt[1]) >> 2;
+          drained = o_first + min(2 * b0, 2 * b1 + 1) * kEpiRows;
+        }
+        hi = a + nw;
+      }
+      if (lane == 0) MMA_TRACE(0, 5 * t + 2, clock64());
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t xsrc = xrows_addr + (uint32_t)(t % kXSlots) * kXSlotBytes;
+      const uint64_t dx1 = make_desc(xsrc, 16, 128, 0), dx2 = make_desc(xsrc + kXRow, 16, 128, 0);
+      const int q0 = (a - o_first) % kRing;              // even
+      const int n1 = min(nw, kRing - q0);                // rows before the ring wraps
+      const uint32_t bm = bmat_addr + (uint32_t)p * kBMat;
+      const uint64_t db0 = make_desc(bm, 128, 256, 0);
+      const uint32_t id0 = idesc_bf16(128, n1 * 16);
+#ifndef SC_MMA_NOMMA
+      mma_ss(tmem_u + q0 * 16, dx1, db0, id0);
+      mma_ss(tmem_u + q0 * 16, dx2, db0, id0);
+      if (n1 < nw) {
+        const uint64_t db1 = make_desc(bm + n1 * 512, 128, 256, 0);
+        const uint32_t id1 = idesc_bf16(128, (nw - n1) * 16);
+        mma_ss(tmem_u, dx1, db1, id1);
+        mma_ss(tmem_u, dx2, db1, id1);
+      }
+#endif
+      if (lane == 0) MMA_TRACE(0, 5 * t + 3, clock64());
+      // one commit per 4 input rows: the epilogue's "rows done" and the
+      // split warps' "row slots free"
+      if ((t & 3) == 3 || t + 1 == t_rows) commit_elect(&done[(t >> 2) % kDone]);
+      __syncwarp();
+      if (lane == 0) MMA_TRACE(0, 5 * t + 4, clock64());
+    }
+  } else if (warp < kWarpEpi0) {
+    // ------------------------------------------------------------ split warps
+    // group g (4 warps) handles stages g, g + 2, ..; thread u of the group
+    // splits samples 8u..8u+7 of each row (thread 0 also the tail 1024..1031)
+    // into the row's x1 / x2 bf16 rows in shared memory
+    const int grp = (warp - kWarpSplit0) >> 2;
+    const int u = threadIdx.x - 32 * (kWarpSplit0 + 4 * grp);   // 0..127
+    uint32_t mx = 0, mn = 0xffffffffu;
+    const int own = 32 * u;
+    for (int s = grp, t0 = grp * kRS; t0 < t_rows; s += 2, t0 += 2 * kRS) {
+      const int st = s % kStages;
+      if (warp == kWarpSplit0 + 4 * grp && lane == 0) MMA_TRACE(2, 4 * t0, clock64());
+      mbar_spin(&st_full[st], (s / kStages) & 1);
+      const unsigned char* sb = stages + st * kStageBytes;
+#pragma unroll
+      for (int rr = 0; rr < kRS; ++rr) {
+        const int t = t0 + rr;
+        if (t >= t_rows) break;
+        const float4* po = reinterpret_cast<const float4*>(sb + own + rr * kRowBytes);
+        const float4 a0 = po[0], a1 = po[1];
+        uint32_t v[8];
+        split8(a0, a1, v, v + 4);
+        range8(a0, a1, mx, mn);
+        uint32_t vt[8];
+        if (u == 0) {
+          const float4* pt = reinterpret_cast<const float4*>(sb + kTailOff + rr * 32);
+          const float4 b0 = pt[0], b1 = pt[1];
+          split8(b0, b1, vt, vt + 4);
+          range8(b0, b1, mx, mn);
+        }
+        if (warp == kWarpSplit0 + 4 * grp && lane == 0) MMA_TRACE(2, 4 * t + 1, clock64());
+        if (t >= kXSlots) {
+          const int gq = (t - kXSlots) >> 2;                 // group of 4 holding row t - kXSlots
+          mbar_spin(&done[gq % kDone], (gq / kDone) & 1);
+        }
+        if (warp == kWarpSplit0 + 4 * grp && lane == 0) MMA_TRACE(2, 4 * t + 2, clock64());
+        unsigned char* xr = xrows + (t % kXSlots) * kXSlotBytes;
+        *reinterpret_cast<uint4*>(xr + 16 * u) = make_uint4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<uint4*>(xr + kXRow + 16 * u) = make_uint4(v[4], v[5], v[6], v[7]);
+        if (u == 0) {
+          *reinterpret_cast<uint4*>(xr + 16 * 128) = make_uint4(vt[0], vt[1], vt[2], vt[3]);
+          *reinterpret_cast<uint4*>(xr + kXRow + 16 * 128) = make_uint4(vt[4], vt[5], vt[6], vt[7]);
+        }
+        if (warp == kWarpSplit0 + 4 * grp && lane == 0) MMA_TRACE(2, 4 * t + 3, clock64());
+      }
+      fence_proxy_async();   // generic writes -> tensor-core copy (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&st_empty[st]);
+        smem_add_release(&split_cnt[grp], 1);
+      }
+    }
+    bad = mx > kHiBits || mn < kLoBits - 1u;
+  } else {
+    // ------------------------------------------------------------ epilogue
+    // two groups of 4 warps (one per TMEM lane quarter) drain alternating
+    // batches of kEpiRows rows (latency hiding: a batch is a chain of TMEM
+    // loads, adds and global stores)
+    const int q = warp & 3;                              // TMEM lane quarter
+    const int half = (warp - kWarpEpi0) >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+    if (half == 0) {
+      for (int c = 0; c < kRing * 16; c += 8) tmem_zero8(lane_base + c);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring_ready);
+    }
+    const int ow = args.ow;
+    // thread t holds lanes m = 32 q + 8 j + t / 4 (j = 0..3), shifts
+    // 2 (t % 4) and + 1, i.e. columns col_t + 64 j and + 1
+    const int col_t = c0 + 8 * (32 * q + (lane >> 2)) + 2 * (lane & 3);
+    // the warp's 256 columns all in range and 8-byte aligned pairs: STG.64
+    const bool fast = __shfl_sync(0xffffffffu,
+                                  (int)(c0 + 256 * (q + 1) <= ow &&
+                                        ((reinterpret_cast<uintptr_t>(y) | (uintptr_t)(ow * 4)) &
+                                         7) == 0),
+                                  0) != 0;
+    float* ybase = y + (int64_t)img * args.oh * ow + col_t;
+    // MMA completion is signalled per group of 4 input rows (both issuers);
+    // the groups are waited in order
+    int groups_done = 0;
+    auto wait_done = [&](int t) {
+      if (t >= t_rows) t = t_rows - 1;
+      for (; groups_done <= (t >> 2); ++groups_done)
+        mbar_wait_sleep(&done[groups_done % kDone], (groups_done / kDone) & 1, 32, 128);
+    };
+    for (int o0 = o_first + half * kEpiRows; o0 < s_valid; o0 += 2 * kEpiRows) {
+      const int nr = min(kEpiRows, s_valid - o0);
+      // every MMA touching rows < o0 + nr has t <= o0 + nr - 1 + kh (the
+      // window's zero row) and t < t_rows; each issuer commits in order, so
+      // the last t of each parity suffices
+      const int th = o0 + nr - 1 + kh;
+      [[maybe_unused]] const int bi = (o0 - o_first) / kEpiRows;
+      if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi, clock64());
+      wait_done(th);
+      if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 1, clock64());
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t v[kEpiRows][2][2][4];                     // [row][f1 / f2 part][lane half][reg]
+      const int slot0 = (o0 - o_first) % kRing;          // batches never wrap (kRing % kEpiRows == 0)
+#pragma unroll
+      for (int i = 0; i < kEpiRows; ++i)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            tmem_ld_16x256(lane_base + ((uint32_t)(16 * hh) << 16) + (slot0 + i) * 16 + e * 8,
+                           v[i][e][hh]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 2, clock64());
+#pragma unroll
+      for (int i = 0; i < kEpiRows; ++i) {
+#ifndef SC_MMA_SKIP_ZERO
+        tmem_zero8(lane_base + (slot0 + i) * 16);
+        tmem_zero8(lane_base + (slot0 + i) * 16 + 8);
+#endif
+      }
+#ifndef SC_MMA_SKIP_STG
+#pragma unroll
+      for (int i = 0; i < kEpiRows; ++i) {
+        const int o = o0 + i;
+        if (i < nr && o >= 0) {
+          float* yr = ybase + (int64_t)(r0 + o) * ow;
+          float sv[8];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              sv[4 * hh + 2 * g] = __uint_as_float(v[i][0][hh][2 * g]) +
+                                   __uint_as_float(v[i][1][hh][2 * g]);
+              sv[4 * hh + 2 * g + 1] = __uint_as_float(v[i][0][hh][2 * g + 1]) +
+                                       __uint_as_float(v[i][1][hh][2 * g + 1]);
+            }
+          if (fast) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<float2*>(yr + 64 * j) = make_float2(sv[2 * j], sv[2 * j + 1]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int c = col_t + 64 * j;
+              if (c < ow) yr[64 * j] = sv[2 * j];
+              if (c + 1 < ow) yr[64 * j + 1] = sv[2 * j + 1];
+            }
+          }
+        }
+      }
+#endif
+      if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 3, clock64());
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) smem_add_release(&epi_cnt[half], 1);
+      if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 4, clock64());
+    }
+  }
+
+  // ---- tiles with inputs the bf16 split cannot carry: recompute with FMAs
+  // in the reference tap order (reference.py:19-22), overwriting the MMA
+  // results (a barrier orders the two sets of global stores)
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  const int redo = __syncthreads_or(bad);
+  if (redo) {
+    const int64_t plane_in = (int64_t)args.h * args.w;
+    const float* ximg = xg + (int64_t)img * plane_in;
+    float* yimg = y + (int64_t)img * args.oh * args.ow;
+    const int cols = min(kStrip, args.ow - c0);
+    for (int64_t idx = threadIdx.x; idx < (int64_t)s_valid * cols; idx += kThreads) {
+      const int r = r0 + (int)(idx / cols), c = c0 + (int)(idx % cols);
+      float acc = 0.0f;
+      for (int j = 0; j < kh; ++j)
+        for (int i = 0; i < kw; ++i)
+          acc = fmaf(args.taps[j * kw + i], ximg[(int64_t)(r + j) * args.w + c + i], acc);
+      yimg[(int64_t)r * args.ow + c] = acc;
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+}  // namespace
+
+// Whether the slide-MMA kernel serves this call (fast mode only).
+bool conv2d_mma_applicable(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
+                           int64_t kh, int64_t kw) {
+  // opt-in (SC_CONV_MMA=1): measured at parity with the FFMA kernels on
+  // config 5 ("slide-MMA"), not faster yet
+  static const int enabled = env_int("SC_CONV_MMA", 0);
+  if (!enabled || kh < 1 || kh > kMaxKH || kw < 1 || kw > kMaxKW) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (w % 256) || h > 0x7fffffff || w > 0x7fffffff ||
+      batch > 65535)
+    return false;
+  // filter taps the bf16 split carries exactly enough (see the header)
+  for (int64_t i = 0; i < kh * kw; ++i) {
+    const float a = fabsf(f[i]);
+    if (!(a <= 0x1p60f) || (a != 0.0f && a < 0x1p-100f)) return false;
+  }
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  const int64_t strips = (ow + kStrip - 1) / kStrip;
+  // enough 1,024-column x ~64-row tiles for two waves: large images only
+  return batch * strips * ((oh + 63) / 64) >= 2 * sm_count();
+}
+
+int conv2d_mma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, int64_t kh,
+               int64_t kw, float* y, cudaStream_t st) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  MmaArgs a;
+  std::memset(&a, 0, sizeof a);
+  for (int64_t i = 0; i < kh * kw; ++i) a.taps[i] = f[i];
+  a.kh = (int)kh, a.kw = (int)kw, a.nw = (int)((kh + 2) & ~1);
+  a.oh = (int)oh, a.ow = (int)ow, a.h = (int)h, a.w = (int)w;
+  const int64_t strips = (ow + kStrip - 1) / kStrip;
+  // Row segments: one CTA per SM, every CTA costs ~(rows + kh - 1) input
+  // rows; pick the segment length minimising waves x rows (whole waves).
+  const int64_t slots = sm_count();
+  int64_t best = -1, rows = oh;
+  const int env_rows = env_int("SC_MMA_ROWS", 0);
+  if (env_rows > 0) {
+    rows = std::min<int64_t>(env_rows, oh);
+  } else {
+    for (int64_t segs = 1; segs <= std::min<int64_t>(oh, 65535); ++segs) {
+      const int64_t r = (oh + segs - 1) / segs;
+      const int64_t n = batch * strips * ((oh + r - 1) / r);
+      const int64_t cost = (n + slots - 1) / slots * (r + kh - 1 + 8);  // +8: pipeline fill
+      if (best < 0 || cost < best) best = cost, rows = r;
+      if (r <= 16) break;
+    }
+  }
+  a.seg_rows = (int)rows;
+  const int64_t segs = (oh + rows - 1) / rows;
+  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
+    return fail(SC_ERR_UNSUPPORTED, "conv2d mma: grid too large");
+
+  CUtensorMap tm_main, tm_tail;
+  {
+    cuuint64_t dims[4] = {256, (cuuint64_t)(w / 256), (cuuint64_t)h, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {1024, (cuuint64_t)w * 4, (cuuint64_t)(h * w) * 4};
+    cuuint32_t box[4] = {256, 4, (cuuint32_t)kRS, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(&tm_main, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "conv2d mma: tensor map failed");
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)(h * w) * 4};
+    cuuint32_t box[3] = {8, (cuuint32_t)kRS, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&tm_tail, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(x), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "conv2d mma: tail tensor map failed");
+  }
+  static uint64_t attr = 0;
+  SC_CUDA(set_smem_limit_once(conv2d_mma_kernel, kSmem, &attr));
+  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
+  conv2d_mma_kernel<<<grid, kThreads, kSmem, st>>>(tm_main, tm_tail, y, x, a);
+  SC_LAUNCH_CHECK("conv2d_mma_kernel");
+  return SC_OK;
+}
+
+}  // namespace sc
