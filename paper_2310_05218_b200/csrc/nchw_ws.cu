@@ -51,7 +51,7 @@ constexpr int kDStride = 112;                 // TMEM columns per accumulator
 constexpr int kTmemA = 2 * kDStride;          // 224
 constexpr int kTmemCols = 512;
 constexpr int kSlots = 4;                     // split input-row ring
-constexpr int kStages = 2;                    // fp32 staging ring
+constexpr int kStages = 3;                    // fp32 staging ring
 constexpr int kPixBytes = 128;                // one pixel's 64 bf16 channels
 constexpr int kXRegion = ((kMaxWt + 2) * kPixBytes + 1023) / 1024 * 1024;  // 15 KiB
 constexpr int kSlotBytes = 2 * kXRegion;                                     // x1 | x2
@@ -64,6 +64,22 @@ constexpr int kIssuer2 = 2 + kSplitWarps + kEpiWarps;   // 14
 constexpr int kThreads = 32 * (kIssuer2 + 1);
 static_assert(kTmemA + 9 * kMaxCin / 2 <= kTmemCols, "TMEM budget");
 
+// Optional timeline of every CTA (tools/micro/ws_trace.cu builds this file
+// with -DSC_WS_TRACE): globaltimer stamps per CTA at fixed events.
+#ifdef SC_WS_TRACE
+__device__ unsigned long long g_ws_trace[160][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+  return t;
+}
+#define WS_TRACE(ev) g_ws_trace[blockIdx.x][ev] = gtime()
+#else
+#define WS_TRACE(ev) \
+  do {               \
+  } while (0)
+#endif
+
 struct WsArgs {
   int nb, cin, h, w, cout;
   int wt, col_tiles, seg_rows, segs;   // row segments of seg_rows rows per (image, column tile)
@@ -75,6 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmh, const uint32_t* __restrict__ apack,
                       float* __restrict__ y, const WsArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  if (threadIdx.x == 0) WS_TRACE(0);
   __shared__ __align__(8) uint64_t stage_full[kStages], stage_empty[kStages];
   __shared__ __align__(8) uint64_t slot_full[kSlots], slot_free[kSlots];
   __shared__ __align__(8) uint64_t d_full[2], d_empty[2];
@@ -138,6 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     // issues all its 16-byte loads before storing (one L2 round trip).
     const int q = warp & 3, third = (warp - 2) >> 2;  // 0..2
     const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+    // launched as a programmatic dependent of the weight-packing kernel: only
+    // this load needs its result; barrier setup, TMEM allocation and the
+    // first input rows overlap it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (third == 0) {
       uint32_t z[16];
 #pragma unroll
@@ -200,59 +221,64 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1 || warp == kIssuer2) {
     // ------------------------------------------------ MMA issuers (x1 / x2)
-    if (lane == 0) {
-      const int part = warp == 1 ? 0 : 1;  // which split product this thread issues
-      const uint32_t idesc = part ? idesc64 : idesc128;
-      mbar_wait(&a_ready, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      int s = 0, o = 0;
-      for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
-        int n, w0, r0, nr;
-        item_of(it, n, w0, r0, nr);
-        const int base = s;  // seq of input row r0 - 1
-        for (int rr = 0; rr < nr; ++rr, ++o) {
-          const int acc = o & 1;
-          if (o >= 2) mbar_wait(&d_empty[acc], ((o >> 1) - 1) & 1);
-          // rows r-1 and r were confirmed by the previous output row (a slot
-          // cannot be refilled before this row frees it), so only the new
-          // row r+1 is waited for -- a try_wait costs ~0.1 us even when the
-          // phase is already complete
+    // whole warp, warp-uniform operands (shuffled), one elected lane issues
+    const int part = __shfl_sync(0xffffffffu, warp == 1 ? 0 : 1, 0);  // which split product
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t idesc = part ? idesc64 : idesc128;
+    const uint32_t slots_u = __shfl_sync(0xffffffffu, smem_u32(slots), 0) + part * kXRegion;
+    mbar_wait(&a_ready, 0);
+    if (part == 0 && threadIdx.x % 32 == 0) WS_TRACE(1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int s = 0, o = 0;
+    for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
+      int n, w0, r0, nr;
+      item_of(it, n, w0, r0, nr);
+      const int base = s;  // seq of input row r0 - 1
+      for (int rr = 0; rr < nr; ++rr, ++o) {
+        const int acc = o & 1;
+        if (o >= 2) mbar_wait(&d_empty[acc], ((o >> 1) - 1) & 1);
+        // rows r-1 and r were confirmed by the previous output row (a slot
+        // cannot be refilled before this row frees it), so only the new
+        // row r+1 is waited for
 #pragma unroll
-          for (int dj = 0; dj < 3; ++dj) {
-            if (rr > 0 && dj < 2) continue;
-            const int sq = base + rr + dj;
-            mbar_wait(&slot_full[sq % kSlots], (sq / kSlots) & 1);
-          }
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t d = tmem + acc * kDStride;
+        for (int dj = 0; dj < 3; ++dj) {
+          if (rr > 0 && dj < 2) continue;
+          const int sq = base + rr + dj;
+          mbar_wait(&slot_full[sq % kSlots], (sq / kSlots) & 1);
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem_u + acc * kDStride;
 #pragma unroll 1
-          for (int dj = 0; dj < 3; ++dj) {
-            const unsigned char* xs =
-                slots + ((base + rr + dj) % kSlots) * kSlotBytes + part * kXRegion;
+        for (int dj = 0; dj < 3; ++dj) {
+          const uint32_t xs = slots_u + ((base + rr + dj) % kSlots) * kSlotBytes;
 #pragma unroll
-            for (int di = 0; di < 3; ++di) {
-              const uint32_t a0 = tmem + kTmemA + (dj * 3 + di) * (cin / 2);
-              // tap column offset di: the window starts at slot pixel 1 + di.
-              // Measured on sm_100a (tools/ws_debug.py): with this 128-byte
-              // swizzled K-major B operand the MMA's first row is the one
-              // after the descriptor start, so the start is one pixel earlier.
-              const uint32_t b0 = smem_u32(xs) + di * kPixBytes;
-              for (int kk = 0; kk < ksteps; ++kk) {
-                const uint64_t db = make_desc(b0 + kk * 32, 16, 1024, 2);
-                mma_bf16_ts_rt(d, a0 + kk * 8, db, idesc, 1u);
-              }
+          for (int di = 0; di < 3; ++di) {
+            const uint32_t a0 = tmem_u + kTmemA + (dj * 3 + di) * (cin / 2);
+            // tap column offset di: the window starts at slot pixel 1 + di.
+            // Measured on sm_100a (tools/ws_debug.py): with this 128-byte
+            // swizzled K-major B operand the MMA's first row is the one
+            // after the descriptor start, so the start is one pixel earlier.
+            const uint32_t b0 = xs + di * kPixBytes;
+            for (int kk = 0; kk < ksteps; ++kk) {
+              const uint64_t db = make_desc(b0 + kk * 32, 16, 1024, 2);
+              mma_bf16_ts_elect(d, a0 + kk * 8, db, idesc);
             }
           }
-          umma_commit(&d_full[acc]);
-          // input row r-1 is not read by any later output row of this item
-          umma_commit(&slot_free[(base + rr) % kSlots]);
-          if (rr == nr - 1) {
-            umma_commit(&slot_free[(base + rr + 1) % kSlots]);
-            umma_commit(&slot_free[(base + rr + 2) % kSlots]);
-          }
         }
-        s = base + nr + 2;
+        if (part == 0 && threadIdx.x % 32 == 0) {
+          if (o == 0) WS_TRACE(2);
+          WS_TRACE(3);
+        }
+        umma_commit_elect(&d_full[acc]);
+        // input row r-1 is not read by any later output row of this item
+        umma_commit_elect(&slot_free[(base + rr) % kSlots]);
+        if (rr == nr - 1) {
+          umma_commit_elect(&slot_free[(base + rr + 1) % kSlots]);
+          umma_commit_elect(&slot_free[(base + rr + 2) % kSlots]);
+        }
+        __syncwarp();
       }
+      s = base + nr + 2;
     }
   } else if (warp < 2 + kSplitWarps) {
     // ------------------------------------------------ split warps
@@ -366,11 +392,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_empty[acc]);
+        if (q == 0 && lane == 0) {
+          if (o == 0) WS_TRACE(6);
+          WS_TRACE(4);
+        }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) WS_TRACE(5);
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -386,6 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // half = even element)
 __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __restrict__ apack,
                                     int cin, int cout) {
+  // let the dependent conv kernel launch now (it waits for this grid's
+  // completion before reading apack)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int a_cols = 9 * cin / 2;
   const int total = (cout + kCo - 1) / kCo * 128 * a_cols;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -484,7 +518,19 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   static uint64_t attr = 0;  // devices whose limit is set
   SC_CUDA(set_smem_limit_once(nchw3x3_ws_kernel, (int)kSmem, &attr));
   const unsigned grid = (unsigned)(a.ctas_per_co * co_tiles);
-  nchw3x3_ws_kernel<<<grid, kThreads, kSmem, st>>>(mx, mh, apack, y, a);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SC_CUDA(cudaLaunchKernelEx(&cfg, nchw3x3_ws_kernel, mx, mh, (const uint32_t*)apack, y, a));
+  }
   SC_LAUNCH_CHECK("nchw3x3_ws_kernel");
   SC_CUDA(cudaFreeAsync(apack, st));
   return SC_OK;

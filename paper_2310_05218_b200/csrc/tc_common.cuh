@@ -97,5 +97,28 @@ __device__ __forceinline__ void mma_bf16_ts_rt(uint32_t tmem_d, uint32_t tmem_a,
       : "memory");
 }
 
+// Whole-warp forms: the warp runs the issue loop with warp-uniform operands
+// and one elected lane issues.  A lone `if (lane == 0)` issuer makes ptxas
+// wrap each tcgen05 instruction in a uniformity loop (R2UR.BROADCAST per
+// operand + BRA.U.ANY): ~120 vs ~70 cycles per MMA per warp
+// (tools/micro/hankel_probe.cu).
+__device__ __forceinline__ void mma_bf16_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                                  uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 }  // namespace tc
 }  // namespace sc
