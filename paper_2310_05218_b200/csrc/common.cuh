@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/slideconv_b200.h"
 
@@ -90,6 +92,32 @@ cudaError_t set_smem_limit_once(F* func, size_t bytes, uint64_t* done, int carve
     e = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
   if (e == cudaSuccess) __atomic_fetch_or(done, bit, __ATOMIC_RELEASE);
   return e;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// once its predecessor in the stream has triggered (griddepcontrol.
+// launch_dependents) and must execute griddepcontrol.wait before touching
+// memory the predecessor may read or write.  Kernels launched this way
+// trigger their own dependents early, so back-to-back calls overlap launch
+// latency and prologue with the predecessor's tail.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool off = [] {
+    const char* e = getenv("SC_PDL");  // SC_PDL=0: plain stream order (A/B knob)
+    return e && e[0] == '0';
+  }();
+  cfg.attrs = at;
+  cfg.numAttrs = off ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------ arithmetic

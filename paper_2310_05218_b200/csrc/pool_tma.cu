@@ -152,6 +152,11 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
   float* stage_all = reinterpret_cast<float*>(base + NBUF * BUF);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // programmatic dependent launch: the next kernel in the stream may start
+  // its prologue now; this one waits for its predecessor (memory visible)
+  // after setting up, so back-to-back launches overlap launch latency and
+  // prologue with the predecessor's tail
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tid == 0) {
     for (int i = 0; i < NBUF; ++i) {
       mbar_init(&full_bar[i], 1);
@@ -160,6 +165,7 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
     fence_mbar_init();
   }
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   // tile t -> (row, first output); 32-bit math (host guarantees the range)
   // CTA b owns the contiguous tiles [b*tpc, min((b+1)*tpc, n)): the hardware
@@ -313,8 +319,9 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
   Taps1<K> taps{};
   if (w)
     for (int i = 0; i < K; ++i) taps.f[i] = w[i];
-  pool_tma_kernel<kOp, K, NBUF><<<(unsigned)grid, 32 * (kTmaWarps + 1), smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, taps);
+  SC_CUDA(launch_pdl(pool_tma_kernel<kOp, K, NBUF>, dim3((unsigned)grid),
+                     dim3(32 * (kTmaWarps + 1)), smem, st, map, y, out_len, tiles_per_row, n_tiles,
+                     tpc, taps));
   SC_LAUNCH_CHECK("pool_tma_kernel");
   return SC_OK;
 }
