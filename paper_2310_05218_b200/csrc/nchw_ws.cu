@@ -86,6 +86,7 @@ struct WsArgs {
   int items_per_co, ctas_per_co;
 };
 
+template <int kKSteps>  // Cin / 16
 __global__ void __launch_bounds__(kThreads, 1)
     nchw3x3_ws_kernel(const __grid_constant__ CUtensorMap tmx,
                       const __grid_constant__ CUtensorMap tmh, const uint32_t* __restrict__ apack,
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int co_tile = blockIdx.x % co_tiles;
   const int cta_in_co = blockIdx.x / co_tiles;
   const int a_cols = 9 * cin / 2;
-  const int ksteps = cin / 16;
+  constexpr int ksteps = kKSteps;
   const uint32_t idesc128 = idesc_bf16(128, wt), idesc64 = idesc_bf16(64, wt);
 
   // item -> (image, column tile, first row, row count)
@@ -237,33 +238,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int rr = 0; rr < nr; ++rr, ++o) {
         const int acc = o & 1;
         if (o >= 2) mbar_wait(&d_empty[acc], ((o >> 1) - 1) & 1);
-        // rows r-1 and r were confirmed by the previous output row (a slot
-        // cannot be refilled before this row frees it), so only the new
-        // row r+1 is waited for
-#pragma unroll
-        for (int dj = 0; dj < 3; ++dj) {
-          if (rr > 0 && dj < 2) continue;
-          const int sq = base + rr + dj;
-          mbar_wait(&slot_full[sq % kSlots], (sq / kSlots) & 1);
-        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        // input rows r-1, r, r+1 are waited for right before the taps that
+        // read them, so at an item's first row the MMAs of row r-1 overlap
+        // the split of rows r and r+1; later rows only wait for the new row
+        // r+1 (rows r-1 and r were confirmed by the previous output row: a
+        // slot cannot be refilled before this row frees it)
         const uint32_t d = tmem_u + acc * kDStride;
-#pragma unroll 1
-        for (int dj = 0; dj < 3; ++dj) {
-          const uint32_t xs = slots_u + ((base + rr + dj) % kSlots) * kSlotBytes;
+        const uint32_t a_base = tmem_u + kTmemA;
 #pragma unroll
-          for (int di = 0; di < 3; ++di) {
-            const uint32_t a0 = tmem_u + kTmemA + (dj * 3 + di) * (cin / 2);
-            // tap column offset di: the window starts at slot pixel 1 + di.
-            // Measured on sm_100a (tools/ws_debug.py): with this 128-byte
-            // swizzled K-major B operand the MMA's first row is the one
-            // after the descriptor start, so the start is one pixel earlier.
-            const uint32_t b0 = xs + di * kPixBytes;
-            for (int kk = 0; kk < ksteps; ++kk) {
-              const uint64_t db = make_desc(b0 + kk * 32, 16, 1024, 2);
-              mma_bf16_ts_elect(d, a0 + kk * 8, db, idesc);
-            }
+        for (int dj = 0; dj < 3; ++dj) {
+          const int sq = base + rr + dj;
+          if (rr == 0 || dj == 2) {
+            mbar_wait(&slot_full[sq % kSlots], (sq / kSlots) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           }
+          // tap column offset di: the window starts at slot pixel 1 + di.
+          // Measured on sm_100a (tools/ws_debug.py): with this 128-byte
+          // swizzled K-major B operand the MMA's first row is the one after
+          // the descriptor start, so the start is one pixel earlier.  Fully
+          // unrolled: operands are compile-time offsets (tap column di =
+          // 128 B, k step = 32 B in the descriptor's 16-byte units).
+          const uint64_t db = make_desc(slots_u + (sq % kSlots) * kSlotBytes, 16, 1024, 2);
+#pragma unroll
+          for (int di = 0; di < 3; ++di)
+#pragma unroll
+            for (int kk = 0; kk < ksteps; ++kk)
+              mma_bf16_ts_elect(d, a_base + (dj * 3 + di) * (ksteps * 8) + kk * 8,
+                                db + (uint64_t)(di * 8 + kk * 2), idesc);
         }
         if (part == 0 && threadIdx.x % 32 == 0) {
           if (o == 0) WS_TRACE(2);
@@ -516,7 +518,9 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
                         0, st>>>(wt, apack, (int)cin, (int)cout);
   SC_LAUNCH_CHECK("pack_weights_kernel");
   static uint64_t attr = 0;  // devices whose limit is set
-  SC_CUDA(set_smem_limit_once(nchw3x3_ws_kernel, (int)kSmem, &attr));
+  auto kern = cin == 64 ? nchw3x3_ws_kernel<4> : nchw3x3_ws_kernel<2>;
+  static uint64_t attr2 = 0;
+  SC_CUDA(set_smem_limit_once(kern, (int)kSmem, cin == 64 ? &attr : &attr2));
   const unsigned grid = (unsigned)(a.ctas_per_co * co_tiles);
   {
     cudaLaunchConfig_t cfg = {};
@@ -529,7 +533,7 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    SC_CUDA(cudaLaunchKernelEx(&cfg, nchw3x3_ws_kernel, mx, mh, (const uint32_t*)apack, y, a));
+    SC_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, (const uint32_t*)apack, y, a));
   }
   SC_LAUNCH_CHECK("nchw3x3_ws_kernel");
   SC_CUDA(cudaFreeAsync(apack, st));
