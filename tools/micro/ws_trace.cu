@@ -41,6 +41,26 @@ int main() {
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0; cudaEventElapsedTime(&ms, e0, e1);
   printf("rc %d %s %.4f ms (pack + conv)\n", rc, cudaGetErrorString(err), ms);
+  // the call as a sequence of separately timed launches
+  {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    float t_full = 0;
+    for (int it = 0; it < 5; ++it) {
+      cudaEventRecord(a);
+      sc::nchw3x3_ws(x, n, c, h, w, wt, c, y, 0);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&t_full, a, b);
+    }
+    printf("full call (pack + conv): %.2f us\n", t_full * 1e3);
+    cudaEventRecord(a);
+    for (int it = 0; it < 20; ++it) sc::nchw3x3_ws(x, n, c, h, w, wt, c, y, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&t_full, a, b);
+    printf("back to back: %.2f us per call\n", t_full * 1e3 / 20);
+  }
   static unsigned long long tr[160][8];
   cudaMemcpyFromSymbol(tr, sc::g_ws_trace, sizeof tr);
   unsigned long long t0 = ~0ull, tend = 0;
