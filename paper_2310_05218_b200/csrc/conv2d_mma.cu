@@ -555,7 +555,7 @@ bool conv2d_mma_applicable(const float* x, int64_t batch, int64_t h, int64_t w, 
                            int64_t kh, int64_t kw) {
   // opt-in (SC_CONV_MMA=1): measured at parity with the FFMA kernels on
   // config 5 ("slide-MMA"), not faster yet
-  static const int enabled = env_int("SC_CONV_MMA", 0);
+  const int enabled = env_int("SC_CONV_MMA", 0);  // read per call (A/B in one process)
   if (!enabled || kh < 1 || kh > kMaxKH || kw < 1 || kw > kMaxKW) return false;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (w % 256) || h > 0x7fffffff || w > 0x7fffffff ||
       batch > 65535)

@@ -1,3 +1,6 @@
+"""Device-side A/B of the slide-MMA conv (SC_CONV_MMA=1) against the FFMA
+kernel on a 7x7 image: max difference, wrong rows / columns.
+python tools/pair_diag.py H W"""
 import os, sys, torch, numpy as np
 sys.path.insert(0, "/root/repo")
 import paper_2310_05218_b200 as sc
