@@ -38,6 +38,15 @@ elif which == "conv1d":
     f = np.random.default_rng(1).standard_normal((1, 7), dtype=np.float32)
     for _ in range(reps):
         sc.conv2d_reference(x, f, exact=False)
+elif which == "conv7full":
+    # config 5 itself: one 65,536^2 image (16 GiB in + 16 GiB out)
+    x = torch.empty((65536, 65536), device=dev)
+    x.uniform_(-1, 1, generator=g)
+    f = np.random.default_rng(7).standard_normal((7, 7), dtype=np.float32) / 7
+    y = torch.empty((65530, 65530), device=dev)
+    from paper_2310_05218_b200 import _ops
+    for _ in range(reps):
+        _ops.conv2d_into(x, f, y)
 elif which == "conv7":
     x = torch.rand((16384, 65536), generator=g, device=dev)
     f = np.random.default_rng(7).standard_normal((7, 7), dtype=np.float32) / 7
