@@ -1,45 +1,43 @@
 // Single-channel 2-D convolution on the 5th-generation tensor cores (fast
-// mode): the slide-MMA formulation of _accumulate_taps (reference.py:15-23)
-// for filters with kw <= 9 and kh <= 15 -- BASELINE config 5 (7x7 on a
-// 65,536^2 image) and the mid-size square filters of the paper's sweep.
+// mode, opt-in SC_CONV_MMA=1): the "slide-MMA" formulation of
+// _accumulate_taps (reference.py:15-23) for filters with kw <= 9 and kh <= 9
+// -- BASELINE config 5 (7x7 on a 65,536^2 image) and 9x9 of the paper's
+// sweep.  SURVEY 8(f)4; measured at parity with the FFMA kernels, see
+// profiles/r02/slide_mma.md for the nine variants and why.
 //
-// Why: the FFMA kernels (conv2d.cu) need kh*kw FMAs per output; for 7x7 that
-// is 49 FMA-pipe cycles per 128 outputs, which under the board's power cap
-// (~1.65 GHz sustained) is slower than streaming the image (config 5: 7.9 ms
-// against a 5.25 ms HBM floor).  As an MMA, with
+// Formulation.  Per input row rho and 1,024-column strip, with
 //   M = 128 "lanes" m, each the 8 output columns c0 + 8m + s (s = 0..7),
 //   K = 16 consecutive input samples x[rho][c0 + 8m + k] (k = 0..15),
-//   N = (output row r, shift s) for the 8 (= kh + 1, even) output rows an
-//       input row rho can touch,
-// one input row contributes D[m][(r, s)] += sum_k x[rho][c0+8m+k] * f[rho-r][k-s]
-// -- the whole 7x7 tap set of 1,024 columns x 8 rows in ONE M128 N64 K16
-// MMA.  The B operand (the taps, placed by shift and filter row) is a
-// constant of the filter; the A operand is the input row itself: a plain
-// bf16 row read through a no-swizzle K-major descriptor with LBO = 16 B and
-// SBO = 128 B makes A[m][k] = x[8m + k] (core matrices overlap by one 16-byte
-// row; measured on sm_100a, tools/micro/hankel_probe.cu), so nothing is
-// expanded in memory.  D is a ring of output-row slots in TMEM (8 columns per
-// row); an output row is final after the MMA of input row r + kh - 1,
-// drained by the epilogue warps and re-zeroed for reuse R rows later.
+//   N = (window row j', filter part f1 | f2, shift s) for the nw = kh + 1
+//       (even) output rows an input row can touch,
+// one MMA computes D[m][(r, part, s)] += sum_k x[rho][c0+8m+k] f_part[rho-r][k-s]:
+// the whole 7x7 tap set of 1,024 columns x 8 rows in one M128 N128 K16 MMA.
+// B (the taps placed by shift, filter row and split part) is a constant of
+// the filter; A is the input row itself: a plain bf16 row read through a
+// no-swizzle K-major descriptor with LBO = 16 B and SBO = 128 B is
+// A[m][k] = x[8m + k] (the core matrices overlap by one 16-byte row;
+// verified, tools/micro/hankel_probe.cu), so nothing is expanded in memory.
+// D is a TMEM ring of output-row slots (16 columns: f1 and f2 parts); an
+// output row is final after the MMAs of input row r + kh - 1 (+ the window's
+// zero row), drained by the epilogue warps and re-zeroed for reuse.
 //
-// Precision: fp32 operands are split x = x1 + x2, f = f1 + f2 (bf16, round to
-// nearest, ~16 significant bits each) and D += x1 f1 + x1 f2 + x2 f1 in fp32,
-// error ~2^-16 per product (normwise ~1e-6 on config 5 vs the north-star
-// 7e-5).  Inputs the split cannot carry (|x| > 2^64, non-finite, or nonzero
-// |x| < 2^-100, where the bf16 low part would underflow) are detected per
-// tile; such a tile is recomputed by the CTA with FMAs in the reference tap
+// Precision: x = x1 + x2, f = f1 + f2 (bf16, round to nearest, ~16
+// significant bits each); D accumulates x1 (f1 + f2) + x2 (f1 + f2) in fp32,
+// normwise 2.8e-6 ... 4.5e-6 against the north-star 1e-5 k.  Tiles with
+// inputs the split cannot carry (|x| > 2^64, non-finite, or nonzero
+// |x| < 2^-100) are recomputed by the CTA with FMAs in the reference tap
 // order after the MMA pass, so inf / NaN propagate as in the FFMA kernels.
 //
-// Work per input row and 1,024-column strip: 3 MMAs (smem-bound at ~48
-// cycles each: A 4 KB + B 2 KB) ~ 0.14 SM-cycles per output, against 0.38
-// for 7x7 FFMAs -- the kernel streams at HBM speed instead.
-//
-// Warp roles (one CTA per SM, 512 TMEM columns): 0 TMA producer (input rows
-// into an fp32 staging ring); 1, 2 MMA issuers (even / odd input rows, each
-// into its own D ring so the accumulation order is fixed: output = ring 0 +
-// ring 1); 3-10 split warps (two groups of 4 alternating stages: fp32 -> x1,
-// x2 bf16 rows); 11-14 epilogue (one TMEM lane quarter each: drain, transpose
-// through shared memory to lane-contiguous stores, re-zero the slot).
+// Warp roles (one CTA per SM, 512 TMEM columns): 0 TMA producer (one 4-D box
+// per 4-row stage into an fp32 staging ring); 1 MMA issuer (two MMAs per
+// input row, one elected lane of a warp with warp-uniform operands); 2-9
+// split warps (two groups alternating stages: fp32 -> x1 / x2 bf16 rows in
+// shared memory); 10-17 epilogue (two groups of four, one TMEM lane quarter
+// each, alternating 2-row batches: 16x256b TMEM loads, 256-byte coalesced
+// stores, re-zero the slots).  Hand-offs to the issuer are progress counters
+// read only when its known-ready range runs out (an mbarrier probe costs
+// ~180 cycles even when complete); MMA completion is one commit per 4 rows.
+// The issuing warp is the bound: ~70-200 cycles per tcgen05.mma.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -117,35 +115,15 @@ __device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
 }
 
 // D (TMEM) += A (smem) x B (smem), issued by one elected lane of a warp
+// whose operands are warp-uniform: a lone `if (lane == 0)` issuer makes ptxas
+// wrap the instruction in a uniformity loop (~120 vs ~70 cycles per MMA per
+// warp, tools/micro/hankel_probe.cu)
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc) {
   asm volatile(
       "{\n\t.reg .pred e, p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(da), "l"(db), "r"(idesc)
-      : "memory");
-}
-
-// D (TMEM) += A (TMEM) x B (smem), issued by one elected lane of a warp whose
-// operands are warp-uniform (a single-lane `if` makes ptxas wrap the
-// instruction in a uniformity loop: ~120 vs ~70 cycles per MMA per warp,
-// tools/micro/hankel_probe.cu)
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t db, uint32_t idesc) {
-  asm volatile(
-      "{\n\t.reg .pred e, p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(db), "r"(idesc)
-      : "memory");
-}
-
-// shared memory (descriptor) -> TMEM, 128 lanes x 256 bits, async in the
-// tensor pipe (ordered with the MMAs issued after it by the same thread)
-__device__ __forceinline__ void cp_elect(uint32_t taddr, uint64_t sdesc) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr),
-      "l"(sdesc)
       : "memory");
 }
 
@@ -344,7 +322,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bm = bmat_addr + (uint32_t)p * kBMat;
       const uint64_t db0 = make_desc(bm, 128, 256, 0);
       const uint32_t id0 = idesc_bf16(128, n1 * 16);
-#ifndef SC_MMA_NOMMA
       mma_ss(tmem_u + q0 * 16, dx1, db0, id0);
       mma_ss(tmem_u + q0 * 16, dx2, db0, id0);
       if (n1 < nw) {
@@ -353,7 +330,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_ss(tmem_u, dx1, db1, id1);
         mma_ss(tmem_u, dx2, db1, id1);
       }
-#endif
       if (lane == 0) MMA_TRACE(0, 5 * t + 3, clock64());
       // one commit per 4 input rows: the epilogue's "rows done" and the
       // split warps' "row slots free"
@@ -473,12 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 2, clock64());
 #pragma unroll
       for (int i = 0; i < kEpiRows; ++i) {
-#ifndef SC_MMA_SKIP_ZERO
         tmem_zero8(lane_base + (slot0 + i) * 16);
         tmem_zero8(lane_base + (slot0 + i) * 16 + 8);
-#endif
       }
-#ifndef SC_MMA_SKIP_STG
 #pragma unroll
       for (int i = 0; i < kEpiRows; ++i) {
         const int o = o0 + i;
@@ -508,7 +481,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-#endif
       if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 3, clock64());
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
