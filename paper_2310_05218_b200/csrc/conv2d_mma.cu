@@ -153,14 +153,22 @@ __device__ long long g_mma_trace[8][4096];
 // Plain shared-memory counters for the hand-offs on the issuer's critical
 // path: an mbarrier probe costs ~180 cycles of latency even when the phase
 // is complete, an acquire load ~30.
-__device__ __forceinline__ void smem_add_release(int* p, int v) {
-  asm volatile("red.release.cta.shared::cta.add.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v)
-               : "memory");
+__device__ __forceinline__ void smem_st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
-__device__ __forceinline__ int smem_ld_acquire(const int* p) {
+// least progress over the four warps of a group: four independent relaxed
+// loads (an acquire load orders everything after it, so four of them would
+// serialise); the caller follows a probe with fence_acquire()
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  asm volatile("ld.relaxed.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
   return v;
+}
+__device__ __forceinline__ int min_progress(const int (&c)[4]) {
+  return min(min(ld_relaxed(&c[0]), ld_relaxed(&c[1])), min(ld_relaxed(&c[2]), ld_relaxed(&c[3])));
+}
+__device__ __forceinline__ void fence_acquire() {
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
 }
 
 // 2^64 / 2^-100 as float bit patterns (magnitudes the bf16 split carries)
@@ -194,10 +202,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const float* __restrict__ xg, const __grid_constant__ MmaArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t st_full[kStages], st_empty[kStages];
-  // progress counters (release / acquire), one per split group (+4 per
-  // stage) and per epilogue half (+4 per batch): the issuer reads them only
-  // when it runs out of known-ready rows
-  __shared__ int split_cnt[2], epi_cnt[2];
+  // progress counters (release / acquire), one per warp: stages completed by
+  // each split warp of a group, batches drained by each epilogue warp of a
+  // half.  The issuer reads them only when it runs out of known-ready rows
+  // and takes the minimum over a group's warps (the warps of a group drift
+  // apart by up to the staging depth, so a sum would over-count).
+  __shared__ int split_cnt[2][4], epi_cnt[2][4];
   __shared__ __align__(8) uint64_t done[kDone];         // MMA completion, one per 4 input rows
   __shared__ __align__(8) uint64_t ring_ready;
   __shared__ uint32_t tmem_base_sh;
@@ -239,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&st_full[s], 1);
       mbar_init(&st_empty[s], 4);
     }
-    split_cnt[0] = split_cnt[1] = epi_cnt[0] = epi_cnt[1] = 0;
+    for (int i = 0; i < 8; ++i) (&split_cnt[0][0])[i] = (&epi_cnt[0][0])[i] = 0;
     for (int s = 0; s < kDone; ++s) mbar_init(&done[s], 1);
     mbar_init(&ring_ready, 4);
     fence_mbar_init();
@@ -294,10 +304,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     int drained = o_first;                  // output rows [o_first, drained) drained + zeroed
     for (int t = 0; t < t_rows; ++t) {
       if (lane == 0) MMA_TRACE(0, 5 * t, clock64());
-      while (t >= rows_ready) {
-        // stage s (rows 2s, 2s + 1) belongs to split group s % 2
-        const int c0s = smem_ld_acquire(&split_cnt[0]) >> 2, c1s = smem_ld_acquire(&split_cnt[1]) >> 2;
+      if (t >= rows_ready) {
+        // rows [0, t) are ready, so t = rows_ready starts stage S: wait for
+        // each warp of its group (one word per spin), then take everything
+        // the counters show.  Stage s (rows kRS s ..) belongs to group s % 2.
+        const int S = t / kRS;
+        for (int i = 0; i < 4; ++i)
+          while (ld_relaxed(&split_cnt[S & 1][i]) <= (S >> 1)) {
+          }
+        const int c0s = min_progress(split_cnt[0]), c1s = min_progress(split_cnt[1]);
         rows_ready = min(2 * c0s, 2 * c1s + 1) * kRS;        // stages [0, min(2 c0, 2 c1 + 1)) done
+        fence_acquire();
       }
       if (lane == 0) MMA_TRACE(0, 5 * t + 1, clock64());
       int a, p;
@@ -306,10 +323,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       // must be drained and zeroed
       if (a + nw > hi) {
         const int need = a + nw - kRing;     // rows < need must be drained
-        while (drained < need) {
-          // batch b (rows o_first + 2b, + 1) belongs to epilogue half b % 2
-          const int b0 = smem_ld_acquire(&epi_cnt[0]) >> 2, b1 = smem_ld_acquire(&epi_cnt[1]) >> 2;
+        if (drained < need) {
+          // batches [0, nb) must be drained; batch b (rows o_first + kEpiRows b
+          // ..) belongs to epilogue half b % 2
+          const int nb = (need - o_first + kEpiRows - 1) / kEpiRows;
+          for (int i = 0; i < 4; ++i) {
+            while (ld_relaxed(&epi_cnt[0][i]) < (nb + 1) / 2) {
+            }
+            while (ld_relaxed(&epi_cnt[1][i]) < nb / 2) {
+            }
+          }
+          const int b0 = min_progress(epi_cnt[0]), b1 = min_progress(epi_cnt[1]);
           drained = o_first + min(2 * b0, 2 * b1 + 1) * kEpiRows;
+          fence_acquire();
         }
         hi = a + nw;
       }
@@ -345,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grp = (warp - kWarpSplit0) >> 2;
     const int u = threadIdx.x - 32 * (kWarpSplit0 + 4 * grp);   // 0..127
     uint32_t mx = 0, mn = 0xffffffffu;
+    int stages_done = 0;                                  // published in split_cnt
     const int own = 32 * u;
     for (int s = grp, t0 = grp * kRS; t0 < t_rows; s += 2, t0 += 2 * kRS) {
       const int st = s % kStages;
@@ -386,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&st_empty[st]);
-        smem_add_release(&split_cnt[grp], 1);
+        smem_st_release(&split_cnt[grp][warp & 3], ++stages_done);
       }
     }
     bad = mx > kHiBits || mn < kLoBits - 1u;
@@ -424,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (; groups_done <= (t >> 2); ++groups_done)
         mbar_wait_sleep(&done[groups_done % kDone], (groups_done / kDone) & 1, 32, 128);
     };
+    int batches_done = 0;                                 // published in epi_cnt
     for (int o0 = o_first + half * kEpiRows; o0 < s_valid; o0 += 2 * kEpiRows) {
       const int nr = min(kEpiRows, s_valid - o0);
       // every MMA touching rows < o0 + nr has t <= o0 + nr - 1 + kh (the
@@ -485,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) smem_add_release(&epi_cnt[half], 1);
+      if (lane == 0) smem_st_release(&epi_cnt[half][warp & 3], ++batches_done);
       if (warp == kWarpEpi0 && lane == 0) MMA_TRACE(4, 5 * bi + 4, clock64());
     }
   }

@@ -1,5 +1,6 @@
 // Event trace of the slide-MMA conv kernel, CTA (0,0,0): per role the
 // clock64 stamps recorded under -DSC_MMA_TRACE (see csrc/conv2d_mma.cu).
+//   ./mma_trace [h] [w] [random 0/1]
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++20 -DSC_MMA_TRACE \
 //   -I../../include tools/micro/mma_trace.cu paper_.../csrc/abi.cu -lcuda -o mma_trace
 #include <cstdio>
@@ -22,12 +23,21 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 }  // namespace sc
 
+__global__ void fill_uniform(float* x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ (uint32_t)(i >> 32);
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    x[i] = (h >> 8) * (2.0f / 16777216.0f) - 1.0f;
+  }
+}
+
 int main(int argc, char** argv) {
   const int64_t h = argc > 1 ? atoll(argv[1]) : 8192, w = argc > 2 ? atoll(argv[2]) : 65536;
   float *x, *y;
   cudaMalloc(&x, h * w * 4);
   cudaMalloc(&y, h * w * 4);
   cudaMemset(x, 0, h * w * 4);
+  if (argc > 3 && atoi(argv[3])) fill_uniform<<<1184, 256>>>(x, h * w);
   float f[49];
   for (int i = 0; i < 49; ++i) f[i] = 0.01f * (i + 1);
   for (int it = 0; it < 3; ++it) {
