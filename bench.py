@@ -16,7 +16,7 @@ last so the driver's stdout tail keeps it; the long form goes to stderr).
 N > 1 (`--gpus N` re-launches itself under torch.distributed.run when
 WORLD_SIZE is unset) adds `rowband_cfg5` (config 5 in G row bands with the
 NCCL halo, efficiency E(G) = T(1) / (G T(G)) with T(1) the whole image on one
-GPU in the same run) and `sharded` (configs 1-3 split across the ranks, no
+GPU in the same run) and `sharded` (configs 1-4 split across the ranks, no
 collective, same efficiency).  `--dry-run` exercises the multi-rank plumbing
 (launch, barriers, max-over-ranks, the real halo exchange over gloo) on CPU
 with no kernels -- a CI check, not a measurement.  Rank 0 prints ONE JSON line.
@@ -511,7 +511,7 @@ def rowband_bench(torch, sc, rank, world, hbm_peak, reps=10):
 
 
 def sharded_bench(torch, sc, rank, world, hbm_peak, reps=10):
-    """Configs 1-3 with the BASELINE batch split across the ranks (no
+    """Configs 1-4 with the BASELINE batch split across the ranks (no
     collective): T(G) max over ranks vs T(1) = the whole batch on rank 0 in
     this run; E(G) = T(1) / (G T(G))."""
     import torch.distributed as dist
@@ -535,6 +535,13 @@ def sharded_bench(torch, sc, rank, world, hbm_peak, reps=10):
                             lambda x: sc.conv2d_custom5(x, f3[5], vm),
                             lambda n: 4 * (n * 4096 * 4096 + n * 4092 * 4092 + 25)),
     }
+    # config 4: the N = 16 images split across the ranks, same weights on every
+    # rank (inputs < L2: T(1) and T(G) are both back-to-back, L2-warm means)
+    w4 = torch.from_numpy((np.random.default_rng([0x5EED, 4]).standard_normal((64, 64, 3, 3), dtype=np.float32)
+                           / np.float32(24)).astype(np.float32)).to(dev)
+    cases["cfg4_nchw_3x3"] = (16, lambda n: torch.randn((n, 64, 112, 112), generator=gen, device=dev),
+                              lambda x: sc.conv2d_nchw(x, w4, 1),
+                              lambda n: 4 * (2 * n * 64 * 112 * 112 + 64 * 64 * 9))
     out = {}
     for name, (units, make, run, nbytes) in cases.items():
         gen.manual_seed(sum(map(ord, name)) + rank)
