@@ -32,6 +32,9 @@ int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k
                 cudaStream_t st);
 int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st);
+int pool1d_exact_sum_part(int op, const float* x, int64_t batch, int64_t length, int k_small,
+                          int64_t k_total, const float* fold, int64_t fold_pitch, int64_t shift,
+                          float* y, int64_t y_pitch, cudaStream_t st);
 int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st);
 namespace {
@@ -443,6 +446,94 @@ int launch_passes(const float* x, int64_t batch, int64_t length, int64_t k, floa
   return SC_OK;
 }
 
+// Exact sums / averages for k > 512 on aligned signals (length % 32 == 0):
+// the reference's arithmetic (pooling.py:37-51) regrouped by who computes
+// which partial, every addition the same.  W = the largest power of two
+// <= k.  P_512 at every position comes from the tile kernel (one pass over
+// x); P_1024 .. P_W are global doubling passes P_2w(i) = P_w(i) + P_w(i + w)
+// (the partials of set bits in [512, W) are kept); the fold
+// acc = P_W(i) + P_b(i + width) ... runs over those kept partials, and the
+// set bits below 512 are folded in by the tile kernel, which recomputes
+// their partials from x and reads acc from global memory.  For k = 1,000
+// that is 2 launches instead of 14 global passes.
+template <int kOp>
+int launch_exact_big(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
+                     cudaStream_t st) {
+  static const bool off = getenv("SC_POOL_NO_EXACT_BLOCK") != nullptr;
+  if (off || k <= 512 || length % 32 != 0 || length < 1024 ||
+      reinterpret_cast<uintptr_t>(x) % 16 != 0 || length / 32 > 0x7fffffff || batch > 0x7fffffff)
+    return 1;
+  const int64_t n = length, out_len = n - k + 1;
+  const float div = (kOp == SC_POOL_AVG) ? (float)k : 0.0f;
+  const int lgw = 63 - __builtin_clzll((unsigned long long)k);
+  const int64_t W = 1LL << lgw;
+  const int k_small = (int)(k & 511);
+  // buffers: two for the doubling chain + one per kept partial (set bits in
+  // [512, W)), all of pitch n
+  int kept = 0;
+  for (int64_t b = 512; b < W; b <<= 1) kept += (k & b) ? 1 : 0;
+  const int nbuf = 2 + kept;
+  float* scratch = nullptr;
+  SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&scratch), (size_t)batch * n * sizeof(float) * nbuf,
+                        st));
+  auto buf = [&](int i) { return scratch + (size_t)i * batch * n; };
+  int free_next = 2;
+  float* parts[64] = {nullptr};
+  int rc = pool1d_exact_sum_part(SC_POOL_SUM, x, batch, n, 512, 512, nullptr, 0, 0, buf(0), n, st);
+  if (rc != SC_OK) {
+    cudaFreeAsync(scratch, st);
+    return rc;
+  }
+  float* cur = buf(0);
+  int spare = 1;  // index of the free chain buffer
+  int64_t cur_len = n - 511;
+  for (int64_t w = 512; w < W; w <<= 1) {
+    float* dst;
+    if (k & w) {  // keep P_w: the chain continues in a fresh buffer
+      parts[__builtin_ctzll((unsigned long long)w)] = cur;
+      dst = buf(free_next < nbuf ? free_next++ : spare);
+    } else {
+      dst = buf(spare);
+    }
+    // P_2w from P_w; the last level writes y directly when nothing follows
+    const bool last = (2 * w == W) && k == W;
+    pool_pass_kernel<kOp><<<pass_grid(batch * (cur_len - w)), 256, 0, st>>>(
+        cur, n, cur, n, w, last ? y : dst, last ? out_len : n, batch, cur_len - w,
+        last ? div : 0.0f);
+    SC_LAUNCH_CHECK("pool_pass_kernel");
+    if (last) {
+      SC_CUDA(cudaFreeAsync(scratch, st));
+      return SC_OK;
+    }
+    if (!(k & w)) spare = (int)((cur - scratch) / ((size_t)batch * n));
+    cur = dst;
+    cur_len -= w;
+  }
+  // the set bits in [512, W), largest first: acc = acc + P_b(i + width)
+  int64_t width = W;
+  for (int64_t b = W >> 1; b >= 512; b >>= 1) {
+    if (!(k & b)) continue;
+    const int64_t m = n - (width + b) + 1;
+    const bool last = k_small == 0 && (k & (b - 1)) == 0;
+    float* dst = last ? y : buf(spare);
+    pool_pass_kernel<kOp><<<pass_grid(batch * m), 256, 0, st>>>(
+        cur, n, parts[__builtin_ctzll((unsigned long long)b)], n, width, dst, last ? out_len : n,
+        batch, m, last ? div : 0.0f);
+    SC_LAUNCH_CHECK("pool_pass_kernel");
+    width += b;
+    if (last) {
+      SC_CUDA(cudaFreeAsync(scratch, st));
+      return SC_OK;
+    }
+    spare = (int)((cur - scratch) / ((size_t)batch * n));
+    cur = dst;
+  }
+  // the set bits below 512, in the tile kernel
+  rc = pool1d_exact_sum_part(kOp, x, batch, n, k_small, k, cur, n, width, y, out_len, st);
+  SC_CUDA(cudaFreeAsync(scratch, st));
+  return rc;
+}
+
 template <int kOp>
 int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode, float* y,
              cudaStream_t st) {
@@ -499,6 +590,10 @@ int dispatch(const float* x, int64_t batch, int64_t length, int64_t k, int mode,
     if (k == 64) return launch_reg<kOp, 16, 2, 64>(x, batch, length, 64, y, st);
     if (k == 128) return launch_reg<kOp, 32, 4, 128>(x, batch, length, 128, y, st);
     if (k == 256) return launch_reg<kOp, 32, 8, 256>(x, batch, length, 256, y, st);
+    {
+      const int rc = launch_exact_big<kOp>(x, batch, length, k, y, st);
+      if (rc != 1) return rc;
+    }
     return launch_passes<kOp>(x, batch, length, k, y, st);
   }
   if (k <= 8192) return launch_prefix<kOp>(x, batch, length, (int)k, y, st);

@@ -91,7 +91,9 @@ template <int B, int kOp>
 __global__ void __launch_bounds__(32 * kWarps, 2)
     pool_exact_sum_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
-                          int tiles_per_cta, int k, int64_t flat_L) {
+                          int tiles_per_cta, int k, int64_t flat_L, int64_t y_pitch,
+                          const float* __restrict__ acc_in, int64_t acc_pitch, int64_t shift,
+                          float fk) {
   using G = XGeo<B>;
   constexpr int V = G::V;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     const unsigned row = t / tpr;
     const int64_t s0 = (int64_t)(t - row * tpr) * (kWarps * V);  // 64-bit: flat batches exceed 2^32 samples
     mbar_arrive_expect_tx(&full_bar[b], G::kRows * 128);
-    tma_load_3d(base + b * G::kBuf, &tmap, &full_bar[b], 0, (int)(s0 / 32), (int)row);
+    tma_load_3d(base + b * G::kBuf, &tmap, &full_bar[b], 0, (int)((s0 + shift) / 32), (int)row);
   };
   if (tid == 0) {
     prefetch_tmap(&tmap);
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
   const int kw = 1 << (31 - __clz(k));     // W: the largest power of two <= k
   const int low = k & (kw - 1);            // the set bits below W
   const int bit1 = low ? 1 << (31 - __clz(low)) : 0;  // the largest of them
-  const float fk = (float)k, rk = 1.0f / fk;
+  const float rk = 1.0f / fk;
   const int row0 = (warp * V) / 32 + lane;  // this lane's 128-byte row in the tile
   float* stage = stage_all + warp * G::kStage;
   float* wrow = stage + lane * kPitch;
@@ -133,53 +135,80 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
     const int b = it % kNbuf;
     mbar_wait(&full_bar[b], (it / kNbuf) & 1);
     const unsigned char* rowp = base + b * G::kBuf + row0 * 128;
+    const unsigned row = t / tpr;
+    const int64_t o_in_row = (int64_t)(t - row * tpr) * (kWarps * V) + warp * V;
+    const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
     float c[kT];
-    // The largest lower set bit's partial is captured on the way up to P_W
-    // (kept lane-striped in registers, at its fold offset kw): one partial
-    // fewer to recompute (k = 255: 22 doubling levels instead of 28).
-    float cap[G::kOutLanes];
-    load_lane_row(rowp, row0 & 7, c);
-    if (bit1) {
-      doubling<B>(c, bit1);
-#pragma unroll
-      for (int r = 0; r < kT; ++r) wrow[r] = c[r];
-      __syncwarp();
-      const int ld = lane + kw;
-      const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
-#pragma unroll
-      for (int mm = 0; mm < G::kOutLanes; ++mm) cap[mm] = sq[kPitch * mm];
-      __syncwarp();
-      doubling<B>(c, kw, bit1);
-    } else {
-      doubling<B>(c, kw);
-    }
-    // acc = P_W(i), i = 32 mm + lane (lane-striped)
-#pragma unroll
-    for (int r = 0; r < kT; ++r) wrow[r] = c[r];
-    __syncwarp();
     float acc[G::kOutLanes];
+    if (acc_in) {
+      // fold mode (windows > 512, pool1d.cu): acc = the caller's partial sum
+      // of the leading bits at i, and the tile starts `shift` samples later;
+      // fold every set bit of k (< B) in, largest first, width from 0
+      const float* ar = acc_in + (int64_t)row * acc_pitch + o_in_row + lane;
 #pragma unroll
-    for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = stage[kPitch * mm + lane];
-    int width = kw;
-    if (bit1) {
+      for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = 32 * mm + lane < lim ? ar[32 * mm] : 0.0f;
+      int width = 0;
+      for (int bit = kw; bit; bit >>= 1) {
+        if (!(k & bit)) continue;
+        load_lane_row(rowp, row0 & 7, c);
+        doubling<B>(c, bit);
+        __syncwarp();
 #pragma unroll
-      for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], cap[mm]);
-      width += bit1;
-    }
-    // the other set bits, largest first: acc = acc + P_bit(i + width)
-    for (int bit = (bit1 ? bit1 : kw) >> 1; bit; bit >>= 1) {
-      if (!(k & bit)) continue;
+        for (int r = 0; r < kT; ++r) wrow[r] = c[r];
+        __syncwarp();
+        const int ld = lane + width;
+        const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], sq[kPitch * mm]);
+        width += bit;
+      }
+    } else {
+      // The largest lower set bit's partial is captured on the way up to P_W
+      // (kept lane-striped in registers, at its fold offset kw): one partial
+      // fewer to recompute (k = 255: 22 doubling levels instead of 28).
+      float cap[G::kOutLanes];
       load_lane_row(rowp, row0 & 7, c);
-      doubling<B>(c, bit);
-      __syncwarp();  // everyone done reading the previous partial
+      if (bit1) {
+        doubling<B>(c, bit1);
+#pragma unroll
+        for (int r = 0; r < kT; ++r) wrow[r] = c[r];
+        __syncwarp();
+        const int ld = lane + kw;
+        const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm) cap[mm] = sq[kPitch * mm];
+        __syncwarp();
+        doubling<B>(c, kw, bit1);
+      } else {
+        doubling<B>(c, kw);
+      }
+      // acc = P_W(i), i = 32 mm + lane (lane-striped)
 #pragma unroll
       for (int r = 0; r < kT; ++r) wrow[r] = c[r];
       __syncwarp();
-      const int ld = lane + width;
-      const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
 #pragma unroll
-      for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], sq[kPitch * mm]);
-      width += bit;
+      for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = stage[kPitch * mm + lane];
+      int width = kw;
+      if (bit1) {
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], cap[mm]);
+        width += bit1;
+      }
+      // the other set bits, largest first: acc = acc + P_bit(i + width)
+      for (int bit = (bit1 ? bit1 : kw) >> 1; bit; bit >>= 1) {
+        if (!(k & bit)) continue;
+        load_lane_row(rowp, row0 & 7, c);
+        doubling<B>(c, bit);
+        __syncwarp();  // everyone done reading the previous partial
+#pragma unroll
+        for (int r = 0; r < kT; ++r) wrow[r] = c[r];
+        __syncwarp();
+        const int ld = lane + width;
+        const float* sq = stage + (ld >> 5) * kPitch + (ld & 31);
+#pragma unroll
+        for (int mm = 0; mm < G::kOutLanes; ++mm) acc[mm] = __fadd_rn(acc[mm], sq[kPitch * mm]);
+        width += bit;
+      }
     }
     __syncwarp();
     if (lane == 0) {  // done with slot b: the last warp refills it
@@ -193,10 +222,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
       }
     }
     if constexpr (kOp == SC_POOL_AVG) div_all_by_k<G::kOutLanes>(acc, fk, rk);
-    const unsigned row = t / tpr;
-    const int64_t o_in_row = (int64_t)(t - row * tpr) * (kWarps * V) + warp * V;
-    const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
-    float* yr = y + (int64_t)row * out_len + o_in_row + lane;
+    float* yr = y + (int64_t)row * y_pitch + o_in_row + lane;
     if (flat_L) {
       // flat-batch mode (signal length not a multiple of 32, as in
       // pool_block.cu): warps inside one signal's kept range store from a
@@ -229,7 +255,8 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
 
 template <int B, int kOp>
 int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st,
-           int64_t flat_L) {
+           int64_t flat_L, int64_t out_len, int64_t y_pitch, const float* acc_in,
+           int64_t acc_pitch, int64_t shift, float fk) {
   using G = XGeo<B>;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -242,7 +269,6 @@ int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaS
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(SC_ERR_CUDA, "pool exact tensor map encode failed");
-  const int64_t out_len = length - k + 1;
   const int64_t tiles_per_row = (out_len + kWarps * G::V - 1) / (kWarps * G::V);
   const int64_t n_tiles = tiles_per_row * batch;
   if (n_tiles >= 0x7fffffff) return 1;
@@ -252,18 +278,23 @@ int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaS
   const int tpc = 8;  // contiguous tiles per CTA
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   pool_exact_sum_kernel<B, kOp><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, k, flat_L);
+      map, y, out_len, tiles_per_row, n_tiles, tpc, k, flat_L, y_pitch, acc_in, acc_pitch, shift, fk);
   SC_LAUNCH_CHECK("pool_exact_sum_kernel");
   return SC_OK;
 }
 
 template <int kOp>
 int dispatch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st,
-             int64_t flat_L) {
-  if (k <= 64) return launch<64, kOp>(x, batch, length, k, y, st, flat_L);
-  if (k <= 128) return launch<128, kOp>(x, batch, length, k, y, st, flat_L);
-  if (k <= 256) return launch<256, kOp>(x, batch, length, k, y, st, flat_L);
-  return launch<512, kOp>(x, batch, length, k, y, st, flat_L);
+             int64_t flat_L, int64_t out_len, int64_t y_pitch, const float* acc_in,
+             int64_t acc_pitch, int64_t shift, float fk) {
+#define SC_EXACT_LAUNCH(B)                                                                   \
+  launch<B, kOp>(x, batch, length, k, y, st, flat_L, out_len, y_pitch, acc_in, acc_pitch, shift, \
+                 fk)
+  if (k <= 64) return SC_EXACT_LAUNCH(64);
+  if (k <= 128) return SC_EXACT_LAUNCH(128);
+  if (k <= 256) return SC_EXACT_LAUNCH(256);
+  return SC_EXACT_LAUNCH(512);
+#undef SC_EXACT_LAUNCH
 }
 
 }  // namespace
@@ -286,8 +317,40 @@ int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int6
     batch = 1;
   }
   if (length / 32 > 0x7fffffff) return 1;
-  return op == SC_POOL_SUM ? dispatch<SC_POOL_SUM>(x, batch, length, (int)k, y, st, flat_L)
-                           : dispatch<SC_POOL_AVG>(x, batch, length, (int)k, y, st, flat_L);
+  const int64_t out_len = length - k + 1;
+  return op == SC_POOL_SUM
+             ? dispatch<SC_POOL_SUM>(x, batch, length, (int)k, y, st, flat_L, out_len, out_len,
+                                     nullptr, 0, 0, (float)k)
+             : dispatch<SC_POOL_AVG>(x, batch, length, (int)k, y, st, flat_L, out_len, out_len,
+                                     nullptr, 0, 0, (float)k);
+}
+
+// Building blocks of the exact sums for k > 512 (pool1d.cu:
+// launch_exact_big), on signals whose length is a multiple of 32 (>= 1,024),
+// 16-byte aligned:
+//  * fold == nullptr: P_512 (the reference's doubling partial of width 512,
+//    pooling.py:37-41) at every position, rows of pitch `y_pitch`;
+//  * fold != nullptr: y(i) = (fold(i) + P_b1(i + shift)) + P_b2(i + shift + b1)
+//    + ... over the set bits b1 > b2 > .. of `k_small` (< 512), the tile
+//    read `shift` samples on (a multiple of 32) -- the low-bit tail of the
+//    reference's left fold (pooling.py:42-51), average divided by `k_total`.
+int pool1d_exact_sum_part(int op, const float* x, int64_t batch, int64_t length, int k_small,
+                          int64_t k_total, const float* fold, int64_t fold_pitch, int64_t shift,
+                          float* y, int64_t y_pitch, cudaStream_t st) {
+  if ((op != SC_POOL_SUM && op != SC_POOL_AVG) || reinterpret_cast<uintptr_t>(x) % 16 != 0 ||
+      length % 32 != 0 || length < kWin || batch > 0x7fffffff || length / 32 > 0x7fffffff ||
+      shift % 32 != 0 || k_small < 1 || k_small > 512 || (fold == nullptr && k_small != 512))
+    return 1;
+  const float fk = (float)k_total;
+  if (fold == nullptr)  // a plain sum: P_512
+    return dispatch<SC_POOL_SUM>(x, batch, length, 512, y, st, 0, length - 511, y_pitch, nullptr,
+                                 0, 0, fk);
+  const int64_t out_len = length - k_total + 1;
+  return op == SC_POOL_SUM
+             ? dispatch<SC_POOL_SUM>(x, batch, length, k_small, y, st, 0, out_len, y_pitch, fold,
+                                     fold_pitch, shift, fk)
+             : dispatch<SC_POOL_AVG>(x, batch, length, k_small, y, st, 0, out_len, y_pitch, fold,
+                                     fold_pitch, shift, fk);
 }
 
 }  // namespace sc

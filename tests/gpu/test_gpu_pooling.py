@@ -104,6 +104,29 @@ def test_exact_sum_block_kernel(k):
         assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32)), (op, k)
 
 
+# pool1d.cu launch_exact_big: exact sums / averages for k > 512 on aligned
+# signals -- P_512 from the tile kernel, global doublings up to W, the kept
+# partials of the bits in [512, W) folded by passes, the bits below 512 by the
+# tile kernel reading the running fold (pooling.py:37-51, every add the same)
+@pytest.mark.parametrize("k", [513, 600, 1000, 1023, 1024, 1025, 1536, 1537, 2048, 2560, 3000,
+                               4095, 4096, 5000, 8191, 12289, 30000])
+def test_exact_sum_wide_windows(k):
+    rng = np.random.default_rng(9500 + k)
+    x = rng.standard_normal((3, 32 * 1500), dtype=np.float32)
+    x[0, 5000] = np.inf
+    x[1, 7000:7003] = np.nan
+    x[2, ::13] = np.float32(1e30)               # large magnitudes: order matters
+    x[2, 1::13] = np.float32(-1e30)
+    xd = torch.from_numpy(x).cuda()
+    for op in ("sum", "avg"):
+        want = O.pool_batched(x, k, op)
+        got = FNS[op](xd, k, exact=True)[0].cpu().numpy()
+        assert got.shape == want.shape
+        assert np.array_equal(np.isnan(got), np.isnan(want)), (op, k)
+        m = ~np.isnan(want)
+        assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32)), (op, k)
+
+
 # signal length not a multiple of 32: the batch viewed as one flat signal
 # (B L % 32 == 0), outputs straddling two signals dropped
 @pytest.mark.parametrize("b,n", [(32, 4001), (64, 1031), (96, 2053), (32, 9001)])
