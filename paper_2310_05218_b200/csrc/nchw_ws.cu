@@ -67,16 +67,27 @@ static_assert(kTmemA + 9 * kMaxCin / 2 <= kTmemCols, "TMEM budget");
 // Optional timeline of every CTA (tools/micro/ws_trace.cu builds this file
 // with -DSC_WS_TRACE): globaltimer stamps per CTA at fixed events.
 #ifdef SC_WS_TRACE
-__device__ unsigned long long g_ws_trace[160][8];
+__device__ unsigned long long g_ws_trace[160][13];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
   return t;
 }
 #define WS_TRACE(ev) g_ws_trace[blockIdx.x][ev] = gtime()
+// global-clock stamps (%globaltimer, ns): conv CTA start / end, pack start
+__device__ unsigned long long g_ws_gt[160][2], g_pack_gt[2];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define WS_GT(ev) g_ws_gt[blockIdx.x][ev] = gtimer()
 #else
 #define WS_TRACE(ev) \
   do {               \
+  } while (0)
+#define WS_GT(ev) \
+  do {            \
   } while (0)
 #endif
 
@@ -92,7 +103,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmh, const uint32_t* __restrict__ apack,
                       float* __restrict__ y, const WsArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  if (threadIdx.x == 0) WS_TRACE(0);
+  if (threadIdx.x == 0) {
+    WS_TRACE(0);
+    WS_GT(0);
+  }
   __shared__ __align__(8) uint64_t stage_full[kStages], stage_empty[kStages];
   __shared__ __align__(8) uint64_t slot_full[kSlots], slot_free[kSlots];
   __shared__ __align__(8) uint64_t d_full[2], d_empty[2];
@@ -160,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // this load needs its result; barrier setup, TMEM allocation and the
     // first input rows overlap it
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp == 2 && lane == 0) WS_TRACE(12);
     if (third == 0) {
       uint32_t z[16];
 #pragma unroll
@@ -211,7 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           unsigned char* dst = stages + st * kStageBytes;
           mbar_arrive_expect_tx(&stage_full[st], bytes);
           // rows -1 and h are outside the image: TMA zero-fills them (padding)
+          if (s == 0) WS_TRACE(10);
           tma_load_4d(dst, &tmx, &stage_full[st], w0, rho, 0, n);
+          if (s == 0) WS_TRACE(11);
           if (left)
             tma_load_4d(dst + kStageBoxBytes, &tmh, &stage_full[st], w0 - kHaloW, rho, 0, n);
           if (right)
@@ -251,6 +268,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int sq = base + rr + dj;
           if (rr == 0 || dj == 2) {
             mbar_wait(&slot_full[sq % kSlots], (sq / kSlots) & 1);
+            if (o == 0 && part == 0 && threadIdx.x % 32 == 0) {
+              if (dj == 0) WS_TRACE(8);
+              if (dj == 2) WS_TRACE(9);
+            }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           }
           // tap column offset di: the window starts at slot pixel 1 + di.
@@ -293,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int rho = r0 - 1; rho <= r0 + nr; ++rho, ++s) {
         const int st = s % kStages, sl = s % kSlots;
         mbar_wait(&stage_full[st], (s / kStages) & 1);
+        if (s == 0 && tid == 0) WS_TRACE(7);
         if (s >= kSlots) mbar_wait(&slot_free[sl], ((s / kSlots) - 1) & 1);
         const unsigned char* src_box = stages + st * kStageBytes;
         unsigned char* xs = slots + sl * kSlotBytes;
@@ -403,7 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x == 0) WS_TRACE(5);
+  if (threadIdx.x == 0) {
+    WS_TRACE(5);
+    WS_GT(1);
+  }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -422,6 +447,9 @@ __global__ void pack_weights_kernel(const float* __restrict__ wt, uint32_t* __re
   // let the dependent conv kernel launch now (it waits for this grid's
   // completion before reading apack)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef SC_WS_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_pack_gt[0] = gtimer();
+#endif
   const int a_cols = 9 * cin / 2;
   const int total = (cout + kCo - 1) / kCo * 128 * a_cols;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
