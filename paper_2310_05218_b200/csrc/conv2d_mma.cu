@@ -3,7 +3,7 @@
 // _accumulate_taps (reference.py:15-23) for filters with kw <= 9 and kh <= 9
 // -- BASELINE config 5 (7x7 on a 65,536^2 image) and 9x9 of the paper's
 // sweep.  SURVEY 8(f)4; measured at parity with the FFMA kernels, see
-// profiles/r02/slide_mma.md for the nine variants and why.
+// profiles/r02/slide_mma.md for the variants and why.
 //
 // Formulation.  Per input row rho and 1,024-column strip, with
 //   M = 128 "lanes" m, each the 8 output columns c0 + 8m + s (s = 0..7),
@@ -28,16 +28,20 @@
 // |x| < 2^-100) are recomputed by the CTA with FMAs in the reference tap
 // order after the MMA pass, so inf / NaN propagate as in the FFMA kernels.
 //
-// Warp roles (one CTA per SM, 512 TMEM columns): 0 TMA producer (one 4-D box
-// per 4-row stage into an fp32 staging ring); 1 MMA issuer (two MMAs per
-// input row, one elected lane of a warp with warp-uniform operands); 2-9
-// split warps (two groups alternating stages: fp32 -> x1 / x2 bf16 rows in
-// shared memory); 10-17 epilogue (two groups of four, one TMEM lane quarter
-// each, alternating 2-row batches: 16x256b TMEM loads, 256-byte coalesced
-// stores, re-zero the slots).  Hand-offs to the issuer are progress counters
-// read only when its known-ready range runs out (an mbarrier probe costs
-// ~180 cycles even when complete); MMA completion is one commit per 4 rows.
-// The issuing warp is the bound: ~70-200 cycles per tcgen05.mma.
+// Warp roles (two CTAs per SM, 256 TMEM columns each; SC_MMA_DUAL=0 builds
+// the one-CTA form with 512 columns and twice the split / epilogue warps):
+// 0 TMA producer (one 4-D box per 4-row stage into an fp32 staging ring);
+// 1 MMA issuer (two MMAs per input row, one elected lane of a warp with
+// warp-uniform operands); 2-5 split warps (fp32 -> x1 / x2 bf16 rows in
+// shared memory); 6-9 epilogue (one TMEM lane quarter each, 2-row batches:
+// 16x256b TMEM loads, 256-byte coalesced stores, re-zero the slots).
+// Hand-offs to the issuer are per-warp progress counters read only when its
+// known-ready range runs out (an mbarrier probe costs ~180 cycles even when
+// complete); MMA completion is one commit per 4 rows.  One issuing warp
+// needs ~570 cycles per input row (~70-200 per tcgen05.mma plus the
+// hand-offs), so the kernel runs two CTAs -- two independent issuers -- per
+// SM: config 5 9.27 -> 7.6 ms, level with the FFMA kernel (7.7 ms; 8.0 vs
+// 7.9 ms under sustained power-capped load).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -56,7 +60,20 @@ using namespace tc;
 
 constexpr int kStrip = 1024;                 // output columns per CTA (128 lanes x 8 shifts)
 constexpr int kRS = 4;                       // input rows per staging stage
-constexpr int kStages = 6;                   // fp32 staging ring (24 rows in flight)
+// SC_MMA_DUAL: two CTAs per SM (two issuing warps per SM, each with its own
+// 256-column TMEM ring and half the shared memory); otherwise one CTA with
+// the whole TMEM
+#ifndef SC_MMA_DUAL
+#define SC_MMA_DUAL 1
+#endif
+constexpr int kCtasPerSm = SC_MMA_DUAL ? 2 : 1;
+#ifndef SC_MMA_STAGES
+#define SC_MMA_STAGES (SC_MMA_DUAL ? 3 : 6)
+#endif
+#ifndef SC_MMA_XSLOTS
+#define SC_MMA_XSLOTS (SC_MMA_DUAL ? 8 : 16)
+#endif
+constexpr int kStages = SC_MMA_STAGES;        // fp32 staging ring (12 / 24 rows in flight)
 // A stage is ONE 4-D TMA box: the image viewed as (256-column chunk, chunk,
 // row, image) with box {256, 4, kRS, 1} lands as kRS rows of 1,024
 // contiguous floats (W % 256 == 0); plus a {8, kRS} box for the 8 columns
@@ -73,20 +90,22 @@ constexpr int kMaxNW = 10;                   // window rows = kh + 1 rounded up 
 constexpr int kBMat = kMaxNW * 16 * 32;      // 5 KiB
 // TMEM (512 columns): one D ring of kRing output-row slots of 16 columns
 // (f1 part | f2 part, 8 shifts each)
-constexpr int kRing = 32;
+constexpr int kRing = SC_MMA_DUAL ? 16 : 32;
+constexpr int kTmemCols = kRing * 16;
 // split bf16 rows (x1 | x2) in shared memory, read by the MMAs (SS form)
 // through the overlapping (Hankel) descriptor
-constexpr int kXSlots = 16;
+constexpr int kXSlots = SC_MMA_XSLOTS;
 constexpr int kXRow = 2176;                  // 1,032 bf16 used, 128-aligned
 constexpr int kXSlotBytes = 2 * kXRow;
-constexpr int kDone = 64;                    // MMA-completion barriers, one per 4 input rows
+constexpr int kDone = SC_MMA_DUAL ? 32 : 64;  // MMA-completion barriers, one per 4 input rows
 constexpr int kEpiRows = 2;                  // output rows drained per epilogue batch
-constexpr int kSplitWarps = 8, kEpiWarps = 8;
+constexpr int kSplitWarps = SC_MMA_DUAL ? 4 : 8, kEpiWarps = SC_MMA_DUAL ? 4 : 8;
+constexpr int kSplitGroups = kSplitWarps / 4, kEpiGroups = kEpiWarps / 4;  // of 4 warps
 constexpr int kWarpSplit0 = 2, kWarpEpi0 = kWarpSplit0 + kSplitWarps;  // 2, 10
-constexpr int kThreads = 32 * (kWarpEpi0 + kEpiWarps);                 // 576
+constexpr int kThreads = 32 * (kWarpEpi0 + kEpiWarps);                 // 576 / 320
 constexpr size_t kSmem =
     1024 + (size_t)kStages * kStageBytes + (size_t)kXSlots * kXSlotBytes + 2 * kBMat;
-static_assert(kRing * 16 == 512, "TMEM budget");
+static_assert(kTmemCols * kCtasPerSm == 512, "TMEM budget");
 static_assert(kRing % kEpiRows == 0, "an epilogue batch never wraps the ring");
 static_assert(kRing >= kMaxNW + kEpiRows + 2, "ring slack");
 static_assert((kMaxKH + 2) / 2 * 2 <= kMaxNW, "window rows");
@@ -196,7 +215,7 @@ __device__ __forceinline__ void range8(const float4 a, const float4 b, uint32_t&
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     conv2d_mma_kernel(const __grid_constant__ CUtensorMap tm_main,
                       const __grid_constant__ CUtensorMap tm_tail, float* __restrict__ y,
                       const float* __restrict__ xg, const __grid_constant__ MmaArgs args) {
@@ -207,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // half.  The issuer reads them only when it runs out of known-ready rows
   // and takes the minimum over a group's warps (the warps of a group drift
   // apart by up to the staging depth, so a sum would over-count).
-  __shared__ int split_cnt[2][4], epi_cnt[2][4];
+  __shared__ int split_cnt[kSplitGroups][4], epi_cnt[kEpiGroups][4];
   __shared__ __align__(8) uint64_t done[kDone];         // MMA completion, one per 4 input rows
   __shared__ __align__(8) uint64_t ring_ready;
   __shared__ uint32_t tmem_base_sh;
@@ -249,14 +268,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&st_full[s], 1);
       mbar_init(&st_empty[s], 4);
     }
-    for (int i = 0; i < 8; ++i) (&split_cnt[0][0])[i] = (&epi_cnt[0][0])[i] = 0;
+    for (int i = 0; i < 4 * kSplitGroups; ++i) (&split_cnt[0][0])[i] = 0;
+    for (int i = 0; i < 4 * kEpiGroups; ++i) (&epi_cnt[0][0])[i] = 0;
     for (int s = 0; s < kDone; ++s) mbar_init(&done[s], 1);
     mbar_init(&ring_ready, 4);
     fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(&tmem_base_sh))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "n"(kTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -310,10 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the counters show.  Stage s (rows kRS s ..) belongs to group s % 2.
         const int S = t / kRS;
         for (int i = 0; i < 4; ++i)
-          while (ld_relaxed(&split_cnt[S & 1][i]) <= (S >> 1)) {
+          while (ld_relaxed(&split_cnt[S % kSplitGroups][i]) <= S / kSplitGroups) {
           }
-        const int c0s = min_progress(split_cnt[0]), c1s = min_progress(split_cnt[1]);
-        rows_ready = min(2 * c0s, 2 * c1s + 1) * kRS;        // stages [0, min(2 c0, 2 c1 + 1)) done
+        // stages [0, min_g(G c_g + g)) done
+        int st_done = kSplitGroups * min_progress(split_cnt[0]);
+        for (int g = 1; g < kSplitGroups; ++g)
+          st_done = min(st_done, kSplitGroups * min_progress(split_cnt[g]) + g);
+        rows_ready = st_done * kRS;
         fence_acquire();
       }
       if (lane == 0) MMA_TRACE(0, 5 * t + 1, clock64());
@@ -327,14 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           // batches [0, nb) must be drained; batch b (rows o_first + kEpiRows b
           // ..) belongs to epilogue half b % 2
           const int nb = (need - o_first + kEpiRows - 1) / kEpiRows;
-          for (int i = 0; i < 4; ++i) {
-            while (ld_relaxed(&epi_cnt[0][i]) < (nb + 1) / 2) {
-            }
-            while (ld_relaxed(&epi_cnt[1][i]) < nb / 2) {
-            }
-          }
-          const int b0 = min_progress(epi_cnt[0]), b1 = min_progress(epi_cnt[1]);
-          drained = o_first + min(2 * b0, 2 * b1 + 1) * kEpiRows;
+          for (int g = 0; g < kEpiGroups; ++g)
+            for (int i = 0; i < 4; ++i)
+              while (ld_relaxed(&epi_cnt[g][i]) < (nb - g + kEpiGroups - 1) / kEpiGroups) {
+              }
+          int b_done = kEpiGroups * min_progress(epi_cnt[0]);
+          for (int g = 1; g < kEpiGroups; ++g)
+            b_done = min(b_done, kEpiGroups * min_progress(epi_cnt[g]) + g);
+          drained = o_first + b_done * kEpiRows;
           fence_acquire();
         }
         hi = a + nw;
@@ -373,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t mx = 0, mn = 0xffffffffu;
     int stages_done = 0;                                  // published in split_cnt
     const int own = 32 * u;
-    for (int s = grp, t0 = grp * kRS; t0 < t_rows; s += 2, t0 += 2 * kRS) {
+    for (int s = grp, t0 = grp * kRS; t0 < t_rows; s += kSplitGroups, t0 += kSplitGroups * kRS) {
       const int st = s % kStages;
       if (warp == kWarpSplit0 + 4 * grp && lane == 0) MMA_TRACE(2, 4 * t0, clock64());
       mbar_spin(&st_full[st], (s / kStages) & 1);
@@ -452,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(&done[groups_done % kDone], (groups_done / kDone) & 1, 32, 128);
     };
     int batches_done = 0;                                 // published in epi_cnt
-    for (int o0 = o_first + half * kEpiRows; o0 < s_valid; o0 += 2 * kEpiRows) {
+    for (int o0 = o_first + half * kEpiRows; o0 < s_valid; o0 += kEpiGroups * kEpiRows) {
       const int nr = min(kEpiRows, s_valid - o0);
       // every MMA touching rows < o0 + nr has t <= o0 + nr - 1 + kh (the
       // window's zero row) and t < t_rows; each issuer commits in order, so
@@ -539,7 +563,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols)
+                 : "memory");
   }
 }
 
@@ -584,7 +609,7 @@ int conv2d_mma(const float* x, int64_t batch, int64_t h, int64_t w, const float*
   const int64_t strips = (ow + kStrip - 1) / kStrip;
   // Row segments: one CTA per SM, every CTA costs ~(rows + kh - 1) input
   // rows; pick the segment length minimising waves x rows (whole waves).
-  const int64_t slots = sm_count();
+  const int64_t slots = (int64_t)kCtasPerSm * sm_count();
   int64_t best = -1, rows = oh;
   const int env_rows = env_int("SC_MMA_ROWS", 0);
   if (env_rows > 0) {
