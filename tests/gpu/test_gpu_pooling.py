@@ -127,6 +127,21 @@ def test_exact_sum_wide_windows(k):
         assert np.array_equal(got[m].view(np.uint32), want[m].view(np.uint32)), (op, k)
 
 
+# edge geometries of the same path: window = signal length (one output),
+# windows just past 512 / a power of two, single signal, odd batch counts
+@pytest.mark.parametrize("b,n,k", [(1, 2048, 2048), (2, 3072, 3000), (5, 1024, 1024), (1, 1056, 513),
+                                   (7, 4096, 4097 - 32), (3, 65536, 65535), (2, 8192, 1536 + 255)])
+def test_exact_sum_wide_windows_edges(b, n, k):
+    rng = np.random.default_rng(b * 100003 + n + k)
+    x = rng.standard_normal((b, n), dtype=np.float32) * np.float32(1e3)
+    xd = torch.from_numpy(x).cuda()
+    for op in ("sum", "avg"):
+        want = O.pool_batched(x, k, op)
+        got = FNS[op](xd, k, exact=True)[0].cpu().numpy()
+        assert got.shape == want.shape == (b, n - k + 1)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (op, b, n, k)
+
+
 # signal length not a multiple of 32: the batch viewed as one flat signal
 # (B L % 32 == 0), outputs straddling two signals dropped
 @pytest.mark.parametrize("b,n", [(32, 4001), (64, 1031), (96, 2053), (32, 9001)])
