@@ -37,11 +37,12 @@ for seed in range(12):
 
 FNS = {"sum": sc.sliding_window_sum, "avg": sc.sliding_window_mean, "max": sc.sliding_window_max}
 while time.time() < t_end:
-    # 2. pooling: random lengths (aligned and ragged), windows 1..600, batch 1..4
+    # 2. pooling: random lengths (aligned and ragged), windows 1..5000, batch 1..4
     aligned = rng.random() < 0.6
     n = int(rng.integers(1024, 40000))
     n = n // 32 * 32 if aligned else n
-    k = int(min(n, rng.choice([rng.integers(1, 34), rng.integers(34, 300), rng.integers(300, 700)])))
+    k = int(min(n, rng.choice([rng.integers(1, 34), rng.integers(34, 300), rng.integers(300, 700),
+                                rng.integers(700, 5000)])))
     b = int(rng.integers(1, 5))
     x = rng.standard_normal((b, n), dtype=np.float32) * np.float32(rng.choice([1e-3, 1.0, 1e3]))
     if rng.random() < 0.2:
