@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     nchw3x3_tc_kernel(const __grid_constant__ CUtensorMap tmx,
                       const __grid_constant__ CUtensorMap tmh,
                       const __grid_constant__ CUtensorMap tmw, float* __restrict__ y, int cin,
-                      int h, int w, int cout, int ntiles) {
+                      int h, int w, int cout, int ntiles, const float* __restrict__ xraw,
+                      const float* __restrict__ wraw) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t a_full[kAStages], a_empty[kAStages];
   // kb_full[s]: B landed (tx) + 8 split warps stored X1/X2; kb_free[s]: both
@@ -189,6 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // inputs the bf16 split cannot carry (inf / NaN, |x| >= 2^127), seen by
+  // the split warps; the CTA's tiles are then recomputed with FMAs at the end
+  uint32_t mag = 0;  // largest |x| bit pattern (2^127, inf, NaN >= 0x7f000000)
 
   if (warp == kAProducer) {
     // ------------------------------------------------ A-box TMA producer
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 4; ++j) {
               const float f0 = *reinterpret_cast<const float*>(src + (2 * j) * stride);
               const float f1 = *reinterpret_cast<const float*>(src + (2 * j + 1) * stride);
+              mag = max(mag, max(__float_as_uint(f0) & 0x7fffffffu, __float_as_uint(f1) & 0x7fffffffu));
               const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
               p1[j] = a1;
               p2[j] = pack_bf16x2(f0 - __uint_as_float(a1 << 16),
@@ -405,7 +410,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (__syncthreads_or(mag >= 0x7f000000u)) {
+    // a non-finite or huge input in one of this CTA's tiles: recompute all of
+    // its tiles with fp32 FMAs (ci, dj, di ascending), overwriting the tensor-
+    // core results (ordered by the barrier), so inf / NaN follow the
+    // reference's pattern instead of the split's NaN.  Never taken on finite
+    // inputs.
+    const int64_t plane = (int64_t)h * w;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const TileCoord tc = tile_coord(t, co_tiles, wtiles, htiles);
+      for (int e = threadIdx.x; e < kN * kM; e += kThreads) {
+        const int co = tc.co0 + e / kM, r = tc.h0 + (e % kM) / kTileW, c = tc.w0 + e % kTileW;
+        if (co >= cout || r >= h || c >= w) continue;
+        const float* xn = xraw + (int64_t)tc.n * cin * plane;
+        const float* wc = wraw + (int64_t)co * cin * 9;
+        float acc = 0.0f;
+        for (int ci = 0; ci < cin; ++ci)
+          for (int dj = 0; dj < 3; ++dj) {
+            const int ri = r + dj - 1;
+            if (ri < 0 || ri >= h) continue;
+            for (int di = 0; di < 3; ++di) {
+              const int cc = c + di - 1;
+              if (cc < 0 || cc >= w) continue;
+              acc = fmaf(wc[ci * 9 + dj * 3 + di], xn[ci * plane + (int64_t)ri * w + cc], acc);
+            }
+          }
+        y[((int64_t)tc.n * cout + co) * plane + (int64_t)r * w + c] = acc;
+      }
+    }
+  }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -487,7 +520,7 @@ int nchw3x3_tc(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
   SC_CUDA(set_smem_limit_once(nchw3x3_tc_kernel, (int)kSmem, &attr));
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, sm_count());
   nchw3x3_tc_kernel<<<grid, kThreads, kSmem, st>>>(mx, mh, mw, y, (int)cin, (int)h, (int)w,
-                                                   (int)cout, (int)ntiles);
+                                                   (int)cout, (int)ntiles, x, wt);
   SC_LAUNCH_CHECK("nchw3x3_tc_kernel");
   SC_CUDA(cudaFreeAsync(wsplit, st));
   return SC_OK;

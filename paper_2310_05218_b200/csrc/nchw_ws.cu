@@ -101,7 +101,8 @@ template <int kKSteps>  // Cin / 16
 __global__ void __launch_bounds__(kThreads, 1)
     nchw3x3_ws_kernel(const __grid_constant__ CUtensorMap tmx,
                       const __grid_constant__ CUtensorMap tmh, const uint32_t* __restrict__ apack,
-                      float* __restrict__ y, const WsArgs args) {
+                      float* __restrict__ y, const WsArgs args, const float* __restrict__ xraw,
+                      const float* __restrict__ wraw) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   if (threadIdx.x == 0) {
     WS_TRACE(0);
@@ -205,6 +206,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   // no CTA-wide barrier here: the producer and split warps start on the
   // first input rows while the A load is in flight; only the issuers wait
+  // inputs the bf16 split cannot carry (inf / NaN, |x| >= 2^127: x - bf16(x)
+  // would be NaN or overflow), seen by the split warps
+  // (tracked as the largest |x| bit pattern: >= 2^127, inf and NaN all
+  // compare above 0x7f000000)
+  uint32_t mag = 0;
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer: input rows
@@ -343,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 4; ++j) {
             const float f0 = *reinterpret_cast<const float*>(src + (2 * j) * stride);
             const float f1 = *reinterpret_cast<const float*>(src + (2 * j + 1) * stride);
+            mag = max(mag, max(__float_as_uint(f0) & 0x7fffffffu, __float_as_uint(f1) & 0x7fffffffu));
             const uint32_t a1 = pack_bf16x2(f0, f1);  // channel 2j in the low half
             p1[j] = a1;
             p2[j] = pack_bf16x2(f0 - __uint_as_float(a1 << 16),
@@ -424,10 +431,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  const int redo = __syncthreads_or(mag >= 0x7f000000u);
   if (threadIdx.x == 0) {
     WS_TRACE(5);
     WS_GT(1);
+  }
+  if (redo) {
+    // a non-finite or huge input in this CTA's rows: recompute its outputs
+    // with fp32 FMAs (ci, dj, di ascending), overwriting the tensor-core
+    // results (the barrier above orders the two sets of global stores), so
+    // inf / NaN come out as the reference's pattern instead of the split's
+    // NaN.  Rare and slow (~0.2 ms per CTA), never taken on finite inputs.
+    const int64_t plane = (int64_t)h * w;
+    for (int it = cta_in_co; it < args.items_per_co; it += args.ctas_per_co) {
+      int n, w0, r0, nr;
+      item_of(it, n, w0, r0, nr);
+      const int cols = min(wt, w - w0);
+      const int64_t total = (int64_t)kCo * nr * cols;
+      for (int64_t e = threadIdx.x; e < total; e += kThreads) {
+        const int cc = (int)(e % cols), rr = (int)((e / cols) % nr), cl = (int)(e / ((int64_t)cols * nr));
+        const int co = co_tile * kCo + cl;
+        if (co >= args.cout) continue;
+        const int r = r0 + rr, c = w0 + cc;
+        const float* xn = xraw + (int64_t)n * cin * plane;
+        const float* wc = wraw + (int64_t)co * cin * 9;
+        float acc = 0.0f;
+        for (int ci = 0; ci < cin; ++ci)
+          for (int dj = 0; dj < 3; ++dj) {
+            const int rin = r + dj - 1;
+            if (rin < 0 || rin >= h) continue;
+            for (int di = 0; di < 3; ++di) {
+              const int cin_c = c + di - 1;
+              if (cin_c < 0 || cin_c >= w) continue;
+              acc = fmaf(wc[ci * 9 + dj * 3 + di], xn[ci * plane + (int64_t)rin * w + cin_c], acc);
+            }
+          }
+        y[((int64_t)n * args.cout + co) * plane + (int64_t)r * w + c] = acc;
+      }
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -561,7 +602,7 @@ int nchw3x3_ws(const float* x, int64_t nb, int64_t cin, int64_t h, int64_t w, co
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    SC_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, (const uint32_t*)apack, y, a));
+    SC_CUDA(cudaLaunchKernelEx(&cfg, kern, mx, mh, (const uint32_t*)apack, y, a, x, wt));
   }
   SC_LAUNCH_CHECK("nchw3x3_ws_kernel");
   SC_CUDA(cudaFreeAsync(apack, st));
