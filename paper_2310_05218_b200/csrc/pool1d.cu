@@ -34,7 +34,7 @@ int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int6
                      cudaStream_t st);
 int pool1d_exact_sum_part(int op, const float* x, int64_t batch, int64_t length, int k_small,
                           int64_t k_total, const float* fold, int64_t fold_pitch, int64_t shift,
-                          float* y, int64_t y_pitch, cudaStream_t st);
+                          float* y, int64_t y_pitch, int64_t flat_L, cudaStream_t st);
 int pool1d_block_max(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st);
 namespace {
@@ -456,13 +456,37 @@ int launch_passes(const float* x, int64_t batch, int64_t length, int64_t k, floa
 // set bits below 512 are folded in by the tile kernel, which recomputes
 // their partials from x and reads acc from global memory.  For k = 1,000
 // that is 2 launches instead of 14 global passes.
+// flat batches (L % 32 != 0, B L % 32 == 0): one signal of B L samples
+// (windows straddling two signals are computed and dropped, as in
+// pool_exact.cu); results the passes would write to y go through
+// flat_compact_kernel instead.
+template <int kOp>
+__global__ void flat_compact_kernel(const float* __restrict__ src, int64_t flat_L, int64_t k,
+                                    int64_t batch, float* __restrict__ y, float scale_div) {
+  const int64_t per = flat_L - k + 1, total = batch * per;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / per, i = e - b * per;
+    float o = src[b * flat_L + i];
+    if (scale_div != 0.0f) o = __fdiv_rn(o, scale_div);
+    y[e] = o;
+  }
+}
+
 template <int kOp>
 int launch_exact_big(const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st) {
   static const bool off = getenv("SC_POOL_NO_EXACT_BLOCK") != nullptr;
-  if (off || k <= 512 || length % 32 != 0 || length < 1024 ||
-      reinterpret_cast<uintptr_t>(x) % 16 != 0 || length / 32 > 0x7fffffff || batch > 0x7fffffff)
+  if (off || k <= 512 || reinterpret_cast<uintptr_t>(x) % 16 != 0 || batch > 0x7fffffff)
     return 1;
+  int64_t flat_L = 0;
+  if (length % 32 != 0) {
+    if ((batch * length) % 32 != 0) return 1;
+    flat_L = length;
+    length *= batch;
+    batch = 1;
+  }
+  if (length < 1024 || length / 32 > 0x7fffffff) return 1;
   const int64_t n = length, out_len = n - k + 1;
   const float div = (kOp == SC_POOL_AVG) ? (float)k : 0.0f;
   const int lgw = 63 - __builtin_clzll((unsigned long long)k);
@@ -479,7 +503,8 @@ int launch_exact_big(const float* x, int64_t batch, int64_t length, int64_t k, f
   auto buf = [&](int i) { return scratch + (size_t)i * batch * n; };
   int free_next = 2;
   float* parts[64] = {nullptr};
-  int rc = pool1d_exact_sum_part(SC_POOL_SUM, x, batch, n, 512, 512, nullptr, 0, 0, buf(0), n, st);
+  int rc =
+      pool1d_exact_sum_part(SC_POOL_SUM, x, batch, n, 512, 512, nullptr, 0, 0, buf(0), n, 0, st);
   if (rc != SC_OK) {
     cudaFreeAsync(scratch, st);
     return rc;
@@ -496,7 +521,7 @@ int launch_exact_big(const float* x, int64_t batch, int64_t length, int64_t k, f
       dst = buf(spare);
     }
     // P_2w from P_w; the last level writes y directly when nothing follows
-    const bool last = (2 * w == W) && k == W;
+    const bool last = (2 * w == W) && k == W && !flat_L;
     pool_pass_kernel<kOp><<<pass_grid(batch * (cur_len - w)), 256, 0, st>>>(
         cur, n, cur, n, w, last ? y : dst, last ? out_len : n, batch, cur_len - w,
         last ? div : 0.0f);
@@ -514,7 +539,7 @@ int launch_exact_big(const float* x, int64_t batch, int64_t length, int64_t k, f
   for (int64_t b = W >> 1; b >= 512; b >>= 1) {
     if (!(k & b)) continue;
     const int64_t m = n - (width + b) + 1;
-    const bool last = k_small == 0 && (k & (b - 1)) == 0;
+    const bool last = k_small == 0 && (k & (b - 1)) == 0 && !flat_L;
     float* dst = last ? y : buf(spare);
     pool_pass_kernel<kOp><<<pass_grid(batch * m), 256, 0, st>>>(
         cur, n, parts[__builtin_ctzll((unsigned long long)b)], n, width, dst, last ? out_len : n,
@@ -528,8 +553,14 @@ int launch_exact_big(const float* x, int64_t batch, int64_t length, int64_t k, f
     spare = (int)((cur - scratch) / ((size_t)batch * n));
     cur = dst;
   }
+  if (k_small == 0) {  // flat batch, k a multiple of 512: compact into y
+    flat_compact_kernel<kOp><<<pass_grid(n), 256, 0, st>>>(cur, flat_L, k, n / flat_L, y, div);
+    SC_LAUNCH_CHECK("flat_compact_kernel");
+    SC_CUDA(cudaFreeAsync(scratch, st));
+    return SC_OK;
+  }
   // the set bits below 512, in the tile kernel
-  rc = pool1d_exact_sum_part(kOp, x, batch, n, k_small, k, cur, n, width, y, out_len, st);
+  rc = pool1d_exact_sum_part(kOp, x, batch, n, k_small, k, cur, n, width, y, out_len, flat_L, st);
   SC_CUDA(cudaFreeAsync(scratch, st));
   return rc;
 }

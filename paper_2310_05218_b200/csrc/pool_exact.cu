@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
                           int64_t out_len, int64_t tiles_per_row, int64_t n_tiles,
                           int tiles_per_cta, int k, int64_t flat_L, int64_t y_pitch,
                           const float* __restrict__ acc_in, int64_t acc_pitch, int64_t shift,
-                          float fk) {
+                          float fk, int k_out) {
   using G = XGeo<B>;
   constexpr int V = G::V;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -228,14 +228,14 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
       // pool_block.cu): warps inside one signal's kept range store from a
       // shifted base, boundary warps element by element
       const int64_t w0 = (int64_t)o_in_row, wb = w0 / flat_L;
-      if (w0 + lim - 1 < wb * flat_L + flat_L - (k - 1)) {
-        yr = y + (w0 - wb * (k - 1)) + lane;
+      if (w0 + lim - 1 < wb * flat_L + flat_L - (k_out - 1)) {
+        yr = y + (w0 - wb * (k_out - 1)) + lane;
       } else {
 #pragma unroll
         for (int mm = 0; mm < G::kOutLanes; ++mm) {
           const int64_t p = w0 + 32 * mm + lane, pb = p / flat_L;
-          if (32 * mm + lane < lim && p - pb * flat_L < flat_L - (k - 1))
-            y[p - pb * (k - 1)] = acc[mm];
+          if (32 * mm + lane < lim && p - pb * flat_L < flat_L - (k_out - 1))
+            y[p - pb * (k_out - 1)] = acc[mm];
         }
         __syncwarp();
         continue;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(32 * kWarps, 2)
 template <int B, int kOp>
 int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st,
            int64_t flat_L, int64_t out_len, int64_t y_pitch, const float* acc_in,
-           int64_t acc_pitch, int64_t shift, float fk) {
+           int64_t acc_pitch, int64_t shift, float fk, int k_out) {
   using G = XGeo<B>;
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -278,7 +278,8 @@ int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaS
   const int tpc = 8;  // contiguous tiles per CTA
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
   pool_exact_sum_kernel<B, kOp><<<(unsigned)grid, 32 * kWarps, smem, st>>>(
-      map, y, out_len, tiles_per_row, n_tiles, tpc, k, flat_L, y_pitch, acc_in, acc_pitch, shift, fk);
+      map, y, out_len, tiles_per_row, n_tiles, tpc, k, flat_L, y_pitch, acc_in, acc_pitch, shift, fk,
+      k_out);
   SC_LAUNCH_CHECK("pool_exact_sum_kernel");
   return SC_OK;
 }
@@ -286,10 +287,10 @@ int launch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaS
 template <int kOp>
 int dispatch(const float* x, int64_t batch, int64_t length, int k, float* y, cudaStream_t st,
              int64_t flat_L, int64_t out_len, int64_t y_pitch, const float* acc_in,
-             int64_t acc_pitch, int64_t shift, float fk) {
+             int64_t acc_pitch, int64_t shift, float fk, int k_out) {
 #define SC_EXACT_LAUNCH(B)                                                                   \
   launch<B, kOp>(x, batch, length, k, y, st, flat_L, out_len, y_pitch, acc_in, acc_pitch, shift, \
-                 fk)
+                 fk, k_out)
   if (k <= 64) return SC_EXACT_LAUNCH(64);
   if (k <= 128) return SC_EXACT_LAUNCH(128);
   if (k <= 256) return SC_EXACT_LAUNCH(256);
@@ -320,9 +321,9 @@ int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int6
   const int64_t out_len = length - k + 1;
   return op == SC_POOL_SUM
              ? dispatch<SC_POOL_SUM>(x, batch, length, (int)k, y, st, flat_L, out_len, out_len,
-                                     nullptr, 0, 0, (float)k)
+                                     nullptr, 0, 0, (float)k, (int)k)
              : dispatch<SC_POOL_AVG>(x, batch, length, (int)k, y, st, flat_L, out_len, out_len,
-                                     nullptr, 0, 0, (float)k);
+                                     nullptr, 0, 0, (float)k, (int)k);
 }
 
 // Building blocks of the exact sums for k > 512 (pool1d.cu:
@@ -333,10 +334,12 @@ int pool1d_exact_sum(int op, const float* x, int64_t batch, int64_t length, int6
 //  * fold != nullptr: y(i) = (fold(i) + P_b1(i + shift)) + P_b2(i + shift + b1)
 //    + ... over the set bits b1 > b2 > .. of `k_small` (< 512), the tile
 //    read `shift` samples on (a multiple of 32) -- the low-bit tail of the
-//    reference's left fold (pooling.py:42-51), average divided by `k_total`.
+//    reference's left fold (pooling.py:42-51), average divided by `k_total`;
+//    flat_L != 0: the batch is one flat signal of signals of flat_L samples,
+//    outputs straddling two signals are dropped (y is [B][flat_L - k_total + 1]).
 int pool1d_exact_sum_part(int op, const float* x, int64_t batch, int64_t length, int k_small,
                           int64_t k_total, const float* fold, int64_t fold_pitch, int64_t shift,
-                          float* y, int64_t y_pitch, cudaStream_t st) {
+                          float* y, int64_t y_pitch, int64_t flat_L, cudaStream_t st) {
   if ((op != SC_POOL_SUM && op != SC_POOL_AVG) || reinterpret_cast<uintptr_t>(x) % 16 != 0 ||
       length % 32 != 0 || length < kWin || batch > 0x7fffffff || length / 32 > 0x7fffffff ||
       shift % 32 != 0 || k_small < 1 || k_small > 512 || (fold == nullptr && k_small != 512))
@@ -344,13 +347,13 @@ int pool1d_exact_sum_part(int op, const float* x, int64_t batch, int64_t length,
   const float fk = (float)k_total;
   if (fold == nullptr)  // a plain sum: P_512
     return dispatch<SC_POOL_SUM>(x, batch, length, 512, y, st, 0, length - 511, y_pitch, nullptr,
-                                 0, 0, fk);
+                                 0, 0, fk, 512);
   const int64_t out_len = length - k_total + 1;
   return op == SC_POOL_SUM
-             ? dispatch<SC_POOL_SUM>(x, batch, length, k_small, y, st, 0, out_len, y_pitch, fold,
-                                     fold_pitch, shift, fk)
-             : dispatch<SC_POOL_AVG>(x, batch, length, k_small, y, st, 0, out_len, y_pitch, fold,
-                                     fold_pitch, shift, fk);
+             ? dispatch<SC_POOL_SUM>(x, batch, length, k_small, y, st, flat_L, out_len, y_pitch, fold,
+                                     fold_pitch, shift, fk, (int)k_total)
+             : dispatch<SC_POOL_AVG>(x, batch, length, k_small, y, st, flat_L, out_len, y_pitch, fold,
+                                     fold_pitch, shift, fk, (int)k_total);
 }
 
 }  // namespace sc

@@ -145,7 +145,8 @@ def test_exact_sum_wide_windows_edges(b, n, k):
 # signal length not a multiple of 32: the batch viewed as one flat signal
 # (B L % 32 == 0), outputs straddling two signals dropped
 @pytest.mark.parametrize("b,n", [(32, 4001), (64, 1031), (96, 2053), (32, 9001)])
-@pytest.mark.parametrize("k", [34, 63, 64, 100, 127, 255, 256, 300, 511, 512, 1000, 2049])
+@pytest.mark.parametrize("k", [34, 63, 64, 100, 127, 255, 256, 300, 511, 512, 1000, 1024, 1536, 2049,
+                               3000])
 def test_flat_batch_unaligned_signals(b, n, k):
     if k > n:
         pytest.skip("window longer than the signal")

@@ -1,4 +1,5 @@
-"""Exact sums for k > 512 on the config-2 input (256 x 262,144): the tile +
+"""Exact sums for k > 512 on the config-2 input (256 x 262,144, and the
+unaligned 256 x 262,143 as one flat signal): the tile +
 pass composite (pool1d.cu launch_exact_big) vs the reference-structured global
 passes (SC_POOL_NO_EXACT_BLOCK=1, run in a subprocess)."""
 import json
@@ -15,9 +16,10 @@ if __name__ == "__main__":
         import paper_2310_05218_b200 as sc
         g = torch.Generator(device="cuda")
         g.manual_seed(2)
-        x = torch.randn((256, 262144), device="cuda", generator=g)
         res = {}
-        for k in (600, 1000, 2048, 3000, 4095, 8191):
+        for L, k in [(262144, 600), (262144, 1000), (262144, 2048), (262144, 3000), (262144, 4095),
+                     (262144, 8191), (262143, 1000), (262143, 2048)]:
+            x = torch.randn((256, L), device="cuda", generator=g)
             for _ in range(2):
                 sc.sliding_window_sum(x, k, exact=True)
             torch.cuda.synchronize()
@@ -27,7 +29,7 @@ if __name__ == "__main__":
                 sc.sliding_window_sum(x, k, exact=True)
             b.record()
             b.synchronize()
-            res[k] = round(a.elapsed_time(b) / 5, 3)
+            res[f"L{L}_k{k}"] = round(a.elapsed_time(b) / 5, 3)
         print(json.dumps({"passes_only": os.environ.get("SC_POOL_NO_EXACT_BLOCK") is not None,
                           "ms": res}), flush=True)
         sys.exit(0)
