@@ -62,6 +62,15 @@ const char* sc_last_error(void);
  * Returns SC_ERR_SHAPE unless 1 <= k <= length (pooling.py:32-33). */
 int sc_pool1d_f32(int op, const float* x, int64_t batch, int64_t length, int64_t k,
                   int mode, float* y, void* stream);
+/* Fused pair (new): y_a = sliding_window_sum (op_a = SC_POOL_SUM) or its
+ * average (SC_POOL_AVG) and y_max = sliding_window_max (pooling.py:28-53 and
+ * :56-78) of the SAME signals in one pass over x -- one read of the input for
+ * both outputs on the TMA kernel's windows (k = 2..33, 64; 16-byte aligned
+ * signals of length % 32 == 0); other shapes run the two single-op kernels
+ * back to back.  Each output is bit-identical to sc_pool1d_f32's for that op
+ * and mode.  y_a and y_max: (batch, length - k + 1) each, not aliased. */
+int sc_pool1d_pair_f32(int op_a, const float* x, int64_t batch, int64_t length, int64_t k,
+                       int mode, float* y_a, float* y_max, void* stream);
 /* Stage count the reference returns alongside y (pooling.py:37-51, :67-76). */
 int64_t sc_pool1d_stages(int op, int64_t k);
 
@@ -146,6 +155,8 @@ int sc_rowband_conv2d_f32(sc_rowband* ctx, float* const* bands, const int64_t* r
  * Same semantics as the device entry points; x and y are HOST pointers. */
 int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t length, int64_t k,
                        int mode, float* y, int device);
+int sc_pool1d_pair_f32_host(int op_a, const float* x, int64_t batch, int64_t length, int64_t k,
+                            int mode, float* y_a, float* y_max, int device);
 int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                        int64_t kh, int64_t kw, int mode, float* y, int device);
 

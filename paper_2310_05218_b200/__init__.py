@@ -13,7 +13,8 @@ from .kernels import (KernelVariant, analytic_counters, applicable_variants, com
                       variant_applicable)
 from .lanes import VectorModel, slide
 from .nchw import conv2d_nchw
-from .pooling import sliding_window_max, sliding_window_mean, sliding_window_sum
+from .pooling import (sliding_window_max, sliding_window_mean, sliding_window_mean_max,
+                      sliding_window_sum, sliding_window_sum_max)
 from .reference import conv1d_reference, conv2d_reference, oracle_conv2d, relative_error
 from .rowband import RowBandGroup, RowBandPlan, alloc_band, conv2d_rowband, plan_row_bands
 from .verify import PropertyResult, VerifyReport, verify_suite
@@ -33,7 +34,7 @@ __all__ = [
     "analytic_counters", "compound_width", "counted_offsets", "variant_applicable",
     "relative_error", "verify_suite", "VerifyReport", "PropertyResult",
     # B200 extensions (BASELINE configs)
-    "sliding_window_mean", "conv2d_nchw", "conv2d_rowband", "plan_row_bands", "RowBandPlan", "alloc_band",
-    "RowBandGroup",
+    "sliding_window_mean", "sliding_window_sum_max", "sliding_window_mean_max", "conv2d_nchw",
+    "conv2d_rowband", "plan_row_bands", "RowBandPlan", "alloc_band", "RowBandGroup",
     "pinned_empty", "set_default_mode",
 ]

@@ -33,6 +33,7 @@ SIGNATURES = {
     "sc_version": (_int, []),
     "sc_last_error": (ctypes.c_char_p, []),
     "sc_pool1d_f32": (_int, [_int, _vp, _i64, _i64, _i64, _int, _vp, _vp]),
+    "sc_pool1d_pair_f32": (_int, [_int, _vp, _i64, _i64, _i64, _int, _vp, _vp, _vp]),
     "sc_pool1d_stages": (_i64, [_int, _i64]),
     "sc_conv1d_f32": (_int, [_vp, _i64, _i64, _vp, _i64, _int, _vp, _vp]),
     "sc_conv2d_f32": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _vp]),
@@ -49,6 +50,7 @@ SIGNATURES = {
                                      _i64, _i64, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                      _int]),
     "sc_pool1d_f32_host": (_int, [_int, _vp, _i64, _i64, _i64, _int, _vp, _int]),
+    "sc_pool1d_pair_f32_host": (_int, [_int, _vp, _i64, _i64, _i64, _int, _vp, _vp, _int]),
     "sc_conv2d_f32_host": (_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _int, _vp, _int]),
 }
 

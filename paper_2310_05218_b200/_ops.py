@@ -108,6 +108,27 @@ def pool1d(op: int, x, k: int, exact=None):
     return y
 
 
+def pool1d_pair(op_a: int, x, k: int, exact=None):
+    """x: (B, L) -> (y_a, y_max), each (B, L - k + 1), from one pass over x
+    (op_a: POOL_SUM or POOL_AVG); host inputs cross the link once."""
+    lib = require_cuda()
+    b, n = (int(d) for d in x.shape)
+    mode = mode_flag(exact)
+    if is_cuda_tensor(x):
+        torch = torch_mod()
+        ya = torch.empty((b, n - k + 1), dtype=torch.float32, device=x.device)
+        ym = torch.empty_like(ya)
+        with on_device(x):
+            _lib.check(lib.sc_pool1d_pair_f32(op_a, ptr(x), b, n, k, mode, ptr(ya), ptr(ym),
+                                              stream_of(x)))
+        return ya, ym
+    ya = host_output((b, n - k + 1))
+    ym = host_output((b, n - k + 1))
+    _lib.check(lib.sc_pool1d_pair_f32_host(op_a, ptr(x), b, n, k, mode, ptr(ya), ptr(ym),
+                                           device_index()))
+    return ya, ym
+
+
 def pool_stages(op: int, k: int) -> int:
     return int(_lib.load().sc_pool1d_stages(op, k))
 

@@ -25,6 +25,8 @@ int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, con
 
 extern "C" int sc_pool1d_f32(int op, const float* x, int64_t batch, int64_t length, int64_t k,
                              int mode, float* y, void* stream);
+extern "C" int sc_pool1d_pair_f32(int op_a, const float* x, int64_t batch, int64_t length,
+                                  int64_t k, int mode, float* y_a, float* y_max, void* stream);
 
 namespace sc {
 namespace {
@@ -68,13 +70,17 @@ struct Slot {
   cudaStream_t stream = nullptr;
   float* d_in = nullptr;
   float* d_out = nullptr;
-  size_t in_cap = 0, out_cap = 0;
+  float* d_out2 = nullptr;  // second output stream (fused pooling pair)
+  size_t in_cap = 0, out_cap = 0, out2_cap = 0;
   float* h_in = nullptr;   // pinned staging
   float* h_out = nullptr;
-  size_t h_in_cap = 0, h_out_cap = 0;
+  float* h_out2 = nullptr;
+  size_t h_in_cap = 0, h_out_cap = 0, h_out2_cap = 0;
   // pending pageable write-back of the chunk last issued on this slot
   float* wb_dst = nullptr;
   size_t wb_bytes = 0;
+  float* wb_dst2 = nullptr;
+  size_t wb_bytes2 = 0;
 };
 
 struct DeviceCtx {
@@ -143,7 +149,9 @@ struct Chunk {
   size_t in_bytes;
   float* out;
   size_t out_bytes;
-  std::function<int(const float*, float*, cudaStream_t)> run;
+  std::function<int(const float*, float*, float*, cudaStream_t)> run;  // (in, out, out2, stream)
+  float* out2 = nullptr;  // second output of the chunk (fused pooling pair), else null
+  size_t out2_bytes = 0;
 };
 
 class DeviceGuard {
@@ -166,6 +174,10 @@ int finish_slot(Slot& s) {
     parallel_memcpy(s.wb_dst, s.h_out, s.wb_bytes);
     s.wb_dst = nullptr;
   }
+  if (s.wb_dst2) {
+    parallel_memcpy(s.wb_dst2, s.h_out2, s.wb_bytes2);
+    s.wb_dst2 = nullptr;
+  }
   return SC_OK;
 }
 
@@ -178,10 +190,11 @@ int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_p
     for (auto& s : ctx.slot) SC_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     ctx.init = true;
   }
-  size_t max_in = 0, max_out = 0;
+  size_t max_in = 0, max_out = 0, max_out2 = 0;
   for (auto& c : chunks) {
     max_in = std::max(max_in, c.in_bytes);
     max_out = std::max(max_out, c.out_bytes);
+    max_out2 = std::max(max_out2, c.out2_bytes);
   }
   for (auto& s : ctx.slot) {
     int rc;
@@ -189,6 +202,8 @@ int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_p
     if ((rc = grow_dev(&s.d_out, &s.out_cap, max_out))) return rc;
     if (!in_pinned && (rc = grow_host(&s.h_in, &s.h_in_cap, max_in))) return rc;
     if (!out_pinned && (rc = grow_host(&s.h_out, &s.h_out_cap, max_out))) return rc;
+    if (max_out2 && (rc = grow_dev(&s.d_out2, &s.out2_cap, max_out2))) return rc;
+    if (max_out2 && !out_pinned && (rc = grow_host(&s.h_out2, &s.h_out2_cap, max_out2))) return rc;
   }
   int status = SC_OK;
   for (size_t i = 0; i < chunks.size() && status == SC_OK; ++i) {
@@ -209,7 +224,7 @@ int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_p
       status = cuda_fail(cudaGetLastError(), "H2D copy");
       break;
     }
-    if ((status = c.run(s.d_in, s.d_out, s.stream))) break;
+    if ((status = c.run(s.d_in, s.d_out, s.d_out2, s.stream))) break;
     float* dst = out_pinned ? c.out : s.h_out;
     if (cudaMemcpyAsync(dst, s.d_out, c.out_bytes, cudaMemcpyDeviceToHost, s.stream) !=
         cudaSuccess) {
@@ -219,6 +234,18 @@ int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_p
     if (!out_pinned) {
       s.wb_dst = c.out;
       s.wb_bytes = c.out_bytes;
+    }
+    if (c.out2) {
+      float* dst2 = out_pinned ? c.out2 : s.h_out2;
+      if (cudaMemcpyAsync(dst2, s.d_out2, c.out2_bytes, cudaMemcpyDeviceToHost, s.stream) !=
+          cudaSuccess) {
+        status = cuda_fail(cudaGetLastError(), "D2H copy");
+        break;
+      }
+      if (!out_pinned) {
+        s.wb_dst2 = c.out2;
+        s.wb_bytes2 = c.out2_bytes;
+      }
     }
   }
   for (auto& s : ctx.slot) {
@@ -231,17 +258,26 @@ int run_pipeline(int dev, std::vector<Chunk>& chunks, bool in_pinned, bool out_p
 }  // namespace
 }  // namespace sc
 
-extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t length, int64_t k,
-                                  int mode, float* y, int device) {
-  using namespace sc;
-  if (op < SC_POOL_SUM || op > SC_POOL_MAX) return fail(SC_ERR_ARG, "pool1d: bad op");
+namespace sc {
+namespace {
+
+// op_a / y: the single op (y_max null), or the fused pair's first op with
+// y_max its maxima; chunking is the same, a pair chunk carries two outputs
+int pool1d_host(int op, const float* x, int64_t batch, int64_t length, int64_t k, int mode,
+                float* y, float* y_max, int device) {
   if (batch < 0 || length < 1) return fail(SC_ERR_SHAPE, "pool1d: signal length must be >= 1");
   if (k < 1 || k > length)
     return fail(SC_ERR_SHAPE, "window " + std::to_string(k) + " out of range for length " +
                                   std::to_string(length));
   if (batch == 0) return SC_OK;
   if (!x || !y) return fail(SC_ERR_ARG, "pool1d: null pointer");
+  const bool pair = y_max != nullptr;
   const int64_t out_len = length - k + 1;
+  auto run_op = [=](const float* din, int64_t rows, int64_t len, float* dout, float* dout2,
+                    cudaStream_t st) {
+    return pair ? sc_pool1d_pair_f32(op, din, rows, len, k, mode, dout, dout2, st)
+                : sc_pool1d_f32(op, din, rows, len, k, mode, dout, st);
+  };
   std::vector<Chunk> chunks;
   const int64_t row_bytes = length * (int64_t)sizeof(float);
   const size_t kChunkBytes = chunk_bytes((size_t)(batch * row_bytes));
@@ -251,11 +287,13 @@ extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t
     for (const int64_t nr : ramp_sizes(batch, rows, 1)) {
       const int64_t r0 = r;
       r += nr;
+      const size_t ob = (size_t)(nr * out_len) * sizeof(float);
       chunks.push_back({x + r0 * length, (size_t)(nr * length) * sizeof(float), y + r0 * out_len,
-                        (size_t)(nr * out_len) * sizeof(float),
-                        [=](const float* din, float* dout, cudaStream_t st) {
-                          return sc_pool1d_f32(op, din, nr, length, k, mode, dout, st);
-                        }});
+                        ob,
+                        [=](const float* din, float* dout, float* dout2, cudaStream_t st) {
+                          return run_op(din, nr, length, dout, dout2, st);
+                        },
+                        pair ? y_max + r0 * out_len : nullptr, pair ? ob : 0});
     }
   } else {
     // one signal is larger than a chunk: segments with a k-1 sample overlap.
@@ -268,14 +306,37 @@ extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t
       for (int64_t o = 0; o < out_len; o += seg) {
         const int64_t no = std::min(seg, out_len - o);
         const int64_t ni = no + k - 1;
-        chunks.push_back({x + r * length + o, (size_t)ni * sizeof(float), y + r * out_len + o,
-                          (size_t)no * sizeof(float),
-                          [=](const float* din, float* dout, cudaStream_t st) {
-                            return sc_pool1d_f32(op, din, 1, ni, k, mode, dout, st);
-                          }});
+        const size_t ob = (size_t)no * sizeof(float);
+        chunks.push_back({x + r * length + o, (size_t)ni * sizeof(float), y + r * out_len + o, ob,
+                          [=](const float* din, float* dout, float* dout2, cudaStream_t st) {
+                            return run_op(din, 1, ni, dout, dout2, st);
+                          },
+                          pair ? y_max + r * out_len + o : nullptr, pair ? ob : 0});
       }
   }
-  return run_pipeline(device, chunks, is_pinned(x), is_pinned(y));
+  return run_pipeline(device, chunks, is_pinned(x), is_pinned(y) && (!pair || is_pinned(y_max)));
+}
+
+}  // namespace
+}  // namespace sc
+
+extern "C" int sc_pool1d_f32_host(int op, const float* x, int64_t batch, int64_t length, int64_t k,
+                                  int mode, float* y, int device) {
+  using namespace sc;
+  if (op < SC_POOL_SUM || op > SC_POOL_MAX) return fail(SC_ERR_ARG, "pool1d: bad op");
+  return pool1d_host(op, x, batch, length, k, mode, y, nullptr, device);
+}
+
+// Fused pair on host buffers: x goes over the link ONCE for both outputs.
+extern "C" int sc_pool1d_pair_f32_host(int op_a, const float* x, int64_t batch, int64_t length,
+                                       int64_t k, int mode, float* y_a, float* y_max,
+                                       int device) {
+  using namespace sc;
+  if (op_a != SC_POOL_SUM && op_a != SC_POOL_AVG)
+    return fail(SC_ERR_ARG, "pool1d_pair: first op must be SUM or AVG");
+  if (!y_max && batch > 0) return fail(SC_ERR_ARG, "pool1d: null pointer");
+  if (y_a == y_max && batch > 0) return fail(SC_ERR_ARG, "pool1d_pair: outputs alias");
+  return pool1d_host(op_a, x, batch, length, k, mode, y_a, y_max, device);
 }
 
 extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int64_t w,
@@ -302,7 +363,7 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
       b_next += nb;
       chunks.push_back({x + b * h * w, (size_t)(nb * h * w) * sizeof(float), y + b * oh * ow,
                         (size_t)(nb * oh * ow) * sizeof(float),
-                        [=, &taps](const float* din, float* dout, cudaStream_t st) {
+                        [=, &taps](const float* din, float* dout, float*, cudaStream_t st) {
                           return conv2d_f32_dispatch(din, nb, h, w, taps.data(), kh, kw, exact,
                                                      dout, st);
                         }});
@@ -321,7 +382,7 @@ extern "C" int sc_conv2d_f32_host(const float* x, int64_t batch, int64_t h, int6
         const int64_t ni = no + kh - 1;
         chunks.push_back({x + (b * h + o) * w, (size_t)(ni * w) * sizeof(float),
                           y + (b * oh + o) * ow, (size_t)(no * ow) * sizeof(float),
-                          [=, &taps](const float* din, float* dout, cudaStream_t st) {
+                          [=, &taps](const float* din, float* dout, float*, cudaStream_t st) {
                             return conv2d_f32_dispatch(din, 1, ni, w, taps.data(), kh, kw, exact,
                                                        dout, st);
                           }});

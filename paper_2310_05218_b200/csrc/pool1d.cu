@@ -26,6 +26,8 @@
 namespace sc {
 int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                cudaStream_t st);
+int pool1d_pair_tma(int op_a, const float* x, int64_t batch, int64_t length, int64_t k,
+                    float* y_a, float* y_max, cudaStream_t st);
 int pool1d_block_sum(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
                      cudaStream_t st);
 int pool1d_wide(int op, const float* x, int64_t batch, int64_t length, int64_t k, float* y,
@@ -659,4 +661,29 @@ extern "C" int sc_pool1d_f32(int op, const float* x, int64_t batch, int64_t leng
     case SC_POOL_AVG: return dispatch<SC_POOL_AVG>(x, batch, length, k, mode, y, st);
     default: return dispatch<SC_POOL_MAX>(x, batch, length, k, mode, y, st);
   }
+}
+
+// Fused sum-or-average + max pooling: one read of x for both outputs on the
+// TMA kernel's windows (k = 2..33, 64 on aligned signals); any other shape runs
+// the two single-op paths back to back.  Either way y_a / y_max are
+// bit-identical to what sc_pool1d_f32 writes for op_a / SC_POOL_MAX.
+extern "C" int sc_pool1d_pair_f32(int op_a, const float* x, int64_t batch, int64_t length,
+                                  int64_t k, int mode, float* y_a, float* y_max, void* stream) {
+  using namespace sc;
+  if (op_a != SC_POOL_SUM && op_a != SC_POOL_AVG)
+    return fail(SC_ERR_ARG, "pool1d_pair: first op must be SUM or AVG");
+  if (mode != SC_MODE_FAST && mode != SC_MODE_EXACT) return fail(SC_ERR_ARG, "pool1d: bad mode");
+  if (batch < 0 || length < 1) return fail(SC_ERR_SHAPE, "pool1d: signal length must be >= 1");
+  if (k < 1 || k > length)
+    return fail(SC_ERR_SHAPE, "window " + std::to_string(k) + " out of range for length " +
+                                  std::to_string(length));
+  if (batch == 0) return SC_OK;
+  if (!x || !y_a || !y_max) return fail(SC_ERR_ARG, "pool1d: null pointer");
+  if (y_a == y_max) return fail(SC_ERR_ARG, "pool1d_pair: outputs alias");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int rc = pool1d_pair_tma(op_a, x, batch, length, k, y_a, y_max, st);
+  if (rc != 1) return rc;
+  const int ra = sc_pool1d_f32(op_a, x, batch, length, k, mode, y_a, stream);
+  if (ra != SC_OK) return ra;
+  return sc_pool1d_f32(SC_POOL_MAX, x, batch, length, k, mode, y_max, stream);
 }

@@ -31,6 +31,10 @@ constexpr int kTmaWarps = 8;
 // kernel "ops" beyond sc_pool_op: 1-D convolution with K taps (BASELINE config 1)
 constexpr int kConvFast = 3;
 constexpr int kConvExact = 4;
+// fused pair: window sums (or averages) AND window maxima of the same tile in
+// one pass -- one read of the input, two output streams (sc_pool1d_pair_f32)
+constexpr int kPairSum = 5;
+constexpr int kPairAvg = 6;
 
 template <int K>
 struct Taps1 {
@@ -139,7 +143,7 @@ __device__ __forceinline__ void blocked_conv(float (&s)[T], const Taps1<K>& taps
 template <int kOp, int K, int NBUF>
 __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
     pool_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ y,
-                    int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
+                    float* __restrict__ y2, int64_t out_len, int64_t tiles_per_row, int64_t n_tiles, int tiles_per_cta,
                     const Taps1<K> taps) {
   constexpr int T = kTmaT;
   constexpr int V = tma_valid(K);
@@ -224,52 +228,69 @@ __global__ void __launch_bounds__(32 * (kTmaWarps + 1))
     };
     load();
     release();  // the window is in registers: hand the buffer back at once
-    if constexpr (kOp == SC_POOL_MAX) {
+    // stage (padded rows, conflict-free STS.128) -> coalesced 32-bit stores
+    auto emit = [&](float* __restrict__ dst) {
+#pragma unroll
+      for (int q = 0; q < T / 4; ++q)
+        *reinterpret_cast<float4*>(stage + lane * kStageStride + 4 * q) =
+            make_float4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
+      __syncwarp();
+      const unsigned row = t / tpr;
+      const int64_t o_in_row = (int64_t)(t - row * tpr) * (kTmaWarps * V) + warp * V;
+      const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
+      float* yr = dst + (int64_t)row * out_len + o_in_row + lane;
+      const float* sp = stage + (lane / T) * kStageStride + (lane % T);
+      if (lim == V) {
+#pragma unroll
+        for (int m = 0; m < V / 32; ++m) yr[32 * m] = sp[(32 / T) * m * kStageStride];
+        if constexpr (V % 32 != 0) {
+          if (lane < V % 32) yr[32 * (V / 32)] = sp[(32 / T) * (V / 32) * kStageStride];
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < (V + 31) / 32; ++m)
+          if (32 * m + lane < lim) yr[32 * m] = sp[(32 / T) * m * kStageStride];
+      }
+      __syncwarp();  // staging slab reused by the next output / tile
+    };
+    auto pool_max = [&]() {
       float s_in[T];
 #pragma unroll
       for (int j = 0; j < T; ++j) s_in[j] = s[j];
-      blocked_pool<T, kOp, false, K>(s);
+      blocked_pool<T, SC_POOL_MAX, false, K>(s);
       bool zero = false;
 #pragma unroll
       for (int j = 0; j < T; ++j) zero |= (s[j] == 0.0f) && (T * lane + j < V);
       if (__any_sync(0xffffffffu, zero)) {  // rare: redo with np.maximum's order
 #pragma unroll
         for (int j = 0; j < T; ++j) s[j] = s_in[j];
-        blocked_pool<T, kOp, true, K>(s);
+        blocked_pool<T, SC_POOL_MAX, true, K>(s);
       }
-    } else if constexpr (kOp >= kConvFast) {
-      blocked_conv<T, K, kOp == kConvExact>(s, taps);
-    } else {
-      blocked_pool<T, kOp, false, K>(s);
-      if constexpr (kOp == SC_POOL_AVG) {
+    };
+    auto pool_sum = [&](bool avg) {
+      blocked_pool<T, SC_POOL_SUM, false, K>(s);
+      if (avg) {
 #pragma unroll
         for (int j = 0; j < T; ++j) s[j] = kPow2 ? s[j] * inv_k : s[j];
         if constexpr (!kPow2) div_all_by_k<T>(s, fk, inv_k);
       }
-    }
-    // stage (padded rows, conflict-free STS.128) -> coalesced 32-bit stores
+    };
+    if constexpr (kOp == kPairSum || kOp == kPairAvg) {
+      float keep[T];
 #pragma unroll
-    for (int q = 0; q < T / 4; ++q)
-      *reinterpret_cast<float4*>(stage + lane * kStageStride + 4 * q) =
-          make_float4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
-    __syncwarp();
-    const unsigned row = t / tpr;
-    const int64_t o_in_row = (int64_t)(t - row * tpr) * (kTmaWarps * V) + warp * V;
-    const int lim = (int)min((int64_t)V, out_len - (int64_t)o_in_row);
-    float* yr = y + (int64_t)row * out_len + o_in_row + lane;
-    const float* sp = stage + (lane / T) * kStageStride + (lane % T);
-    if (lim == V) {
+      for (int j = 0; j < T; ++j) keep[j] = s[j];
+      pool_sum(kOp == kPairAvg);
+      emit(y);
 #pragma unroll
-      for (int m = 0; m < V / 32; ++m) yr[32 * m] = sp[(32 / T) * m * kStageStride];
-      if constexpr (V % 32 != 0) {
-        if (lane < V % 32) yr[32 * (V / 32)] = sp[(32 / T) * (V / 32) * kStageStride];
-      }
+      for (int j = 0; j < T; ++j) s[j] = keep[j];
+      pool_max();
+      emit(y2);
     } else {
-#pragma unroll
-      for (int m = 0; m < (V + 31) / 32; ++m)
-        if (32 * m + lane < lim) yr[32 * m] = sp[(32 / T) * m * kStageStride];
+      if constexpr (kOp == SC_POOL_MAX) pool_max();
+      else if constexpr (kOp >= kConvFast) blocked_conv<T, K, kOp == kConvExact>(s, taps);
+      else pool_sum(kOp == SC_POOL_AVG);
+      emit(y);
     }
-    __syncwarp();  // staging slab reused by the next tile
   }
 }
 
@@ -282,7 +303,7 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 
 template <int kOp, int K, int NBUF>
 int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
-                const float* w) {
+                const float* w, float* y2 = nullptr) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap map;
@@ -313,6 +334,7 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
       kOp == SC_POOL_SUM ? (K <= 24 ? 2 : 4)
       : kOp == SC_POOL_AVG ? ((kPow2 && K <= 16) || K == 3 ? 2 : 4)
       : kOp == SC_POOL_MAX ? (K <= 8 ? 2 : 4)
+      : (kOp == kPairSum || kOp == kPairAvg) ? (K <= 16 ? 2 : 4)  // k = 16: 121.7 us at 2, 123.1 at 4
       : 2;  // weighted (conv1d) windows
   const int tpc = env_int("SC_POOL_TPC", kTpcDefault, 1, 64);
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
@@ -320,24 +342,25 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
   if (w)
     for (int i = 0; i < K; ++i) taps.f[i] = w[i];
   SC_CUDA(launch_pdl(pool_tma_kernel<kOp, K, NBUF>, dim3((unsigned)grid),
-                     dim3(32 * (kTmaWarps + 1)), smem, st, map, y, out_len, tiles_per_row, n_tiles,
-                     tpc, taps));
+                     dim3(32 * (kTmaWarps + 1)), smem, st, map, y, y2, out_len, tiles_per_row,
+                     n_tiles, tpc, taps));
   SC_LAUNCH_CHECK("pool_tma_kernel");
   return SC_OK;
 }
 
 template <int kOp, int K>
 int launch_one(const float* x, int64_t batch, int64_t length, float* y, cudaStream_t st,
-               const float* w) {
+               const float* w, float* y2 = nullptr) {
   // ring depth 2 with 4 contiguous tiles per CTA measured best (tools/pool_sweep.py)
-  return launch_nbuf<kOp, K, 2>(x, batch, length, y, st, w);
+  return launch_nbuf<kOp, K, 2>(x, batch, length, y, st, w, y2);
 }
 
 template <int kOp, int... Ks>
 int launch_switch(int k, const float* x, int64_t batch, int64_t length, float* y,
-                  cudaStream_t st, std::integer_sequence<int, Ks...>, const float* w = nullptr) {
+                  cudaStream_t st, std::integer_sequence<int, Ks...>, const float* w = nullptr,
+                  float* y2 = nullptr) {
   int rc = -1000;
-  ((k == Ks ? (rc = launch_one<kOp, Ks>(x, batch, length, y, st, w), 0) : 0), ...);
+  ((k == Ks ? (rc = launch_one<kOp, Ks>(x, batch, length, y, st, w, y2), 0) : 0), ...);
   return rc;
 }
 
@@ -362,6 +385,24 @@ int pool1d_tma(int op, const float* x, int64_t batch, int64_t length, int64_t k,
     case SC_POOL_AVG: rc = launch_switch<SC_POOL_AVG>((int)k, x, batch, length, y, st, Windows{}); break;
     default: rc = launch_switch<SC_POOL_MAX>((int)k, x, batch, length, y, st, Windows{}); break;
   }
+  return rc == -1000 ? 1 : rc;
+}
+
+// Fused pair (sc_pool1d_pair_f32): y_a = window sums (op_a = SUM) or averages
+// (AVG), y_max = window maxima, both from one read of x; each output is
+// bit-identical to its single-op launch (same per-op code on the same
+// registers).  Returns 1 when the TMA path does not apply.
+int pool1d_pair_tma(int op_a, const float* x, int64_t batch, int64_t length, int64_t k,
+                    float* y_a, float* y_max, cudaStream_t st) {
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0 || length % 32 != 0 || k < 2 || k > 64 ||
+      (k > 33 && k != 64) || length / 32 > 0x7fffffff || batch > 0x7fffffff)
+    return 1;
+  if (length < kTmaWin) return 1;
+  const int rc = op_a == SC_POOL_AVG
+                     ? launch_switch<kPairAvg>((int)k, x, batch, length, y_a, st, Windows{},
+                                               nullptr, y_max)
+                     : launch_switch<kPairSum>((int)k, x, batch, length, y_a, st, Windows{},
+                                               nullptr, y_max);
   return rc == -1000 ? 1 : rc;
 }
 

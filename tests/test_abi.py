@@ -29,7 +29,8 @@ def test_header_declares_the_expected_entry_points():
     syms = declared_symbols()
     for s in ("sc_pool1d_f32", "sc_conv1d_f32", "sc_conv2d_f32", "sc_conv2d_f64",
               "sc_conv2d_nchw_f32", "sc_im2col_f32", "sc_gemm_f32", "sc_pool1d_f32_host",
-              "sc_conv2d_f32_host", "sc_version", "sc_last_error"):
+              "sc_conv2d_f32_host", "sc_version", "sc_last_error", "sc_pool1d_pair_f32",
+              "sc_pool1d_pair_f32_host"):
         assert s in syms
 
 

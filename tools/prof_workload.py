@@ -20,6 +20,11 @@ if which.startswith("psum") or which.startswith("pavg") or which.startswith("pma
     x = torch.randn((256, 262144), generator=g, device=dev)
     for _ in range(reps):
         fn(x, k)
+elif which.startswith("pair"):
+    k = int(which[4:])
+    x = torch.randn((256, 262144), generator=g, device=dev)
+    for _ in range(reps):
+        sc.sliding_window_mean_max(x, k)
 elif which.startswith("pool"):
     k = int(which[4:])
     x = torch.randn((256, 262144), generator=g, device=dev)
