@@ -1,0 +1,457 @@
+// Large single-channel filters on the 5th-generation tensor cores (fast mode):
+// the slide-MMA formulation of _accumulate_taps (reference.py:15-23) for the
+// paper's large-filter sweep (kernels.py:248-255, conv2d_slide_compound),
+// 10 <= kw <= 57 and kh <= 53.  SURVEY 8(f)3 / 8(f)4.
+//
+// Per input row t and 1,024-column strip:
+//   M = 128 lanes m, lane m owning output columns c0 + 8 m + s (s = 0..7),
+//   K = 16 kb + k: input samples x[t][c0 + 8 m + 16 kb + k] -- A is the input
+//       row itself, read through a no-swizzle K-major descriptor with
+//       LBO = 16 B and SBO = 128 B, so A[m][k] = x[8 m + 16 kb + k] (core
+//       matrices overlap by one 16-byte row; nothing is expanded in memory,
+//       same descriptor as conv2d_mma.cu, tools/micro/hankel_probe.cu),
+//   N = (output row o = t - j, shift s): B[(o, s)][k] = f[t - o][16 kb + k - s].
+// One MMA adds the taps of ALL filter rows that input row t feeds (a window
+// of kh output rows) for 16 input samples per lane:
+//   D[m][(o, s)] += sum_k x[t][c0 + 8 m + 16 kb + k] f[t - o][16 kb + k - s].
+// D is a TMEM ring of 64 output-row slots of 8 columns (512 columns, one CTA
+// per SM); an output row is final after the MMAs of input row o + kh - 1,
+// then drained by the epilogue warps and re-zeroed.  The window of row t
+// starts on a multiple of 4 rows (D offsets are multiples of 32 columns), the
+// remaining 0..3 row phase is a 256-byte offset into a zero-padded B image.
+//
+// Precision: x = x1 + x2, f = f1 + f2 (bf16, round to nearest); D
+// accumulates x1 f1 + x1 f2 + x2 f1 in fp32 (the x2 f2 term is ~2^-18 of a
+// product), ~4e-6 normwise against the north-star 1e-5 k.  CTAs whose inputs
+// the split cannot carry (|x| > 2^64, non-finite, nonzero |x| < 2^-100)
+// recompute their outputs with FMAs in the reference tap order afterwards.
+//
+// Warps: 0-3 split (global fp32 row -> x1 / x2 bf16 rows in shared memory,
+// 4 rows per batch, the next batch's loads in flight while waiting for a
+// slot), 4-7 epilogue (one TMEM lane quarter each, 4 output rows per batch),
+// 8 MMA issuer (3 products x K blocks x window pieces per input row, one
+// commit per batch).  Hand-offs are per batch of 4 rows (~1,000-12,000 tensor
+// cycles of work), so plain counters / mbarriers suffice.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace sc {
+namespace {
+using namespace tc;
+
+constexpr int kStrip = 1024;             // output columns per CTA (128 lanes x 8 shifts)
+constexpr int kRB = 4;                   // input rows per batch
+constexpr int kXB = 3;                   // batches of split rows in shared memory
+constexpr int kRing = 64;                // output-row slots in TMEM (8 columns each)
+constexpr int kMaxKH = 53, kMaxKW = 57;
+constexpr int kMaxKB = 4;                // K blocks of 16 samples: 16 n_kb >= kw + 7
+constexpr int kXRow = 2176;              // bytes per bf16 row (1,080 samples used)
+constexpr int kXSlot = 2 * kXRow;        // x1 | x2
+constexpr int kND = 32;                  // MMA-completion barriers (one per batch, ring)
+constexpr int kThreads = 32 * 9;
+constexpr int kPad = 3;                  // zero slots in front of the B image (row phase)
+
+__host__ __device__ constexpr int win_rows(int kh) { return (kh + 3 + 1) & ~1; }       // even
+__host__ __device__ constexpr int bimg_slots(int kh) { return kPad + win_rows(kh) + 1; }
+__host__ __device__ constexpr int bimg_bytes(int kh) { return bimg_slots(kh) * 256; }
+
+struct BigMmaArgs {
+  int kh, kw, nkb, nw;
+  int oh, ow, h, w;
+  int seg_rows;
+};
+
+struct TapsArg {
+  float f[kMaxKH * kMaxKW];
+};
+
+// B images in global memory, [part f1 / f2][kb][slot][k half][s][k & 7] bf16:
+// element (n = 8 slot + s, k) of the no-swizzle K-major layout (LBO 128 B
+// between the k halves, SBO 256 B per 8 rows); slot = kPad + jslot holds
+// filter row j = kh - 1 - jslot, zeros elsewhere.  Then the fp32 taps (for
+// the FMA fallback).
+__global__ void build_b_kernel(const __grid_constant__ TapsArg taps, int kh, int kw, int nkb,
+                               __nv_bfloat16* __restrict__ bimg, float* __restrict__ taps_out) {
+  const int slots = bimg_slots(kh);
+  const int per = slots * 128;  // elements per (part, kb) image
+  const int total = 2 * nkb * per;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int img = e / per, r = e - img * per;
+    const int part = img / nkb, kb = img - part * nkb;
+    const int slot = r >> 7, kh2 = (r >> 6) & 1, s = (r >> 3) & 7, k7 = r & 7;
+    const int k = 8 * kh2 + k7;
+    const int jslot = slot - kPad, j = kh - 1 - jslot, i = 16 * kb + k - s;
+    float v = 0.0f;
+    if (jslot >= 0 && j >= 0 && i >= 0 && i < kw) v = taps.f[j * kw + i];
+    const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
+    bimg[e] = part ? __float2bfloat16_rn(v - __bfloat162float(v1)) : v1;
+  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kh * kw; e += gridDim.x * blockDim.x)
+    taps_out[e] = taps.f[e];
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\tsetp.eq.u32 p, 1, 1;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(da), "l"(db), "r"(idesc)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+      "r"(0u)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
+// 2^64 / 2^-100 as float bit patterns (magnitudes the bf16 split carries)
+constexpr uint32_t kHiBits = 0x5F800000u, kLoBits = 0x0D800000u;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    conv2d_mma_big_kernel(const float* __restrict__ xg, float* __restrict__ y,
+                          const uint4* __restrict__ bimg, const float* __restrict__ taps,
+                          const __grid_constant__ BigMmaArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ int split_cnt[4], epi_cnt[4];       // batches done per warp (release / acquire)
+  __shared__ __align__(8) uint64_t done[kND];    // MMA completion, one per batch of input rows
+  __shared__ __align__(8) uint64_t ring_ready;
+  __shared__ uint32_t tmem_base_sh;
+  unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  unsigned char* xrows = base;                                   // kXB * kRB slots
+  unsigned char* bmats = xrows + kXB * kRB * kXSlot;             // 2 * nkb images
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kh = args.kh, kw = args.kw, nkb = args.nkb, nw = args.nw;
+  const int c0 = blockIdx.x * kStrip;
+  const int r0 = blockIdx.y * args.seg_rows;
+  const int img = blockIdx.z;
+  const int s_valid = min(args.seg_rows, args.oh - r0);  // output rows of this CTA
+  const int t_rows = s_valid + kh - 1;                    // input rows it reads
+  const int n_batches = (t_rows + kRB - 1) / kRB;
+  const int o_start = -(((kh - 1) + 3) & ~3);            // first ring row, multiple of 4
+  const int bimg_b = bimg_bytes(kh);
+
+  // ---- B images: global -> shared (16-byte copies)
+  {
+    const int n16 = 2 * nkb * bimg_b / 16;
+    uint4* dst = reinterpret_cast<uint4*>(bmats);
+    for (int e = threadIdx.x; e < n16; e += kThreads) dst[e] = bimg[e];
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) split_cnt[i] = 0, epi_cnt[i] = 0;
+    for (int s = 0; s < kND; ++s) mbar_init(&done[s], 1);
+    mbar_init(&ring_ready, 4);
+    fence_mbar_init();
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "n"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_proxy_async();  // B images (generic writes) -> tensor core (async proxy)
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_sh;
+  bool bad = false;
+
+  if (warp < 4) {
+    // ------------------------------------------------------------ split warps
+    // thread u splits samples 8u .. 8u+7 of each row; threads 0..7 also the
+    // tail samples 1024 + 8u .. (the K blocks reach 8*127 + 16 nkb <= 1,080)
+    const int u = threadIdx.x;  // 0..127
+    const int64_t plane = (int64_t)args.h * args.w;
+    const float* xrow0 = xg + (int64_t)img * plane + (int64_t)r0 * args.w;
+    const int w = args.w;
+    const bool vec = (w & 3) == 0;
+    uint32_t mx = 0, mn = 0xffffffffu;
+    auto load8 = [&](const float* rowp, int col, float (&f)[8]) {
+      if (vec && col + 8 <= w) {
+        const float4 a = *reinterpret_cast<const float4*>(rowp + col);
+        const float4 b = *reinterpret_cast<const float4*>(rowp + col + 4);
+        f[0] = a.x, f[1] = a.y, f[2] = a.z, f[3] = a.w;
+        f[4] = b.x, f[5] = b.y, f[6] = b.z, f[7] = b.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = col + j < w ? rowp[col + j] : 0.0f;
+      }
+    };
+    auto split_store = [&](const float (&f)[8], unsigned char* dst) {
+      uint32_t w1[4], w2[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t h = pack_bf16x2(f[2 * j], f[2 * j + 1]);
+        w1[j] = h;
+        w2[j] = pack_bf16x2(f[2 * j] - __uint_as_float(h << 16),
+                            f[2 * j + 1] - __uint_as_float(h & 0xffff0000u));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t bits = __float_as_uint(f[j]) & 0x7fffffffu;
+        mx = max(mx, bits);
+        mn = min(mn, bits - 1u);  // zero -> 0xffffffff (ignored)
+      }
+      *reinterpret_cast<uint4*>(dst) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+      *reinterpret_cast<uint4*>(dst + kXRow) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+    };
+    float cur[kRB][8], tail[kRB][8];
+    auto fetch = [&](int b) {
+#pragma unroll
+      for (int rr = 0; rr < kRB; ++rr) {
+        const int t = min(b * kRB + rr, t_rows - 1);
+        const float* rowp = xrow0 + (int64_t)t * w;
+        load8(rowp, c0 + 8 * u, cur[rr]);
+        if (u < 8) load8(rowp, c0 + kStrip + 8 * u, tail[rr]);
+      }
+    };
+    fetch(0);
+    for (int b = 0; b < n_batches; ++b) {
+      if (b >= kXB) {
+        const int pb = b - kXB;  // the batch that used this slot: its MMAs must be complete
+        mbar_wait(&done[pb % kND], (pb / kND) & 1);
+      }
+      unsigned char* slot0 = xrows + (b % kXB) * kRB * kXSlot;
+#pragma unroll
+      for (int rr = 0; rr < kRB; ++rr) {
+        split_store(cur[rr], slot0 + rr * kXSlot + 16 * u);
+        if (u < 8) split_store(tail[rr], slot0 + rr * kXSlot + 16 * (128 + u));
+      }
+      if (b + 1 < n_batches) fetch(b + 1);  // in flight during the next wait
+      fence_proxy_async();                   // generic writes -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) st_release(&split_cnt[warp], b + 1);
+    }
+    bad = mx > kHiBits || mn < kLoBits - 1u;
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
+    for (int c = 0; c < 512; c += 8) tmem_zero8(lane_base + c);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ring_ready);
+    const int ow = args.ow;
+    const int col = c0 + 8 * (32 * q + lane);  // this thread's 8 output columns
+    float* ybase = y + (int64_t)img * args.oh * ow + col;
+    const bool full = col + 8 <= ow;
+    const int n_epi = (s_valid - o_start + 3) / 4;
+    int batches_done = 0;  // MMA batches known complete (waited in order)
+    for (int e = 0; e < n_epi; ++e) {
+      const int o0 = o_start + 4 * e;
+      const int t_final = min(o0 + 3 + kh - 1, t_rows - 1);
+      for (; batches_done <= t_final / kRB; ++batches_done)
+        mbar_wait(&done[batches_done % kND], (batches_done / kND) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int slot0 = (o0 - o_start) & (kRing - 1);
+      uint32_t v[4][8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tmem_ld8(lane_base + (slot0 + i) * 8, v[i]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tmem_zero8(lane_base + (slot0 + i) * 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int o = o0 + i;
+        if (o >= 0 && o < s_valid && col < ow) {
+          float* yr = ybase + (int64_t)(r0 + o) * ow;
+          if (full && (reinterpret_cast<uintptr_t>(yr) & 15) == 0) {
+            *reinterpret_cast<uint4*>(yr) = make_uint4(v[i][0], v[i][1], v[i][2], v[i][3]);
+            *reinterpret_cast<uint4*>(yr + 4) = make_uint4(v[i][4], v[i][5], v[i][6], v[i][7]);
+          } else {
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              if (col + s < ow) yr[s] = __uint_as_float(v[i][s]);
+          }
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) st_release(&epi_cnt[q], e + 1);
+    }
+  } else {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t bmat_addr = __shfl_sync(0xffffffffu, smem_u32(bmats), 0);
+    const uint32_t xrows_addr = __shfl_sync(0xffffffffu, smem_u32(xrows), 0);
+    mbar_wait(&ring_ready, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    int epi_known = 0;  // epilogue batches known drained
+    for (int b = 0; b < n_batches; ++b) {
+      for (int i = 0; i < 4; ++i)
+        while (ld_acquire(&split_cnt[i]) <= b) {
+        }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int rr = 0; rr < kRB; ++rr) {
+        const int t = b * kRB + rr;
+        if (t >= t_rows) break;
+        const int uo = t - kh + 1;   // first output row this input row feeds
+        const int a = uo & ~3;       // window start (floor to a multiple of 4)
+        const int p = uo - a;        // row phase 0..3
+        // ring slots re-entering the window must be drained and zeroed: rows
+        // below a + nw - kRing, i.e. epilogue batches [0, need)
+        const int need = (a + nw - kRing - o_start + 3) >> 2;
+        if (need > epi_known) {
+          for (int i = 0; i < 4; ++i)
+            while (ld_acquire(&epi_cnt[i]) < need) {
+            }
+          epi_known = need;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        }
+        const uint32_t xsrc = xrows_addr + (uint32_t)((b % kXB) * kRB + rr) * kXSlot;
+        const int q0 = (a - o_start) & (kRing - 1);  // multiple of 4
+        // pieces of the window: split at the ring end and at 32 slots (N <= 256)
+        for (int bs = 0; bs < nw;) {
+          const int qs = (q0 + bs) & (kRing - 1);
+          const int ns = min(min(nw - bs, kRing - qs), 32);
+          const uint32_t idesc = idesc_bf16(128, ns * 8);
+          const uint32_t d = tmem_u + qs * 8;
+          const uint32_t boff = (uint32_t)(kPad - p + bs) * 256;
+          for (int prod = 0; prod < 3; ++prod) {
+            const int xp = prod == 2, fp = prod == 1;  // x1 f1, x1 f2, x2 f1
+            for (int kb = 0; kb < nkb; ++kb) {
+              const uint64_t da = make_desc(xsrc + xp * kXRow + 32 * kb, 16, 128, 0);
+              const uint64_t db =
+                  make_desc(bmat_addr + (uint32_t)(fp * nkb + kb) * bimg_b + boff, 128, 256, 0);
+              mma_ss(d, da, db, idesc);
+            }
+          }
+          bs += ns;
+        }
+      }
+      umma_commit_elect(&done[b % kND]);
+      __syncwarp();
+    }
+  }
+
+  // ---- CTAs with inputs the bf16 split cannot carry: recompute with FMAs in
+  // the reference tap order (reference.py:19-22), overwriting the MMA results
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  const int redo = __syncthreads_or(bad);
+  if (redo) {
+    const int64_t plane_in = (int64_t)args.h * args.w;
+    const float* ximg = xg + (int64_t)img * plane_in;
+    float* yimg = y + (int64_t)img * args.oh * args.ow;
+    const int cols = min(kStrip, args.ow - c0);
+    for (int64_t idx = threadIdx.x; idx < (int64_t)s_valid * cols; idx += kThreads) {
+      const int r = r0 + (int)(idx / cols), c = c0 + (int)(idx % cols);
+      float acc = 0.0f;
+      for (int j = 0; j < kh; ++j)
+        for (int i = 0; i < kw; ++i)
+          acc = fmaf(taps[j * kw + i], ximg[(int64_t)(r + j) * args.w + c + i], acc);
+      yimg[(int64_t)r * args.ow + c] = acc;
+    }
+  }
+  if (warp == 8) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512)
+                 : "memory");
+  }
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+size_t smem_bytes(int kh, int nkb) {
+  return 1024 + (size_t)kXB * kRB * kXSlot + (size_t)2 * nkb * bimg_bytes(kh);
+}
+
+}  // namespace
+
+// Whether the large-filter slide-MMA kernel serves this call (fast mode only).
+bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
+                               int64_t kh, int64_t kw) {
+  const int mode = env_int("SC_CONV_MMA_BIG", 1);  // read per call (A/B in one process)
+  if (!mode || kh < 2 || kh > kMaxKH || kw < 10 || kw > kMaxKW) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || h > 0x7fffffff || w > 0x7fffffff || batch > 65535)
+    return false;
+  if (mode == 1 && kh * kw < 100) return false;
+  // filter taps the bf16 split carries (as in conv2d_mma.cu)
+  for (int64_t i = 0; i < kh * kw; ++i) {
+    const float a = fabsf(f[i]);
+    if (!(a <= 0x1p60f) || (a != 0.0f && a < 0x1p-100f)) return false;
+  }
+  return true;
+}
+
+int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, int64_t kh,
+                   int64_t kw, float* y, cudaStream_t st) {
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  BigMmaArgs a;
+  a.kh = (int)kh, a.kw = (int)kw, a.nkb = (int)((kw + 7 + 15) / 16), a.nw = win_rows((int)kh);
+  a.oh = (int)oh, a.ow = (int)ow, a.h = (int)h, a.w = (int)w;
+  const int64_t strips = (ow + kStrip - 1) / kStrip;
+  // Row segments: one CTA per SM, every CTA costs ~(rows + kh - 1) input
+  // rows plus the pipeline fill; pick the segment length minimising
+  // waves x rows.
+  const int64_t slots = sm_count();
+  int64_t best = -1, rows = oh;
+  const int env_rows = env_int("SC_MMA_BIG_ROWS", 0);
+  if (env_rows > 0) {
+    rows = std::min<int64_t>(env_rows, oh);
+  } else {
+    for (int64_t segs = 1; segs <= std::min<int64_t>(oh, 65535); ++segs) {
+      const int64_t r = (oh + segs - 1) / segs;
+      const int64_t n = batch * strips * ((oh + r - 1) / r);
+      const int64_t cost = (n + slots - 1) / slots * (r + kh - 1 + 12);
+      if (best < 0 || cost < best) best = cost, rows = r;
+      if (r <= 8) break;
+    }
+  }
+  a.seg_rows = (int)rows;
+  const int64_t segs = (oh + rows - 1) / rows;
+  if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
+    return fail(SC_ERR_UNSUPPORTED, "conv2d mma: grid too large");
+
+  static thread_local TapsArg taps;
+  std::copy(f, f + kh * kw, taps.f);
+  const size_t bbytes = (size_t)2 * a.nkb * bimg_bytes(a.kh);
+  unsigned char* scratch = nullptr;
+  SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&scratch), bbytes + (size_t)kh * kw * 4, st));
+  __nv_bfloat16* bimg = reinterpret_cast<__nv_bfloat16*>(scratch);
+  float* taps_dev = reinterpret_cast<float*>(scratch + bbytes);
+  build_b_kernel<<<32, 256, 0, st>>>(taps, a.kh, a.kw, a.nkb, bimg, taps_dev);
+  SC_LAUNCH_CHECK("build_b_kernel");
+  const size_t smem = smem_bytes(a.kh, a.nkb);
+  static uint64_t attr = 0;
+  SC_CUDA(set_smem_limit_once(conv2d_mma_big_kernel, smem_bytes(kMaxKH, kMaxKB), &attr));
+  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
+  conv2d_mma_big_kernel<<<grid, kThreads, smem, st>>>(x, y, reinterpret_cast<const uint4*>(bimg),
+                                                     taps_dev, a);
+  SC_LAUNCH_CHECK("conv2d_mma_big_kernel");
+  SC_CUDA(cudaFreeAsync(scratch, st));
+  return SC_OK;
+}
+
+}  // namespace sc

@@ -59,3 +59,41 @@ tt = t(lambda: sc.sliding_window_mean_max(xh, K))
 print(f"fused host call (chunk {os.environ.get('SC_HOST_CHUNK_MB', 'dflt')} MB): {tt * 1e3:.2f} ms")
 tt = t(lambda: (sc.sliding_window_mean(xh, K), sc.sliding_window_max(xh, K)))
 print(f"two host calls: {tt * 1e3:.2f} ms")
+
+# the pipeline's own pattern with plain copies: chunk i = 16 MB up, then two
+# 16 MB downloads, on slot stream i % 3 (device buffers reused per slot)
+for cmb in (16, 64):
+    cn = (cmb << 20) // 4
+    nchunk = (B * L) // cn
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    din = [torch.empty(cn, device="cuda") for _ in range(3)]
+    xf, y1f, y2f = xt.view(-1), y1.view(-1), y2.view(-1)
+
+    def chunked():
+        for i in range(nchunk):
+            s = streams[i % 3]
+            with torch.cuda.stream(s):
+                din[i % 3].copy_(xf[i * cn:(i + 1) * cn], non_blocking=True)
+                y1f[i * cn:(i + 1) * cn].copy_(din[i % 3], non_blocking=True)
+                y2f[i * cn:(i + 1) * cn].copy_(din[i % 3], non_blocking=True)
+
+    tc = t(chunked)
+    print(f"plain copies, {nchunk} x {cmb} MB chunks (1 up, 2 down) on 3 slot streams: {tc * 1e3:.2f} ms")
+
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    dall = torch.empty(B * L, device="cuda")
+
+    def roles():  # upload runs ahead on its own stream; downloads follow by events
+        evs = []
+        for i in range(nchunk):
+            with torch.cuda.stream(up):
+                dall[i * cn:(i + 1) * cn].copy_(xf[i * cn:(i + 1) * cn], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(up)
+            with torch.cuda.stream(down):
+                down.wait_event(e)
+                y1f[i * cn:(i + 1) * cn].copy_(dall[i * cn:(i + 1) * cn], non_blocking=True)
+                y2f[i * cn:(i + 1) * cn].copy_(dall[i * cn:(i + 1) * cn], non_blocking=True)
+
+    tr = t(roles)
+    print(f"plain copies, {nchunk} x {cmb} MB chunks, upload-ahead role streams: {tr * 1e3:.2f} ms")

@@ -17,8 +17,13 @@ res = {t: [] for t in tpcs}
 for rnd in range(12):
     for t in tpcs:
         os.environ["SC_POOL_TPC"] = str(t)
-        for _ in range(3):
-            fn()
+        t_hot = time.time() + float(os.environ.get("HOT", "0"))  # sustained load first
+        while True:
+            for _ in range(20):
+                fn()
+            torch.cuda.synchronize()
+            if time.time() >= t_hot:
+                break
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         torch.cuda._sleep(int(2e9 * (50 * 100e-6 + 1e-3)))
         e0.record()
