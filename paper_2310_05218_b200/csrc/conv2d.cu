@@ -898,10 +898,19 @@ bool conv2d_mma_applicable(const float* x, int64_t batch, int64_t h, int64_t w, 
 int conv2d_mma(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, int64_t kh,
                int64_t kw, float* y, cudaStream_t st);
 
+bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
+                               int64_t kh, int64_t kw);
+int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, int64_t kh,
+                   int64_t kw, float* y, cudaStream_t st);
+
 int conv2d_f32_dispatch(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                         int64_t kh, int64_t kw, bool exact, float* y, cudaStream_t st) {
   bool done = false;
   int rc = SC_OK;
+  // fast mode, large filters (kw >= 10): the large-filter slide-MMA kernel
+  // (conv2d_mma_big.cu)
+  if (!exact && conv2d_mma_big_applicable(x, batch, h, w, f, kh, kw))
+    return conv2d_mma_big(x, batch, h, w, f, kh, kw, y, st);
   // fast mode, filters of >= 36 taps with kw <= 9, kh <= 15 on large images:
   // the slide-MMA tensor-core kernel (conv2d_mma.cu; FMA-bound otherwise)
   if (!exact && kh * kw >= 36 && conv2d_mma_applicable(x, batch, h, w, f, kh, kw))

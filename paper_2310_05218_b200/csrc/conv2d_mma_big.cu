@@ -57,6 +57,8 @@ constexpr int kXSlot = 2 * kXRow;        // x1 | x2
 constexpr int kND = 32;                  // MMA-completion barriers (one per batch, ring)
 constexpr int kThreads = 32 * 9;
 constexpr int kPad = 3;                  // zero slots in front of the B image (row phase)
+constexpr int kEStride = 9;              // epilogue staging: floats per TMEM lane (8 + 1 pad)
+constexpr int kEStage = 4 * 32 * kEStride * 4;  // bytes per epilogue warp (4 rows x 32 lanes)
 
 __host__ __device__ constexpr int win_rows(int kh) { return (kh + 3 + 1) & ~1; }       // even
 __host__ __device__ constexpr int bimg_slots(int kh) { return kPad + win_rows(kh) + 1; }
@@ -144,7 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base_sh;
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* xrows = base;                                   // kXB * kRB slots
-  unsigned char* bmats = xrows + kXB * kRB * kXSlot;             // 2 * nkb images
+  unsigned char* estage = xrows + kXB * kRB * kXSlot;            // 4 epilogue warps
+  unsigned char* bmats = estage + 4 * kEStage;                   // 2 * nkb images
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kh = args.kh, kw = args.kw, nkb = args.nkb, nw = args.nw;
@@ -260,9 +263,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring_ready);
     const int ow = args.ow;
-    const int col = c0 + 8 * (32 * q + lane);  // this thread's 8 output columns
-    float* ybase = y + (int64_t)img * args.oh * ow + col;
-    const bool full = col + 8 <= ow;
+    // a TMEM lane holds 8 consecutive output columns; the warp's 256 columns
+    // go through a padded shared-memory slab so that every global store is a
+    // coalesced 128-byte row segment whatever the alignment of the output row
+    // (per-lane 32-byte stores cost ~1,000 cycles per output row)
+    float* est = reinterpret_cast<float*>(estage + q * kEStage);
+    const int colw = c0 + 256 * q;  // first column of this warp
+    float* ybase = y + (int64_t)img * args.oh * ow + colw;
     const int n_epi = (s_valid - o_start + 3) / 4;
     int batches_done = 0;  // MMA batches known complete (waited in order)
     for (int e = 0; e < n_epi; ++e) {
@@ -278,20 +285,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 4; ++i) tmem_zero8(lane_base + (slot0 + i) * 8);
+      if (o0 + 3 >= 0 && colw < ow) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int o = o0 + i;
-        if (o >= 0 && o < s_valid && col < ow) {
-          float* yr = ybase + (int64_t)(r0 + o) * ow;
-          if (full && (reinterpret_cast<uintptr_t>(yr) & 15) == 0) {
-            *reinterpret_cast<uint4*>(yr) = make_uint4(v[i][0], v[i][1], v[i][2], v[i][3]);
-            *reinterpret_cast<uint4*>(yr + 4) = make_uint4(v[i][4], v[i][5], v[i][6], v[i][7]);
-          } else {
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-            for (int s = 0; s < 8; ++s)
-              if (col + s < ow) yr[s] = __uint_as_float(v[i][s]);
+          for (int s8 = 0; s8 < 8; ++s8)
+            est[(i * 32 + lane) * kEStride + s8] = __uint_as_float(v[i][s8]);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int o = o0 + i;
+          if (o >= 0 && o < s_valid) {
+            float* yr = ybase + (int64_t)(r0 + o) * ow;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int ee = it * 32 + lane;
+              if (colw + ee < ow) yr[ee] = est[(i * 32 + (ee >> 3)) * kEStride + (ee & 7)];
+            }
           }
         }
+        __syncwarp();
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -384,19 +397,55 @@ int env_int(const char* name, int dflt) {
 }
 
 size_t smem_bytes(int kh, int nkb) {
-  return 1024 + (size_t)kXB * kRB * kXSlot + (size_t)2 * nkb * bimg_bytes(kh);
+  return 1024 + (size_t)kXB * kRB * kXSlot + 4 * (size_t)kEStage + (size_t)2 * nkb * bimg_bytes(kh);
+}
+
+
+// Row segments: one CTA per SM, every CTA costs ~(rows + kh - 1) input rows
+// plus the pipeline fill; pick the segment length minimising waves x rows.
+// Returns the output rows per segment and the modelled rows per SM.
+int64_t plan_rows(int64_t batch, int64_t oh, int64_t ow, int64_t kh, int64_t* cost_rows) {
+  const int64_t strips = (ow + kStrip - 1) / kStrip;
+  const int64_t slots = sm_count();
+  int64_t best = -1, rows = oh;
+  for (int64_t segs = 1; segs <= std::min<int64_t>(oh, 65535); ++segs) {
+    const int64_t r = (oh + segs - 1) / segs;
+    const int64_t n = batch * strips * ((oh + r - 1) / r);
+    const int64_t cost = (n + slots - 1) / slots * (r + kh - 1 + 12);
+    if (best < 0 || cost < best) best = cost, rows = r;
+    if (r <= 8) break;
+  }
+  if (cost_rows) *cost_rows = best;
+  return rows;
 }
 
 }  // namespace
 
-// Whether the large-filter slide-MMA kernel serves this call (fast mode only).
+// Whether the large-filter slide-MMA kernel serves this call (fast mode
+// only).  SC_CONV_MMA_BIG: 0 off, 1 (default) when the modelled tensor-core
+// time beats the FFMA kernels', 2 whenever the shape fits.
 bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t w, const float* f,
                                int64_t kh, int64_t kw) {
   const int mode = env_int("SC_CONV_MMA_BIG", 1);  // read per call (A/B in one process)
-  if (!mode || kh < 2 || kh > kMaxKH || kw < 10 || kw > kMaxKW) return false;
-  if ((reinterpret_cast<uintptr_t>(x) & 15) || h > 0x7fffffff || w > 0x7fffffff || batch > 65535)
+  if (!mode || kh < 2 || kh > kMaxKH || kw < 2 || kw > kMaxKW) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || h > 0x7fffffff || w > 0x7fffffff || batch > 65535 ||
+      batch < 1)
     return false;
-  if (mode == 1 && kh * kw < 100) return false;
+  const int64_t oh = h - kh + 1, ow = w - kw + 1;
+  if (mode == 1) {
+    if (kh * kw < 150) return false;
+    // cycles per SM: the issuer needs ~115 cycles per MMA (3 products x K
+    // blocks x window pieces per input row) and ~1,500 per row at least; the
+    // FFMA kernels sustain ~55 % of the FP32 pipe on full grids (measured,
+    // tools/mma_big_check.py: the model picks the faster side on the sweep)
+    int64_t cost_rows = 0;
+    plan_rows(batch, oh, ow, kh, &cost_rows);
+    const int nkb = (int)((kw + 7 + 15) / 16), nw = win_rows((int)kh);
+    const double n_mma = 3.0 * nkb * ((nw + 31) / 32 + 0.3);
+    const double t_mma = (double)cost_rows * std::max(1500.0, 115.0 * n_mma);
+    const double t_ffma = (double)batch * oh * ow * kh * kw / (sm_count() * 128.0 * 0.55);
+    if (t_mma > 0.8 * t_ffma) return false;
+  }
   // filter taps the bf16 split carries (as in conv2d_mma.cu)
   for (int64_t i = 0; i < kh * kw; ++i) {
     const float a = fabsf(f[i]);
@@ -412,23 +461,9 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   a.kh = (int)kh, a.kw = (int)kw, a.nkb = (int)((kw + 7 + 15) / 16), a.nw = win_rows((int)kh);
   a.oh = (int)oh, a.ow = (int)ow, a.h = (int)h, a.w = (int)w;
   const int64_t strips = (ow + kStrip - 1) / kStrip;
-  // Row segments: one CTA per SM, every CTA costs ~(rows + kh - 1) input
-  // rows plus the pipeline fill; pick the segment length minimising
-  // waves x rows.
-  const int64_t slots = sm_count();
-  int64_t best = -1, rows = oh;
   const int env_rows = env_int("SC_MMA_BIG_ROWS", 0);
-  if (env_rows > 0) {
-    rows = std::min<int64_t>(env_rows, oh);
-  } else {
-    for (int64_t segs = 1; segs <= std::min<int64_t>(oh, 65535); ++segs) {
-      const int64_t r = (oh + segs - 1) / segs;
-      const int64_t n = batch * strips * ((oh + r - 1) / r);
-      const int64_t cost = (n + slots - 1) / slots * (r + kh - 1 + 12);
-      if (best < 0 || cost < best) best = cost, rows = r;
-      if (r <= 8) break;
-    }
-  }
+  const int64_t rows =
+      env_rows > 0 ? std::min<int64_t>(env_rows, oh) : plan_rows(batch, oh, ow, kh, nullptr);
   a.seg_rows = (int)rows;
   const int64_t segs = (oh + rows - 1) / rows;
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)

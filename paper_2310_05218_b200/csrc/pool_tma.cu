@@ -334,7 +334,7 @@ int launch_nbuf(const float* x, int64_t batch, int64_t length, float* y, cudaStr
       kOp == SC_POOL_SUM ? (K <= 24 ? 2 : 4)
       : kOp == SC_POOL_AVG ? ((kPow2 && K <= 16) || K == 3 ? 2 : 4)
       : kOp == SC_POOL_MAX ? (K <= 8 ? 2 : 4)
-      : (kOp == kPairSum || kOp == kPairAvg) ? (K <= 16 ? 2 : 4)  // k = 16: 121.7 us at 2, 123.1 at 4
+      : (kOp == kPairSum || kOp == kPairAvg) ? 4  // k = 16 under sustained load: 129.5 us at 4, 134.2 at 2
       : 2;  // weighted (conv1d) windows
   const int tpc = env_int("SC_POOL_TPC", kTpcDefault, 1, 64);
   const int64_t grid = (n_tiles + tpc - 1) / tpc;
