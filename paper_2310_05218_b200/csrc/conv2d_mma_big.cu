@@ -20,20 +20,26 @@
 // starts on a multiple of 4 rows (D offsets are multiples of 32 columns), the
 // remaining 0..3 row phase is a 256-byte offset into a zero-padded B image.
 //
-// Precision: x = x1 + x2, f = f1 + f2 (bf16, round to nearest); D
-// accumulates x1 f1 + x1 f2 + x2 f1 in fp32 (the x2 f2 term is ~2^-18 of a
-// product), ~4e-6 normwise against the north-star 1e-5 k.  CTAs whose inputs
-// the split cannot carry (|x| > 2^64, non-finite, nonzero |x| < 2^-100)
-// recompute their outputs with FMAs in the reference tap order afterwards.
+// Precision: a scaled fp16 split.  The CTA first scans its input rows for
+// the largest magnitude and scales x by a power of two to just under 2^15;
+// the filter is scaled the same way on the host.  x' = x1 + x2, f' = f1 + f2
+// with fp16 parts (11 significant bits each, so a pair carries ~22 bits of
+// the scaled value; samples below 2^-24 of the CTA's maximum lose bits, which
+// is an ABSOLUTE error of ~2^-25 of that maximum, i.e. fp32-accumulation
+// class); D accumulates x1 f1 + x1 f2 + x2 f1 in fp32 (the x2 f2 term is
+// ~2^-24 of a product) and the epilogue undoes the two power-of-two scales
+// (exact).  Measured ~1e-7 normwise, like the FFMA kernels.  CTAs whose
+// inputs hold inf / NaN or magnitudes outside [2^-87, 2^73] skip the tensor
+// cores and compute their outputs with FMAs in the reference tap order.
 //
-// Warps: 0-3 split (global fp32 row -> x1 / x2 bf16 rows in shared memory,
+// Warps: 0-3 split (global fp32 row -> x1 / x2 fp16 rows in shared memory,
 // 4 rows per batch, the next batch's loads in flight while waiting for a
 // slot), 4-7 epilogue (one TMEM lane quarter each, 4 output rows per batch),
 // 8 MMA issuer (3 products x K blocks x window pieces per input row, one
 // commit per batch).  Hand-offs are per batch of 4 rows (~1,000-12,000 tensor
 // cycles of work), so plain counters / mbarriers suffice.
 #include <cuda.h>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -52,7 +58,7 @@ constexpr int kXB = 3;                   // batches of split rows in shared memo
 constexpr int kRing = 64;                // output-row slots in TMEM (8 columns each)
 constexpr int kMaxKH = 53, kMaxKW = 57;
 constexpr int kMaxKB = 4;                // K blocks of 16 samples: 16 n_kb >= kw + 7
-constexpr int kXRow = 2176;              // bytes per bf16 row (1,080 samples used)
+constexpr int kXRow = 2176;              // bytes per fp16 row (1,080 samples used)
 constexpr int kXSlot = 2 * kXRow;        // x1 | x2
 constexpr int kND = 32;                  // MMA-completion barriers (one per batch, ring)
 constexpr int kThreads = 32 * 9;
@@ -68,19 +74,21 @@ struct BigMmaArgs {
   int kh, kw, nkb, nw;
   int oh, ow, h, w;
   int seg_rows;
+  float f_scale, f_unscale;  // 2^sf applied to the taps, and 2^-sf
 };
 
 struct TapsArg {
   float f[kMaxKH * kMaxKW];
 };
 
-// B images in global memory, [part f1 / f2][kb][slot][k half][s][k & 7] bf16:
+// B images in global memory, [part f1 / f2][kb][slot][k half][s][k & 7] fp16:
 // element (n = 8 slot + s, k) of the no-swizzle K-major layout (LBO 128 B
 // between the k halves, SBO 256 B per 8 rows); slot = kPad + jslot holds
 // filter row j = kh - 1 - jslot, zeros elsewhere.  Then the fp32 taps (for
 // the FMA fallback).
 __global__ void build_b_kernel(const __grid_constant__ TapsArg taps, int kh, int kw, int nkb,
-                               __nv_bfloat16* __restrict__ bimg, float* __restrict__ taps_out) {
+                               float f_scale, __half* __restrict__ bimg,
+                               float* __restrict__ taps_out) {
   const int slots = bimg_slots(kh);
   const int per = slots * 128;  // elements per (part, kb) image
   const int total = 2 * nkb * per;
@@ -91,12 +99,24 @@ __global__ void build_b_kernel(const __grid_constant__ TapsArg taps, int kh, int
     const int k = 8 * kh2 + k7;
     const int jslot = slot - kPad, j = kh - 1 - jslot, i = 16 * kb + k - s;
     float v = 0.0f;
-    if (jslot >= 0 && j >= 0 && i >= 0 && i < kw) v = taps.f[j * kw + i];
-    const __nv_bfloat16 v1 = __float2bfloat16_rn(v);
-    bimg[e] = part ? __float2bfloat16_rn(v - __bfloat162float(v1)) : v1;
+    if (jslot >= 0 && j >= 0 && i >= 0 && i < kw) v = taps.f[j * kw + i] * f_scale;
+    const __half v1 = __float2half_rn(v);
+    bimg[e] = part ? __float2half_rn(v - __half2float(v1)) : v1;
   }
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kh * kw; e += gridDim.x * blockDim.x)
     taps_out[e] = taps.f[e];
+}
+
+// kind::f16 instruction descriptor with fp16 A / B (format 0), D f32,
+// both K-major (tc_common.cuh idesc_bf16 sets format 1 = bf16)
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t da, uint64_t db, uint32_t idesc) {
@@ -132,8 +152,8 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-// 2^64 / 2^-100 as float bit patterns (magnitudes the bf16 split carries)
-constexpr uint32_t kHiBits = 0x5F800000u, kLoBits = 0x0D800000u;
+// biased exponents of the largest input magnitude a CTA scales (2^-87 .. 2^73)
+constexpr int kExpLo = 40, kExpHi = 200;
 
 __global__ void __launch_bounds__(kThreads, 1)
     conv2d_mma_big_kernel(const float* __restrict__ xg, float* __restrict__ y,
@@ -184,9 +204,56 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
-  bool bad = false;
 
-  if (warp < 4) {
+  // ---- range scan of the CTA's input rows (all threads): largest magnitude
+  // -> power-of-two scale; inf / NaN or an extreme range -> FMA fallback
+  __shared__ uint32_t xmax_sh;
+  if (threadIdx.x == 0) xmax_sh = 0;
+  __syncthreads();
+  {
+    const float* xrow0 = xg + (int64_t)img * args.h * args.w + (int64_t)r0 * args.w;
+    const int w = args.w;
+    const int span = min(kStrip + 16 * nkb + 8, w - c0);  // samples the K blocks reach
+    uint32_t mx = 0;
+    auto amax4 = [](uint32_t m, const float4 v) {
+      return max(max(m, __float_as_uint(v.x) & 0x7fffffffu),
+                 max(__float_as_uint(v.y) & 0x7fffffffu,
+                     max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
+    };
+    if ((w & 3) == 0) {
+      // 16 rows per step: 16 independent 16-byte loads in flight per thread
+      const int n4 = span >> 2;  // c0 and w are multiples of 4
+      const int w4 = w >> 2;
+      const float4* rp0 = reinterpret_cast<const float4*>(xrow0 + c0);
+      for (int e = threadIdx.x; e < n4; e += kThreads) {
+        for (int t = 0; t < t_rows; t += 16) {
+          float4 v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = rp0[(int64_t)min(t + j, t_rows - 1) * w4 + e];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) mx = amax4(mx, v[j]);
+        }
+      }
+    } else {
+      for (int t = 0; t < t_rows; ++t) {
+        const float* rp = xrow0 + (int64_t)t * w + c0;
+        for (int e = threadIdx.x; e < span; e += kThreads)
+          mx = max(mx, __float_as_uint(rp[e]) & 0x7fffffffu);
+      }
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) atomicMax(&xmax_sh, mx);
+  }
+  __syncthreads();
+  const int xexp = (int)(xmax_sh >> 23);  // biased exponent of the largest magnitude
+  // all-zero input: any scale works; otherwise 2^(14 - exponent) puts the maximum in [2^14, 2^15)
+  const bool bad = xmax_sh != 0 && (xexp < kExpLo || xexp > kExpHi);
+  const float x_scale = xmax_sh == 0 ? 1.0f : __uint_as_float((uint32_t)(268 - xexp) << 23);
+  const float x_unscale = xmax_sh == 0 ? 1.0f : __uint_as_float((uint32_t)(xexp - 14) << 23);
+
+  if (bad) {
+    // no tensor-core pass for this CTA (see the fallback below)
+  } else if (warp < 4) {
     // ------------------------------------------------------------ split warps
     // thread u splits samples 8u .. 8u+7 of each row; threads 0..7 also the
     // tail samples 1024 + 8u .. (the K blocks reach 8*127 + 16 nkb <= 1,080)
@@ -195,7 +262,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float* xrow0 = xg + (int64_t)img * plane + (int64_t)r0 * args.w;
     const int w = args.w;
     const bool vec = (w & 3) == 0;
-    uint32_t mx = 0, mn = 0xffffffffu;
     auto load8 = [&](const float* rowp, int col, float (&f)[8]) {
       if (vec && col + 8 <= w) {
         const float4 a = *reinterpret_cast<const float4*>(rowp + col);
@@ -211,16 +277,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t w1[4], w2[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const uint32_t h = pack_bf16x2(f[2 * j], f[2 * j + 1]);
+        const float a = f[2 * j] * x_scale, b = f[2 * j + 1] * x_scale;
+        const uint32_t h = pack_f16x2(a, b);
+        const float2 hf = __half22float2(*reinterpret_cast<const __half2*>(&h));
         w1[j] = h;
-        w2[j] = pack_bf16x2(f[2 * j] - __uint_as_float(h << 16),
-                            f[2 * j + 1] - __uint_as_float(h & 0xffff0000u));
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t bits = __float_as_uint(f[j]) & 0x7fffffffu;
-        mx = max(mx, bits);
-        mn = min(mn, bits - 1u);  // zero -> 0xffffffff (ignored)
+        w2[j] = pack_f16x2(a - hf.x, b - hf.y);
       }
       *reinterpret_cast<uint4*>(dst) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
       *reinterpret_cast<uint4*>(dst + kXRow) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
@@ -252,7 +313,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) st_release(&split_cnt[warp], b + 1);
     }
-    bad = mx > kHiBits || mn < kLoBits - 1u;
   } else if (warp < 8) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter
@@ -263,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&ring_ready);
     const int ow = args.ow;
+    const float f_unscale = args.f_unscale;
     // a TMEM lane holds 8 consecutive output columns; the warp's 256 columns
     // go through a padded shared-memory slab so that every global store is a
     // coalesced 128-byte row segment whatever the alignment of the output row
@@ -290,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int s8 = 0; s8 < 8; ++s8)
-            est[(i * 32 + lane) * kEStride + s8] = __uint_as_float(v[i][s8]);
+            est[(i * 32 + lane) * kEStride + s8] = __uint_as_float(v[i][s8]) * x_unscale * f_unscale;
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -346,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int bs = 0; bs < nw;) {
           const int qs = (q0 + bs) & (kRing - 1);
           const int ns = min(min(nw - bs, kRing - qs), 32);
-          const uint32_t idesc = idesc_bf16(128, ns * 8);
+          const uint32_t idesc = idesc_f16(128, ns * 8);
           const uint32_t d = tmem_u + qs * 8;
           const uint32_t boff = (uint32_t)(kPad - p + bs) * 256;
           for (int prod = 0; prod < 3; ++prod) {
@@ -366,11 +427,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  // ---- CTAs with inputs the bf16 split cannot carry: recompute with FMAs in
+  // ---- CTAs whose inputs the scaled split cannot carry: compute with FMAs in
   // the reference tap order (reference.py:19-22), overwriting the MMA results
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  const int redo = __syncthreads_or(bad);
-  if (redo) {
+  __syncthreads();
+  if (bad) {
     const int64_t plane_in = (int64_t)args.h * args.w;
     const float* ximg = xg + (int64_t)img * plane_in;
     float* yimg = y + (int64_t)img * args.oh * args.ow;
@@ -446,12 +507,14 @@ bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t
     const double t_ffma = (double)batch * oh * ow * kh * kw / (sm_count() * 128.0 * 0.55);
     if (t_mma > 0.8 * t_ffma) return false;
   }
-  // filter taps the bf16 split carries (as in conv2d_mma.cu)
+  // a finite filter whose largest tap the power-of-two scale can carry
+  float fmax = 0.0f;
   for (int64_t i = 0; i < kh * kw; ++i) {
     const float a = fabsf(f[i]);
-    if (!(a <= 0x1p60f) || (a != 0.0f && a < 0x1p-100f)) return false;
+    if (!(a <= 0x1p60f)) return false;
+    fmax = std::max(fmax, a);
   }
-  return true;
+  return fmax >= 0x1p-60f;
 }
 
 int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const float* f, int64_t kh,
@@ -469,14 +532,20 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
     return fail(SC_ERR_UNSUPPORTED, "conv2d mma: grid too large");
 
+  float fmax = 0.0f;
+  for (int64_t i = 0; i < kh * kw; ++i) fmax = std::max(fmax, fabsf(f[i]));
+  int fe = 0;
+  frexpf(fmax, &fe);                       // fmax = m 2^fe, m in [0.5, 1)
+  a.f_scale = ldexpf(1.0f, 14 - fe);       // largest tap in [2^13, 2^14)
+  a.f_unscale = ldexpf(1.0f, fe - 14);
   static thread_local TapsArg taps;
   std::copy(f, f + kh * kw, taps.f);
   const size_t bbytes = (size_t)2 * a.nkb * bimg_bytes(a.kh);
   unsigned char* scratch = nullptr;
   SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&scratch), bbytes + (size_t)kh * kw * 4, st));
-  __nv_bfloat16* bimg = reinterpret_cast<__nv_bfloat16*>(scratch);
+  __half* bimg = reinterpret_cast<__half*>(scratch);
   float* taps_dev = reinterpret_cast<float*>(scratch + bbytes);
-  build_b_kernel<<<32, 256, 0, st>>>(taps, a.kh, a.kw, a.nkb, bimg, taps_dev);
+  build_b_kernel<<<32, 256, 0, st>>>(taps, a.kh, a.kw, a.nkb, a.f_scale, bimg, taps_dev);
   SC_LAUNCH_CHECK("build_b_kernel");
   const size_t smem = smem_bytes(a.kh, a.nkb);
   static uint64_t attr = 0;
