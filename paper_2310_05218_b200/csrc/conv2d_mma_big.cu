@@ -75,7 +75,13 @@ struct BigMmaArgs {
   int oh, ow, h, w;
   int seg_rows;
   float f_scale, f_unscale;  // 2^sf applied to the taps, and 2^-sf
+  long long* trace;          // SC_MMA_BIG_TRACE: clock64 stamps of CTA (0, 0, 0), [role][index]
 };
+#define BIG_TRACE(role, idx, v)                                                              \
+  do {                                                                                       \
+    if (args.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (idx) < 1024) \
+      args.trace[(role) * 1024 + (idx)] = (v);                                               \
+  } while (0)
 
 struct TapsArg {
   float f[kMaxKH * kMaxKW];
@@ -155,6 +161,7 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 // biased exponents of the largest input magnitude a CTA scales (2^-87 .. 2^73)
 constexpr int kExpLo = 40, kExpHi = 200;
 
+template <int NKB>
 __global__ void __launch_bounds__(kThreads, 1)
     conv2d_mma_big_kernel(const float* __restrict__ xg, float* __restrict__ y,
                           const uint4* __restrict__ bimg, const float* __restrict__ taps,
@@ -170,7 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* bmats = estage + 4 * kEStage;                   // 2 * nkb images
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kh = args.kh, kw = args.kw, nkb = args.nkb, nw = args.nw;
+  constexpr int nkb = NKB;  // K blocks: compile-time so a piece's MMAs issue as one unrolled block
+  const int kh = args.kh, kw = args.kw, nw = args.nw;
   const int c0 = blockIdx.x * kStrip;
   const int r0 = blockIdx.y * args.seg_rows;
   const int img = blockIdx.z;
@@ -204,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_sh;
+  if (threadIdx.x == 0) BIG_TRACE(7, 0, clock64());
 
   // ---- range scan of the CTA's input rows (all threads): largest magnitude
   // -> power-of-two scale; inf / NaN or an extreme range -> FMA fallback
@@ -245,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) atomicMax(&xmax_sh, mx);
   }
   __syncthreads();
+  if (threadIdx.x == 0) BIG_TRACE(7, 1, clock64());
   const int xexp = (int)(xmax_sh >> 23);  // biased exponent of the largest magnitude
   // all-zero input: any scale works; otherwise 2^(14 - exponent) puts the maximum in [2^14, 2^15)
   const bool bad = xmax_sh != 0 && (xexp < kExpLo || xexp > kExpHi);
@@ -255,13 +265,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     // no tensor-core pass for this CTA (see the fallback below)
   } else if (warp < 4) {
     // ------------------------------------------------------------ split warps
-    // thread u splits samples 8u .. 8u+7 of each row; threads 0..7 also the
-    // tail samples 1024 + 8u .. (the K blocks reach 8*127 + 16 nkb <= 1,080)
+    // A batch is kRB rows x 136 chunks of 8 samples (column c0 + 8 cc -> byte
+    // 16 cc of the row's x1 / x2 slots; the K blocks reach 8*127 + 16 nkb + 15
+    // <= 1,087).  Thread u owns chunks u + 128 j (j = 0..3, and j = 4 for
+    // u < 32) of every batch.  Two batches of loads are kept in flight in
+    // registers: with one, the load latency was exposed once per batch
+    // (~750 cycles per input row with no MMAs at all).
+    constexpr int kChunks = 136, kOwn = 5;
     const int u = threadIdx.x;  // 0..127
     const int64_t plane = (int64_t)args.h * args.w;
     const float* xrow0 = xg + (int64_t)img * plane + (int64_t)r0 * args.w;
     const int w = args.w;
     const bool vec = (w & 3) == 0;
+    int crow[kOwn], ccol[kOwn];
+#pragma unroll
+    for (int j = 0; j < kOwn; ++j) {
+      const int c = u + 128 * j;
+      crow[j] = c / kChunks;
+      ccol[j] = c - crow[j] * kChunks;
+    }
+    const bool own4 = u < kRB * kChunks - 512;  // chunk 512 + u exists
     auto load8 = [&](const float* rowp, int col, float (&f)[8]) {
       if (vec && col + 8 <= w) {
         const float4 a = *reinterpret_cast<const float4*>(rowp + col);
@@ -286,32 +309,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       *reinterpret_cast<uint4*>(dst) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
       *reinterpret_cast<uint4*>(dst + kXRow) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
     };
-    float cur[kRB][8], tail[kRB][8];
-    auto fetch = [&](int b) {
+    auto fetch = [&](int b, float (&buf)[kOwn][8]) {
 #pragma unroll
-      for (int rr = 0; rr < kRB; ++rr) {
-        const int t = min(b * kRB + rr, t_rows - 1);
-        const float* rowp = xrow0 + (int64_t)t * w;
-        load8(rowp, c0 + 8 * u, cur[rr]);
-        if (u < 8) load8(rowp, c0 + kStrip + 8 * u, tail[rr]);
+      for (int j = 0; j < kOwn; ++j) {
+        if (j == kOwn - 1 && !own4) break;
+        const int t = min(b * kRB + crow[j], t_rows - 1);
+        load8(xrow0 + (int64_t)t * w, c0 + 8 * ccol[j], buf[j]);
       }
     };
-    fetch(0);
-    for (int b = 0; b < n_batches; ++b) {
+    auto emit = [&](int b, const float (&buf)[kOwn][8]) {
       if (b >= kXB) {
         const int pb = b - kXB;  // the batch that used this slot: its MMAs must be complete
         mbar_wait(&done[pb % kND], (pb / kND) & 1);
       }
+      if (threadIdx.x == 0) BIG_TRACE(0, b, clock64());
       unsigned char* slot0 = xrows + (b % kXB) * kRB * kXSlot;
 #pragma unroll
-      for (int rr = 0; rr < kRB; ++rr) {
-        split_store(cur[rr], slot0 + rr * kXSlot + 16 * u);
-        if (u < 8) split_store(tail[rr], slot0 + rr * kXSlot + 16 * (128 + u));
+      for (int j = 0; j < kOwn; ++j) {
+        if (j == kOwn - 1 && !own4) break;
+        split_store(buf[j], slot0 + crow[j] * kXSlot + 16 * ccol[j]);
       }
-      if (b + 1 < n_batches) fetch(b + 1);  // in flight during the next wait
-      fence_proxy_async();                   // generic writes -> tensor-core reads
+    };
+    auto publish = [&](int b) {
+      fence_proxy_async();  // generic writes -> tensor-core reads
       __syncwarp();
       if (lane == 0) st_release(&split_cnt[warp], b + 1);
+      if (threadIdx.x == 0) BIG_TRACE(1, b, clock64());
+    };
+    float buf0[kOwn][8], buf1[kOwn][8];
+    fetch(0, buf0);
+    if (n_batches > 1) fetch(1, buf1);
+    for (int b = 0; b < n_batches; b += 2) {
+      emit(b, buf0);
+      if (b + 2 < n_batches) fetch(b + 2, buf0);
+      publish(b);
+      if (b + 1 < n_batches) {
+        emit(b + 1, buf1);
+        if (b + 3 < n_batches) fetch(b + 3, buf1);
+        publish(b + 1);
+      }
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ epilogue
@@ -339,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (; batches_done <= t_final / kRB; ++batches_done)
         mbar_wait(&done[batches_done % kND], (batches_done / kND) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (warp == 4 && lane == 0) BIG_TRACE(5, e, clock64());
       const int slot0 = (o0 - o_start) & (kRing - 1);
       uint32_t v[4][8];
 #pragma unroll
@@ -371,6 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) st_release(&epi_cnt[q], e + 1);
+      if (warp == 4 && lane == 0) BIG_TRACE(6, e, clock64());
     }
   } else {
     // ------------------------------------------------------------ MMA issuer
@@ -381,9 +419,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     int epi_known = 0;  // epilogue batches known drained
     for (int b = 0; b < n_batches; ++b) {
+      if (lane == 0) BIG_TRACE(2, b, clock64());
       for (int i = 0; i < 4; ++i)
         while (ld_acquire(&split_cnt[i]) <= b) {
         }
+      if (lane == 0) BIG_TRACE(3, b, clock64());
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int rr = 0; rr < kRB; ++rr) {
         const int t = b * kRB + rr;
@@ -410,20 +450,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t idesc = idesc_f16(128, ns * 8);
           const uint32_t d = tmem_u + qs * 8;
           const uint32_t boff = (uint32_t)(kPad - p + bs) * 256;
+          // descriptors differ only in their 14-bit address fields: one base
+          // each, then plain adds (a row's samples stay inside one 16 KiB
+          // window of the field, as do the B images)
+          const uint64_t da0 = make_desc(xsrc, 16, 128, 0);
+          const uint64_t db0 = make_desc(bmat_addr + boff, 128, 256, 0);
+          const uint32_t bstep = (uint32_t)bimg_b >> 4;
+#pragma unroll
           for (int prod = 0; prod < 3; ++prod) {
             const int xp = prod == 2, fp = prod == 1;  // x1 f1, x1 f2, x2 f1
-            for (int kb = 0; kb < nkb; ++kb) {
-              const uint64_t da = make_desc(xsrc + xp * kXRow + 32 * kb, 16, 128, 0);
-              const uint64_t db =
-                  make_desc(bmat_addr + (uint32_t)(fp * nkb + kb) * bimg_b + boff, 128, 256, 0);
-              mma_ss(d, da, db, idesc);
-            }
+#pragma unroll
+            for (int kb = 0; kb < nkb; ++kb)
+              mma_ss(d, da0 + (uint32_t)(xp * (kXRow >> 4) + 2 * kb),
+                     db0 + (uint64_t)((fp * nkb + kb) * bstep), idesc);
           }
           bs += ns;
         }
       }
       umma_commit_elect(&done[b % kND]);
       __syncwarp();
+      if (lane == 0) BIG_TRACE(4, b, clock64());
     }
   }
 
@@ -495,17 +541,18 @@ bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t
   const int64_t oh = h - kh + 1, ow = w - kw + 1;
   if (mode == 1) {
     if (kh * kw < 150) return false;
-    // cycles per SM: the issuer needs ~115 cycles per MMA (3 products x K
-    // blocks x window pieces per input row) and ~1,500 per row at least; the
-    // FFMA kernels sustain ~55 % of the FP32 pipe on full grids (measured,
+    // cycles per SM: ~115 per MMA (3 products x K blocks x window pieces per
+    // input row; issue-bound for short windows, tensor-bound from N ~ 200),
+    // ~900 per row at least, ~30,000 for the range scan and fill; the FFMA
+    // kernels sustain ~55 % of the FP32 pipe on full grids (measured,
     // tools/mma_big_check.py: the model picks the faster side on the sweep)
     int64_t cost_rows = 0;
     plan_rows(batch, oh, ow, kh, &cost_rows);
     const int nkb = (int)((kw + 7 + 15) / 16), nw = win_rows((int)kh);
     const double n_mma = 3.0 * nkb * ((nw + 31) / 32 + 0.3);
-    const double t_mma = (double)cost_rows * std::max(1500.0, 115.0 * n_mma);
+    const double t_mma = (double)cost_rows * std::max(900.0, 115.0 * n_mma) + 30000.0;
     const double t_ffma = (double)batch * oh * ow * kh * kw / (sm_count() * 128.0 * 0.55);
-    if (t_mma > 0.8 * t_ffma) return false;
+    if (t_mma > 0.75 * t_ffma) return false;
   }
   // a finite filter whose largest tap the power-of-two scale can carry
   float fmax = 0.0f;
@@ -523,6 +570,8 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   BigMmaArgs a;
   a.kh = (int)kh, a.kw = (int)kw, a.nkb = (int)((kw + 7 + 15) / 16), a.nw = win_rows((int)kh);
   a.oh = (int)oh, a.ow = (int)ow, a.h = (int)h, a.w = (int)w;
+  a.trace = nullptr;
+  if (const char* e = getenv("SC_MMA_BIG_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
   const int64_t strips = (ow + kStrip - 1) / kStrip;
   const int env_rows = env_int("SC_MMA_BIG_ROWS", 0);
   const int64_t rows =
@@ -548,11 +597,20 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   build_b_kernel<<<32, 256, 0, st>>>(taps, a.kh, a.kw, a.nkb, a.f_scale, bimg, taps_dev);
   SC_LAUNCH_CHECK("build_b_kernel");
   const size_t smem = smem_bytes(a.kh, a.nkb);
-  static uint64_t attr = 0;
-  SC_CUDA(set_smem_limit_once(conv2d_mma_big_kernel, smem_bytes(kMaxKH, kMaxKB), &attr));
   dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
-  conv2d_mma_big_kernel<<<grid, kThreads, smem, st>>>(x, y, reinterpret_cast<const uint4*>(bimg),
-                                                     taps_dev, a);
+  const uint4* bimg4 = reinterpret_cast<const uint4*>(bimg);
+  auto launch = [&](auto kernel, uint64_t* done_attr) -> cudaError_t {
+    cudaError_t e = set_smem_limit_once(kernel, smem_bytes(kMaxKH, kMaxKB), done_attr);
+    if (e == cudaSuccess) kernel<<<grid, kThreads, smem, st>>>(x, y, bimg4, taps_dev, a);
+    return e;
+  };
+  static uint64_t attrs[kMaxKB] = {};
+  switch (a.nkb) {
+    case 1: SC_CUDA(launch(conv2d_mma_big_kernel<1>, &attrs[0])); break;
+    case 2: SC_CUDA(launch(conv2d_mma_big_kernel<2>, &attrs[1])); break;
+    case 3: SC_CUDA(launch(conv2d_mma_big_kernel<3>, &attrs[2])); break;
+    default: SC_CUDA(launch(conv2d_mma_big_kernel<4>, &attrs[3])); break;
+  }
   SC_LAUNCH_CHECK("conv2d_mma_big_kernel");
   SC_CUDA(cudaFreeAsync(scratch, st));
   return SC_OK;

@@ -1,0 +1,32 @@
+"""Per-role clock64 timeline of CTA (0,0,0) of the large-filter slide-MMA
+kernel: python tools/mma_big_trace.py B H W K"""
+import os, sys
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2310_05218_b200 as sc
+b, h, w, k = (int(v) for v in sys.argv[1:5])
+x = torch.rand((b, h, w), device="cuda") * 2 - 1
+f = (np.random.default_rng(k).standard_normal((k, k)) / k).astype(np.float32)
+tr = torch.zeros(8 * 1024, dtype=torch.int64, device="cuda")
+os.environ["SC_CONV_MMA_BIG"] = "2"
+for _ in range(2):
+    sc.conv2d_reference(x, f, exact=False)
+os.environ["SC_MMA_BIG_TRACE"] = hex(tr.data_ptr())
+sc.conv2d_reference(x, f, exact=False)
+torch.cuda.synchronize()
+t = tr.cpu().numpy().reshape(8, 1024)
+t0 = t[7, 0]
+print("prepass", t[7, 1] - t0)
+names = ["split_wait_done", "split_publish", "iss_begin", "iss_split_ready", "iss_commit", "epi_begin", "epi_end"]
+n = int((t[4] > 0).sum())
+print("batches", n)
+print("b  " + " ".join(f"{s:>16}" for s in names))
+for i in list(range(0, min(n, 12))) + list(range(max(12, n - 4), n)):
+    print(f"{i:<3}" + " ".join(f"{(t[r, i] - t0) if t[r, i] else -1:>16}" for r in range(7)))
+d = np.diff(t[4, :n])
+print("issuer period per batch: median", np.median(d), "mean", d.mean())
+print("issue time per batch (commit - split_ready): median", np.median(t[4, :n] - t[3, :n]))
+print("split: publish - wait_done median", np.median(t[1, :n] - t[0, :n]))
+ne = int((t[6] > 0).sum())
+print("epilogue body median", np.median(t[6, :ne] - t[5, :ne]), "batches", ne)
