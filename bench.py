@@ -420,6 +420,29 @@ def per_config(torch, sc, hbm_peak, args, traffic):
                                              4 * (262 * 65536 + 256 * 65530), 2 * 256 * 65530 * 49)}
     del xb
     torch.cuda.empty_cache()
+
+    # ---- the paper's large-filter sweep, 4 x 2048^2, fast
+    # mode: default dispatch (the tensor-core slide-MMA kernel where its cost
+    # model wins) against the FFMA kernels alone (SC_CONV_MMA_BIG=0, read per
+    # call); frac = useful 2 MACs / time over the FP32 FFMA peak
+    xl = torch.rand((4, 2048, 2048), generator=gen, device=dev) * 2 - 1
+    for k in (17, 25, 51):
+        fk = (np.random.default_rng([0x5EED, 6, k]).standard_normal((k, k), dtype=np.float32)
+              / np.float32(k)).astype(np.float32)
+        fl = 2 * 4 * (2048 - k + 1) ** 2 * k * k
+        nb = 4 * (4 * 2048 * 2048 + 4 * (2048 - k + 1) ** 2 + k * k)
+        prev = os.environ.get("SC_CONV_MMA_BIG")
+        t_def = time_launches(torch, lambda: sc.conv2d_slide_compound(xl, fk, vm), 10, 3)
+        os.environ["SC_CONV_MMA_BIG"] = "0"
+        t_ffma = time_launches(torch, lambda: sc.conv2d_slide_compound(xl, fk, vm), 5, 2)
+        if prev is None:
+            del os.environ["SC_CONV_MMA_BIG"]
+        else:
+            os.environ["SC_CONV_MMA_BIG"] = prev
+        out[f"sweep_4x2048_k{k}"] = {"ms": round(t_def * 1e3, 4), **roofline(nb, fl, t_def, hbm_peak),
+                                     "ffma_only_ms": round(t_ffma * 1e3, 4)}
+    del xl
+    torch.cuda.empty_cache()
     return out
 
 
@@ -831,6 +854,8 @@ def compact_per_config(detail: dict) -> dict:
                 c["tc_frac"] = d["tensor_roofline"]["frac"]
             if "clocks" in d and d["clocks"]:
                 c["sm_mhz"] = d["clocks"].get("sm_mhz")
+            if "ffma_only_ms" in d:  # large-filter sweep: tensor-core kernel vs FFMA kernels
+                c = {"ms": d["ms"], "fp32_frac": d["frac_of_bound"], "ffma_only_ms": d["ffma_only_ms"]}
             out[name] = c
     out["key"] = "cfg2: op -> [ms, GB/s, frac]; others frac of max(t_hbm, t_fp32) roofline"
     return out
