@@ -32,6 +32,11 @@
 // inputs hold inf / NaN or magnitudes outside [2^-87, 2^73] skip the tensor
 // cores and compute their outputs with FMAs in the reference tap order.
 //
+// Narrow images (the paper's 512 x 512): P = floor((1024 - ow) / pitch) + 1
+// images sit side by side in one strip, image p at samples p * pitch .. (pitch
+// = w rounded up to 8), so its valid outputs only ever read its own samples;
+// lanes that straddle two images produce columns >= ow that are not stored.
+//
 // Warps: 0-3 split (global fp32 row -> x1 / x2 fp16 rows in shared memory,
 // 4 rows per batch, the next batch's loads in flight while waiting for a
 // slot), 4-7 epilogue (one TMEM lane quarter each, 4 output rows per batch),
@@ -74,6 +79,8 @@ struct BigMmaArgs {
   int kh, kw, nkb, nw;
   int oh, ow, h, w;
   int seg_rows;
+  int pack, pitch, batch;    // pack > 1: that many images side by side in the strip, `pitch`
+                             // samples apart (a multiple of 8, >= w); batch = images in all
   float f_scale, f_unscale;  // 2^sf applied to the taps, and 2^-sf
   long long* trace;          // SC_MMA_BIG_TRACE: clock64 stamps of CTA (0, 0, 0), [role][index]
 };
@@ -181,7 +188,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kh = args.kh, kw = args.kw, nw = args.nw;
   const int c0 = blockIdx.x * kStrip;
   const int r0 = blockIdx.y * args.seg_rows;
-  const int img = blockIdx.z;
+  const int pack = args.pack, pitch = args.pitch;
+  const int img = blockIdx.z * pack;                    // first image of this CTA
+  const int nimg = min(pack, args.batch - img);         // images packed in the strip
   const int s_valid = min(args.seg_rows, args.oh - r0);  // output rows of this CTA
   const int t_rows = s_valid + kh - 1;                    // input rows it reads
   const int n_batches = (t_rows + kRB - 1) / kRB;
@@ -220,34 +229,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) xmax_sh = 0;
   __syncthreads();
   {
-    const float* xrow0 = xg + (int64_t)img * args.h * args.w + (int64_t)r0 * args.w;
     const int w = args.w;
-    const int span = min(kStrip + 16 * nkb + 8, w - c0);  // samples the K blocks reach
+    // one image: the samples the K blocks reach from this strip; packed: whole rows
+    const int span = pack > 1 ? w : min(kStrip + 16 * nkb + 8, w - c0);
     uint32_t mx = 0;
     auto amax4 = [](uint32_t m, const float4 v) {
       return max(max(m, __float_as_uint(v.x) & 0x7fffffffu),
                  max(__float_as_uint(v.y) & 0x7fffffffu,
                      max(__float_as_uint(v.z) & 0x7fffffffu, __float_as_uint(v.w) & 0x7fffffffu)));
     };
-    if ((w & 3) == 0) {
-      // 16 rows per step: 16 independent 16-byte loads in flight per thread
-      const int n4 = span >> 2;  // c0 and w are multiples of 4
-      const int w4 = w >> 2;
-      const float4* rp0 = reinterpret_cast<const float4*>(xrow0 + c0);
-      for (int e = threadIdx.x; e < n4; e += kThreads) {
-        for (int t = 0; t < t_rows; t += 16) {
-          float4 v[16];
+    for (int p = 0; p < nimg; ++p) {
+      const float* xrow0 = xg + (int64_t)(img + p) * args.h * args.w + (int64_t)r0 * args.w;
+      if ((w & 3) == 0) {
+        // 16 rows per step: 16 independent 16-byte loads in flight per thread
+        const int n4 = span >> 2;  // c0 and w are multiples of 4
+        const int w4 = w >> 2;
+        const float4* rp0 = reinterpret_cast<const float4*>(xrow0 + c0);
+        for (int e = threadIdx.x; e < n4; e += kThreads) {
+          for (int t = 0; t < t_rows; t += 16) {
+            float4 v[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = rp0[(int64_t)min(t + j, t_rows - 1) * w4 + e];
+            for (int j = 0; j < 16; ++j) v[j] = rp0[(int64_t)min(t + j, t_rows - 1) * w4 + e];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) mx = amax4(mx, v[j]);
+            for (int j = 0; j < 16; ++j) mx = amax4(mx, v[j]);
+          }
         }
-      }
-    } else {
-      for (int t = 0; t < t_rows; ++t) {
-        const float* rp = xrow0 + (int64_t)t * w + c0;
-        for (int e = threadIdx.x; e < span; e += kThreads)
-          mx = max(mx, __float_as_uint(rp[e]) & 0x7fffffffu);
+      } else {
+        for (int t = 0; t < t_rows; ++t) {
+          const float* rp = xrow0 + (int64_t)t * w + c0;
+          for (int e = threadIdx.x; e < span; e += kThreads)
+            mx = max(mx, __float_as_uint(rp[e]) & 0x7fffffffu);
+        }
       }
     }
     mx = __reduce_max_sync(0xffffffffu, mx);
@@ -277,12 +289,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float* xrow0 = xg + (int64_t)img * plane + (int64_t)r0 * args.w;
     const int w = args.w;
     const bool vec = (w & 3) == 0;
-    int crow[kOwn], ccol[kOwn];
+    // chunk -> (row of the batch, chunk of the row); the chunk's samples are
+    // columns xcol .. xcol + 7 of image img + ximg (packed: pitch is a
+    // multiple of 8, so a chunk never straddles two images; ximg < 0: zeros)
+    int crow[kOwn], ccol[kOwn], xcol[kOwn], ximg[kOwn];
 #pragma unroll
     for (int j = 0; j < kOwn; ++j) {
       const int c = u + 128 * j;
       crow[j] = c / kChunks;
       ccol[j] = c - crow[j] * kChunks;
+      if (pack > 1) {
+        const int pi = 8 * ccol[j] / pitch;
+        ximg[j] = pi < nimg ? pi : -1;
+        xcol[j] = 8 * ccol[j] - pi * pitch;
+      } else {
+        ximg[j] = 0;
+        xcol[j] = c0 + 8 * ccol[j];
+      }
     }
     const bool own4 = u < kRB * kChunks - 512;  // chunk 512 + u exists
     auto load8 = [&](const float* rowp, int col, float (&f)[8]) {
@@ -314,7 +337,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < kOwn; ++j) {
         if (j == kOwn - 1 && !own4) break;
         const int t = min(b * kRB + crow[j], t_rows - 1);
-        load8(xrow0 + (int64_t)t * w, c0 + 8 * ccol[j], buf[j]);
+        if (ximg[j] >= 0) {
+          load8(xrow0 + ximg[j] * plane + (int64_t)t * w, xcol[j], buf[j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) buf[j][i] = 0.0f;
+        }
       }
     };
     auto emit = [&](int b, const float (&buf)[kOwn][8]) {
@@ -365,8 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // coalesced 128-byte row segment whatever the alignment of the output row
     // (per-lane 32-byte stores cost ~1,000 cycles per output row)
     float* est = reinterpret_cast<float*>(estage + q * kEStage);
-    const int colw = c0 + 256 * q;  // first column of this warp
-    float* ybase = y + (int64_t)img * args.oh * ow + colw;
+    const int colw = c0 + 256 * q;  // first column (one image) / strip position (packed) of this warp
+    const int64_t oplane = (int64_t)args.oh * ow;
+    float* ybase = y + (int64_t)img * oplane;
     const int n_epi = (s_valid - o_start + 3) / 4;
     int batches_done = 0;  // MMA batches known complete (waited in order)
     for (int e = 0; e < n_epi; ++e) {
@@ -383,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 4; ++i) tmem_zero8(lane_base + (slot0 + i) * 8);
-      if (o0 + 3 >= 0 && colw < ow) {
+      if (o0 + 3 >= 0 && (pack > 1 || colw < ow)) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -398,7 +427,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
               const int ee = it * 32 + lane;
-              if (colw + ee < ow) yr[ee] = est[(i * 32 + (ee >> 3)) * kEStride + (ee & 7)];
+              const float val = est[(i * 32 + (ee >> 3)) * kEStride + (ee & 7)];
+              if (pack > 1) {
+                const int pos = colw + ee, pi = pos / pitch, c = pos - pi * pitch;
+                if (pi < nimg && c < ow) yr[pi * oplane + c] = val;
+              } else if (colw + ee < ow) {
+                yr[colw + ee] = val;
+              }
             }
           }
         }
@@ -479,16 +514,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (bad) {
     const int64_t plane_in = (int64_t)args.h * args.w;
-    const float* ximg = xg + (int64_t)img * plane_in;
-    float* yimg = y + (int64_t)img * args.oh * args.ow;
     const int cols = min(kStrip, args.ow - c0);
-    for (int64_t idx = threadIdx.x; idx < (int64_t)s_valid * cols; idx += kThreads) {
-      const int r = r0 + (int)(idx / cols), c = c0 + (int)(idx % cols);
-      float acc = 0.0f;
-      for (int j = 0; j < kh; ++j)
-        for (int i = 0; i < kw; ++i)
-          acc = fmaf(taps[j * kw + i], ximg[(int64_t)(r + j) * args.w + c + i], acc);
-      yimg[(int64_t)r * args.ow + c] = acc;
+    for (int p = 0; p < nimg; ++p) {
+      const float* ximg = xg + (int64_t)(img + p) * plane_in;
+      float* yimg = y + (int64_t)(img + p) * args.oh * args.ow;
+      for (int64_t idx = threadIdx.x; idx < (int64_t)s_valid * cols; idx += kThreads) {
+        const int r = r0 + (int)(idx / cols), c = c0 + (int)(idx % cols);
+        float acc = 0.0f;
+        for (int j = 0; j < kh; ++j)
+          for (int i = 0; i < kw; ++i)
+            acc = fmaf(taps[j * kw + i], ximg[(int64_t)(r + j) * args.w + c + i], acc);
+        yimg[(int64_t)r * args.ow + c] = acc;
+      }
     }
   }
   if (warp == 8) {
@@ -511,6 +548,14 @@ size_t smem_bytes(int kh, int nkb) {
 // Row segments: one CTA per SM, every CTA costs ~(rows + kh - 1) input rows
 // plus the pipeline fill; pick the segment length minimising waves x rows.
 // Returns the output rows per segment and the modelled rows per SM.
+// Images packed side by side in one strip (1 = none) and their pitch in samples.
+int pack_of(int64_t w, int64_t ow, int* pitch) {
+  const int64_t pt = (w + 7) / 8 * 8;
+  *pitch = (int)pt;
+  if (ow > kStrip - pt) return 1;  // a second image's valid outputs would not fit the lanes
+  return (int)std::min<int64_t>((kStrip - ow) / pt + 1, 64);
+}
+
 int64_t plan_rows(int64_t batch, int64_t oh, int64_t ow, int64_t kh, int64_t* cost_rows) {
   const int64_t strips = (ow + kStrip - 1) / kStrip;
   const int64_t slots = sm_count();
@@ -547,7 +592,9 @@ bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t
     // kernels sustain ~55 % of the FP32 pipe on full grids (measured,
     // tools/mma_big_check.py: the model picks the faster side on the sweep)
     int64_t cost_rows = 0;
-    plan_rows(batch, oh, ow, kh, &cost_rows);
+    int pitch = 0;
+    const int pack = pack_of(w, ow, &pitch);
+    plan_rows((batch + pack - 1) / pack, oh, ow, kh, &cost_rows);
     const int nkb = (int)((kw + 7 + 15) / 16), nw = win_rows((int)kh);
     const double n_mma = 3.0 * nkb * ((nw + 31) / 32 + 0.3);
     const double t_mma = (double)cost_rows * std::max(900.0, 115.0 * n_mma) + 30000.0;
@@ -573,9 +620,13 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   a.trace = nullptr;
   if (const char* e = getenv("SC_MMA_BIG_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
   const int64_t strips = (ow + kStrip - 1) / kStrip;
+  a.pack = env_int("SC_MMA_BIG_PACK", 1) ? pack_of(w, ow, &a.pitch) : 1;
+  if (a.pack == 1) a.pitch = 0;
+  a.batch = (int)batch;
+  const int64_t groups = (batch + a.pack - 1) / a.pack;
   const int env_rows = env_int("SC_MMA_BIG_ROWS", 0);
   const int64_t rows =
-      env_rows > 0 ? std::min<int64_t>(env_rows, oh) : plan_rows(batch, oh, ow, kh, nullptr);
+      env_rows > 0 ? std::min<int64_t>(env_rows, oh) : plan_rows(groups, oh, ow, kh, nullptr);
   a.seg_rows = (int)rows;
   const int64_t segs = (oh + rows - 1) / rows;
   if (strips > 0x7fffffff || segs > 65535 || batch > 65535)
@@ -597,7 +648,7 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   build_b_kernel<<<32, 256, 0, st>>>(taps, a.kh, a.kw, a.nkb, a.f_scale, bimg, taps_dev);
   SC_LAUNCH_CHECK("build_b_kernel");
   const size_t smem = smem_bytes(a.kh, a.nkb);
-  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)batch);
+  dim3 grid((unsigned)strips, (unsigned)segs, (unsigned)groups);
   const uint4* bimg4 = reinterpret_cast<const uint4*>(bimg);
   auto launch = [&](auto kernel, uint64_t* done_attr) -> cudaError_t {
     cudaError_t e = set_smem_limit_once(kernel, smem_bytes(kMaxKH, kMaxKB), done_attr);

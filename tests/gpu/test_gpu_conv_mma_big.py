@@ -43,7 +43,10 @@ def _bands(oh, kh, nb=3, rows=5):
     ((1, 700, 777), 33, 10, None),
     ((1, 600, 1500), 40, 3, None),       # tall, narrow filter (one K block)
     ((1, 200, 2300), 2, 40, None),
-    ((5, 64, 64), 21, 21, None),         # images smaller than a strip
+    ((5, 64, 64), 21, 21, None),         # 16 images side by side in one strip (5 present)
+    ((32, 512, 512), 51, 51, None),      # the paper's sweep shape: two images per strip
+    ((7, 100, 203), 15, 9, 30),          # packed, odd width (pitch 208), ragged last group
+    ((3, 80, 520), 11, 57, None),        # two images, the widest filter
 ])
 def test_forced_mma_matches_oracle(shape, kh, kw, rows, monkeypatch):
     rng = np.random.default_rng(kh * 100 + kw)
