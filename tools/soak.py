@@ -5,6 +5,7 @@ mode within the north-star tolerance, max pooling always bit-exact.
 
 usage: python tools/soak.py [seconds]   (prints one summary line per family)
 """
+import os
 import sys
 import time
 
@@ -64,6 +65,19 @@ while time.time() < t_end:
         elif np.isfinite(x).all():
             note(f"pool {op} fast", O.normwise_error(got_f, want) <= O.north_star_tol(k),
                  f"n={n} k={k}")
+    # 2b. the fused pair: bit-identical to the single-op calls, both modes
+    for mean in (False, True):
+        pair = sc.sliding_window_mean_max if mean else sc.sliding_window_sum_max
+        one = sc.sliding_window_mean if mean else sc.sliding_window_sum
+        for ex in (False, True):
+            (ya, _), (ym, _) = pair(xd, k, exact=ex)
+            ra = one(xd, k, exact=ex)[0]
+            rm = sc.sliding_window_max(xd, k, exact=ex)[0]
+            same = all(np.array_equal(np.isnan(a_), np.isnan(b_)) and np.array_equal(
+                a_[~np.isnan(b_)].view(np.uint32), b_[~np.isnan(b_)].view(np.uint32))
+                for a_, b_ in ((ya.cpu().numpy(), ra.cpu().numpy()),
+                               (ym.cpu().numpy(), rm.cpu().numpy())))
+            note("pool pair", same, f"n={n} k={k} b={b} mean={mean} exact={ex}")
     # 3. 2-D conv: random shapes and filters (square and not, 1..64)
     kh = int(rng.choice([1, 3, 5, 7, rng.integers(1, 65)]))
     kw = int(rng.choice([kh, rng.integers(1, 65)]))
@@ -80,6 +94,26 @@ while time.time() < t_end:
     ref64 = np.stack([O.oracle_conv2d(img, f) for img in x])
     note("conv2d fast", O.normwise_error(fast, ref64) <= O.north_star_tol(max(kh, kw)),
          f"{b}x{h}x{w} f{kh}x{kw}")
+    # 3b. the large-filter tensor-core kernel, forced (kh <= 53, kw <= 57):
+    # tolerance, and the FFMA kernels' inf / NaN pattern
+    if 2 <= kh <= 53 and 2 <= kw <= 57:
+        xs = x.copy()
+        if rng.random() < 0.3:
+            xs[0, rng.integers(0, h), rng.integers(0, w)] = rng.choice([np.inf, np.nan, 1e35, -np.inf])
+        xs *= np.float32(rng.choice([1e-6, 1.0, 1e5]))
+        xsd = torch.from_numpy(xs).cuda()
+        if rng.random() < 0.5:
+            os.environ["SC_MMA_BIG_ROWS"] = str(int(rng.integers(1, 80)))
+        os.environ["SC_CONV_MMA_BIG"] = "2"
+        got = sc.conv2d_reference(xsd, f).cpu().numpy()
+        os.environ["SC_CONV_MMA_BIG"] = "0"
+        os.environ.pop("SC_MMA_BIG_ROWS", None)
+        ref = sc.conv2d_reference(xsd, f).cpu().numpy()
+        os.environ.pop("SC_CONV_MMA_BIG", None)
+        fin = np.isfinite(ref)
+        ok = (np.array_equal(np.isnan(got), np.isnan(ref)) and np.array_equal(np.isinf(got), np.isinf(ref))
+              and O.normwise_error(got[fin], ref[fin]) <= O.north_star_tol(max(kh, kw)))
+        note("conv2d mma_big", ok, f"{b}x{h}x{w} f{kh}x{kw}")
     # 4. NCHW 3x3 pad 1 (tensor-core and CUDA-core paths)
     if rng.random() < 0.25:
         cin = int(rng.choice([32, 64, 128, 3, 17]))
