@@ -565,7 +565,7 @@ int64_t plan_rows(int64_t batch, int64_t oh, int64_t ow, int64_t kh, int64_t* co
     const int64_t n = batch * strips * ((oh + r - 1) / r);
     const int64_t cost = (n + slots - 1) / slots * (r + kh - 1 + 12);
     if (best < 0 || cost < best) best = cost, rows = r;
-    if (r <= 8) break;
+    if (r <= 8 || n > 64 * slots) break;  // shorter segments only add halo rows
   }
   if (cost_rows) *cost_rows = best;
   return rows;
