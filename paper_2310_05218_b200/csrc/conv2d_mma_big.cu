@@ -37,10 +37,9 @@
 // = w rounded up to 8), so its valid outputs only ever read its own samples;
 // lanes that straddle two images produce columns >= ow that are not stored.
 //
-// Warps: 0-3 split (global fp32 row -> x1 / x2 fp16 rows in shared memory,
-// 4 rows per batch, the next batch's loads in flight while waiting for a
-// slot), 4-7 epilogue (one TMEM lane quarter each, 4 output rows per batch),
-// 8 MMA issuer (3 products x K blocks x window pieces per input row, one
+// Warps: 0-5 split (global fp32 row -> x1 / x2 fp16 rows in shared memory,
+// 4 rows per batch, two batches of loads in flight), 6-9 epilogue (one TMEM
+// lane quarter each, 4 output rows per batch), 10 MMA issuer (3 products x K blocks x window pieces per input row, one
 // commit per batch).  Hand-offs are per batch of 4 rows (~1,000-12,000 tensor
 // cycles of work), so plain counters / mbarriers suffice.
 #include <cuda.h>
@@ -66,7 +65,9 @@ constexpr int kMaxKB = 4;                // K blocks of 16 samples: 16 n_kb >= k
 constexpr int kXRow = 2176;              // bytes per fp16 row (1,080 samples used)
 constexpr int kXSlot = 2 * kXRow;        // x1 | x2
 constexpr int kND = 32;                  // MMA-completion barriers (one per batch, ring)
-constexpr int kThreads = 32 * 9;
+constexpr int kSplitWarps = 6;            // warps 0..5; epilogue warps 6..9 (TMEM quarter = warp % 4); issuer 10
+constexpr int kWarpEpi0 = kSplitWarps, kWarpIssue = kSplitWarps + 4;
+constexpr int kThreads = 32 * (kWarpIssue + 1);
 constexpr int kPad = 3;                  // zero slots in front of the B image (row phase)
 constexpr int kEStride = 9;              // epilogue staging: floats per TMEM lane (8 + 1 pad)
 constexpr int kEStage = 4 * 32 * kEStride * 4;  // bytes per epilogue warp (4 rows x 32 lanes)
@@ -174,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const uint4* __restrict__ bimg, const float* __restrict__ taps,
                           const __grid_constant__ BigMmaArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ int split_cnt[4], epi_cnt[4];       // batches done per warp (release / acquire)
+  __shared__ int split_cnt[kSplitWarps], epi_cnt[4];       // batches done per warp (release / acquire)
   __shared__ __align__(8) uint64_t done[kND];    // MMA completion, one per batch of input rows
   __shared__ __align__(8) uint64_t ring_ready;
   __shared__ uint32_t tmem_base_sh;
@@ -204,12 +205,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int e = threadIdx.x; e < n16; e += kThreads) dst[e] = bimg[e];
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 4; ++i) split_cnt[i] = 0, epi_cnt[i] = 0;
+    for (int i = 0; i < kSplitWarps; ++i) split_cnt[i] = 0;
+    for (int i = 0; i < 4; ++i) epi_cnt[i] = 0;
     for (int s = 0; s < kND; ++s) mbar_init(&done[s], 1);
     mbar_init(&ring_ready, 4);
     fence_mbar_init();
   }
-  if (warp == 8) {
+  if (warp == kWarpIssue) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
                  "n"(512)
@@ -275,16 +277,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (bad) {
     // no tensor-core pass for this CTA (see the fallback below)
-  } else if (warp < 4) {
+  } else if (warp < kSplitWarps) {
     // ------------------------------------------------------------ split warps
     // A batch is kRB rows x 136 chunks of 8 samples (column c0 + 8 cc -> byte
     // 16 cc of the row's x1 / x2 slots; the K blocks reach 8*127 + 16 nkb + 15
-    // <= 1,087).  Thread u owns chunks u + 128 j (j = 0..3, and j = 4 for
-    // u < 32) of every batch.  Two batches of loads are kept in flight in
+    // <= 1,087).  Thread u of the 192 owns chunks u + 192 j (j = 0, 1, and
+    // j = 2 for u < 160) of every batch.  Two batches of loads are kept in flight in
     // registers: with one, the load latency was exposed once per batch
     // (~750 cycles per input row with no MMAs at all).
-    constexpr int kChunks = 136, kOwn = 5;
-    const int u = threadIdx.x;  // 0..127
+    constexpr int kChunks = 136, kOwn = 3, kSplitThreads = 32 * kSplitWarps;
+    const int u = threadIdx.x;  // 0..191
     const int64_t plane = (int64_t)args.h * args.w;
     const float* xrow0 = xg + (int64_t)img * plane + (int64_t)r0 * args.w;
     const int w = args.w;
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int crow[kOwn], ccol[kOwn], xcol[kOwn], ximg[kOwn];
 #pragma unroll
     for (int j = 0; j < kOwn; ++j) {
-      const int c = u + 128 * j;
+      const int c = u + kSplitThreads * j;
       crow[j] = c / kChunks;
       ccol[j] = c - crow[j] * kChunks;
       if (pack > 1) {
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         xcol[j] = c0 + 8 * ccol[j];
       }
     }
-    const bool own4 = u < kRB * kChunks - 512;  // chunk 512 + u exists
+    const bool own4 = u < kRB * kChunks - (kOwn - 1) * kSplitThreads;  // the last owned chunk exists
     auto load8 = [&](const float* rowp, int col, float (&f)[8]) {
       if (vec && col + 8 <= w) {
         const float4 a = *reinterpret_cast<const float4*>(rowp + col);
@@ -348,7 +350,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto emit = [&](int b, const float (&buf)[kOwn][8]) {
       if (b >= kXB) {
         const int pb = b - kXB;  // the batch that used this slot: its MMAs must be complete
-        mbar_wait(&done[pb % kND], (pb / kND) & 1);
+        // back off between probes (the waiters share sub-partitions with the
+        // MMA-issuing warp; measured neutral against plain spinning)
+        mbar_wait_sleep(&done[pb % kND], (pb / kND) & 1, 32, 256);
       }
       if (threadIdx.x == 0) BIG_TRACE(0, b, clock64());
       unsigned char* slot0 = xrows + (b % kXB) * kRB * kXSlot;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         publish(b + 1);
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < kWarpIssue) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter
     const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
@@ -402,9 +406,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int o0 = o_start + 4 * e;
       const int t_final = min(o0 + 3 + kh - 1, t_rows - 1);
       for (; batches_done <= t_final / kRB; ++batches_done)
-        mbar_wait(&done[batches_done % kND], (batches_done / kND) & 1);
+        mbar_wait_sleep(&done[batches_done % kND], (batches_done / kND) & 1, 32, 256);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (warp == 4 && lane == 0) BIG_TRACE(5, e, clock64());
+      if (warp == kWarpEpi0 && lane == 0) BIG_TRACE(5, e, clock64());
       const int slot0 = (o0 - o_start) & (kRing - 1);
       uint32_t v[4][8];
 #pragma unroll
@@ -443,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) st_release(&epi_cnt[q], e + 1);
-      if (warp == 4 && lane == 0) BIG_TRACE(6, e, clock64());
+      if (warp == kWarpEpi0 && lane == 0) BIG_TRACE(6, e, clock64());
     }
   } else {
     // ------------------------------------------------------------ MMA issuer
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int epi_known = 0;  // epilogue batches known drained
     for (int b = 0; b < n_batches; ++b) {
       if (lane == 0) BIG_TRACE(2, b, clock64());
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < kSplitWarps; ++i)
         while (ld_acquire(&split_cnt[i]) <= b) {
         }
       if (lane == 0) BIG_TRACE(3, b, clock64());
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (warp == 8) {
+  if (warp == kWarpIssue) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512)
                  : "memory");
@@ -588,7 +592,7 @@ bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t
     if (kh * kw < 150) return false;
     // cycles per SM: ~115 per MMA (3 products x K blocks x window pieces per
     // input row; issue-bound for short windows, tensor-bound from N ~ 200),
-    // ~900 per row at least, ~30,000 for the range scan and fill; the FFMA
+    // ~750 per row at least, ~30,000 for the range scan and fill; the FFMA
     // kernels sustain ~55 % of the FP32 pipe on full grids (measured,
     // tools/mma_big_check.py: the model picks the faster side on the sweep)
     int64_t cost_rows = 0;
@@ -597,7 +601,7 @@ bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t
     plan_rows((batch + pack - 1) / pack, oh, ow, kh, &cost_rows);
     const int nkb = (int)((kw + 7 + 15) / 16), nw = win_rows((int)kh);
     const double n_mma = 3.0 * nkb * ((nw + 31) / 32 + 0.3);
-    const double t_mma = (double)cost_rows * std::max(900.0, 115.0 * n_mma) + 30000.0;
+    const double t_mma = (double)cost_rows * std::max(750.0, 115.0 * n_mma) + 30000.0;
     const double t_ffma = (double)batch * oh * ow * kh * kw / (sm_count() * 128.0 * 0.55);
     if (t_mma > 0.75 * t_ffma) return false;
   }
