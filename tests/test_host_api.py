@@ -93,6 +93,11 @@ def test_pool_window_out_of_range():                   # test_pooling.py:62-66
         sc.sliding_window_max([1.0, 2.0], 0)
     with pytest.raises(sc.ShapeError):
         sc.sliding_window_mean(np.zeros((2, 5)), 6)
+    # the fused pair validates like the single-op calls (pooling.py:32-33), before any CUDA call
+    with pytest.raises(sc.ShapeError):
+        sc.sliding_window_sum_max([1.0, 2.0], 3)
+    with pytest.raises(sc.ShapeError):
+        sc.sliding_window_mean_max(np.zeros((2, 5)), 0)
 
 
 def test_tensor_coercion_errors():
@@ -147,6 +152,8 @@ def test_no_cpu_fallback_without_gpu():
         sc.conv2d_reference(np.ones((4, 4), np.float32), np.ones((2, 2), np.float32))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         sc.sliding_window_sum(np.ones(8, np.float32), 3)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        sc.sliding_window_mean_max(np.ones(8, np.float32), 3)
 
 
 def test_verify_suite_rejects_zero_trials():
