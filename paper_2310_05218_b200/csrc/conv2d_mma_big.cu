@@ -160,10 +160,24 @@ __device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.cta.shared::cta.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Progress counters are read with independent relaxed loads (an acquire load
+// orders everything after it, so a row of them serialises: ~100 cycles each,
+// 700 per batch with six split warps) and one acquire fence once the wait is
+// over.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  asm volatile("ld.relaxed.cta.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
   return v;
+}
+template <int N>
+__device__ __forceinline__ int min_progress(const int (&c)[N]) {
+  int m = ld_relaxed(&c[0]);
+#pragma unroll
+  for (int i = 1; i < N; ++i) m = min(m, ld_relaxed(&c[i]));
+  return m;
+}
+__device__ __forceinline__ void fence_acquire() {
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
 }
 
 // biased exponents of the largest input magnitude a CTA scales (2^-87 .. 2^73)
@@ -459,9 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int epi_known = 0;  // epilogue batches known drained
     for (int b = 0; b < n_batches; ++b) {
       if (lane == 0) BIG_TRACE(2, b, clock64());
-      for (int i = 0; i < kSplitWarps; ++i)
-        while (ld_acquire(&split_cnt[i]) <= b) {
-        }
+      while (min_progress(split_cnt) <= b) {
+      }
+      fence_acquire();
       if (lane == 0) BIG_TRACE(3, b, clock64());
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int rr = 0; rr < kRB; ++rr) {
@@ -474,10 +488,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // below a + nw - kRing, i.e. epilogue batches [0, need)
         const int need = (a + nw - kRing - o_start + 3) >> 2;
         if (need > epi_known) {
-          for (int i = 0; i < 4; ++i)
-            while (ld_acquire(&epi_cnt[i]) < need) {
-            }
-          epi_known = need;
+          int got;
+          while ((got = min_progress(epi_cnt)) < need) {
+          }
+          fence_acquire();
+          epi_known = got;  // everything the counters show, not just what was needed
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         }
         const uint32_t xsrc = xrows_addr + (uint32_t)((b % kXB) * kRB + rr) * kXSlot;
