@@ -69,7 +69,8 @@ constexpr int kSplitWarps = 6;            // warps 0..5; epilogue warps 6..9 (TM
 constexpr int kWarpEpi0 = kSplitWarps, kWarpIssue = kSplitWarps + 4;
 constexpr int kThreads = 32 * (kWarpIssue + 1);
 constexpr int kPad = 3;                  // zero slots in front of the B image (row phase)
-constexpr int kEStride = 9;              // epilogue staging: floats per TMEM lane (8 + 1 pad)
+constexpr int kEStride = 12;             // epilogue staging: floats per TMEM lane (8 + 4 pad: 16-byte
+                                         // aligned, conflict-free STS.128, 2-way on 4 banks for the reads)
 constexpr int kEStage = 4 * 32 * kEStride * 4;  // bytes per epilogue warp (4 rows x 32 lanes)
 
 __host__ __device__ constexpr int win_rows(int kh) { return (kh + 3 + 1) & ~1; }       // even
@@ -414,6 +415,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int colw = c0 + 256 * q;  // first column (one image) / strip position (packed) of this warp
     const int64_t oplane = (int64_t)args.oh * ow;
     float* ybase = y + (int64_t)img * oplane;
+    // element it * 32 + lane of the warp's 256: its offset inside an output
+    // row (packed: image plane + column) and whether it is stored -- fixed
+    // for the CTA, so the divisions happen once, not per element and row
+    int eoff[8];  // 32-bit: the host packs only while pack * oh * ow < 2^31
+    uint32_t emask = 0;
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int pos = colw + it * 32 + lane;
+      if (pack > 1) {
+        const int pi = pos / pitch, c = pos - pi * pitch;
+        eoff[it] = pi * (int)oplane + c;
+        emask |= (uint32_t)(pi < nimg && c < ow) << it;
+      } else {
+        eoff[it] = pos;
+        emask |= (uint32_t)(pos < ow) << it;
+      }
+    }
+    const bool any_col = __any_sync(0xffffffffu, emask != 0);
+    const bool full_cols = pack == 1 && colw + 256 <= ow;  // no per-element bounds
+    // two multiplications undo the scales (their product may leave the float range)
     const int n_epi = (s_valid - o_start + 3) / 4;
     int batches_done = 0;  // MMA batches known complete (waited in order)
     for (int e = 0; e < n_epi; ++e) {
@@ -430,12 +451,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 4; ++i) tmem_zero8(lane_base + (slot0 + i) * 8);
-      if (o0 + 3 >= 0 && (pack > 1 || colw < ow)) {
+      if (o0 + 3 >= 0 && any_col) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i) {
+          float o8[8];
 #pragma unroll
           for (int s8 = 0; s8 < 8; ++s8)
-            est[(i * 32 + lane) * kEStride + s8] = __uint_as_float(v[i][s8]) * x_unscale * f_unscale;
+            o8[s8] = __uint_as_float(v[i][s8]) * x_unscale * f_unscale;
+          float4* dst = reinterpret_cast<float4*>(est + (i * 32 + lane) * kEStride);
+          dst[0] = make_float4(o8[0], o8[1], o8[2], o8[3]);
+          dst[1] = make_float4(o8[4], o8[5], o8[6], o8[7]);
+        }
         __syncwarp();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -447,10 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int ee = it * 32 + lane;
               const float val = est[(i * 32 + (ee >> 3)) * kEStride + (ee & 7)];
               if (pack > 1) {
-                const int pos = colw + ee, pi = pos / pitch, c = pos - pi * pitch;
-                if (pi < nimg && c < ow) yr[pi * oplane + c] = val;
-              } else if (colw + ee < ow) {
-                yr[colw + ee] = val;
+                if ((emask >> it) & 1) yr[eoff[it]] = val;
+              } else if (full_cols || colw + ee < ow) {
+                yr[colw + ee] = val;  // immediate offsets from one base per row
               }
             }
           }
@@ -574,6 +599,12 @@ int pack_of(int64_t w, int64_t ow, int* pitch) {
   if (ow > kStrip - pt) return 1;  // a second image's valid outputs would not fit the lanes
   return (int)std::min<int64_t>((kStrip - ow) / pt + 1, 64);
 }
+// ... and only while an image group's outputs stay 32-bit addressable
+int pack_for(int64_t w, int64_t oh, int64_t ow, int* pitch) {
+  int p = pack_of(w, ow, pitch);
+  while (p > 1 && (int64_t)p * oh * ow >= ((int64_t)1 << 31)) --p;
+  return p;
+}
 
 int64_t plan_rows(int64_t batch, int64_t oh, int64_t ow, int64_t kh, int64_t* cost_rows) {
   const int64_t strips = (ow + kStrip - 1) / kStrip;
@@ -612,7 +643,7 @@ bool conv2d_mma_big_applicable(const float* x, int64_t batch, int64_t h, int64_t
     // tools/mma_big_check.py: the model picks the faster side on the sweep)
     int64_t cost_rows = 0;
     int pitch = 0;
-    const int pack = pack_of(w, ow, &pitch);
+    const int pack = pack_for(w, oh, ow, &pitch);
     plan_rows((batch + pack - 1) / pack, oh, ow, kh, &cost_rows);
     const int nkb = (int)((kw + 7 + 15) / 16), nw = win_rows((int)kh);
     const double n_mma = 3.0 * nkb * ((nw + 31) / 32 + 0.3);
@@ -639,7 +670,7 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   a.trace = nullptr;
   if (const char* e = getenv("SC_MMA_BIG_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
   const int64_t strips = (ow + kStrip - 1) / kStrip;
-  a.pack = env_int("SC_MMA_BIG_PACK", 1) ? pack_of(w, ow, &a.pitch) : 1;
+  a.pack = env_int("SC_MMA_BIG_PACK", 1) ? pack_for(w, oh, ow, &a.pitch) : 1;
   if (a.pack == 1) a.pitch = 0;
   a.batch = (int)batch;
   const int64_t groups = (batch + a.pack - 1) / a.pack;
