@@ -103,3 +103,21 @@ def test_cost_model_and_exact_mode(monkeypatch):
     # small problems stay on the FFMA kernels under the model
     xs = torch.from_numpy(x[:1, :512, :512].copy()).cuda()
     assert np.array_equal(_fast(xs, f, 1, monkeypatch), _fast(xs, f, 0, monkeypatch))
+
+
+def test_host_pipeline_with_large_filter(monkeypatch):
+    """numpy in -> numpy out: the host pipeline's chunks (one image each here)
+    go through the same dispatch and cost model"""
+    rng = np.random.default_rng(77)
+    x = rng.uniform(-1, 1, (3, 1100, 2048)).astype(np.float32)
+    f = (rng.standard_normal((25, 25)) / 25).astype(np.float32)
+    monkeypatch.setenv("SC_CONV_MMA_BIG", "1")
+    monkeypatch.setenv("SC_HOST_CHUNK_MB", "32")     # chunks of whole images
+    got = sc.conv2d_slide_compound(x, f, VM, exact=False)[0]
+    assert isinstance(got, np.ndarray) and got.shape == (3, 1076, 2024)
+    monkeypatch.setenv("SC_CONV_MMA_BIG", "0")
+    ref = sc.conv2d_slide_compound(x, f, VM, exact=False)[0]
+    assert not np.array_equal(got, ref)               # the tensor-core kernel did run
+    assert O.normwise_error(got, ref) <= O.north_star_tol(25)
+    want = O.conv2d_batched(x[:, 500:500 + 4 + 24], f)
+    assert O.normwise_error(got[:, 500:504], want) <= O.north_star_tol(25)
