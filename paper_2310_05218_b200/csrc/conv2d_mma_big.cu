@@ -104,6 +104,7 @@ struct TapsArg {
 __global__ void build_b_kernel(const __grid_constant__ TapsArg taps, int kh, int kw, int nkb,
                                float f_scale, __half* __restrict__ bimg,
                                float* __restrict__ taps_out) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the conv kernel's prologue may start
   const int slots = bimg_slots(kh);
   const int per = slots * 128;  // elements per (part, kb) image
   const int total = 2 * nkb * per;
@@ -213,12 +214,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int o_start = -(((kh - 1) + 3) & ~3);            // first ring row, multiple of 4
   const int bimg_b = bimg_bytes(kh);
 
-  // ---- B images: global -> shared (16-byte copies)
-  {
-    const int n16 = 2 * nkb * bimg_b / 16;
-    uint4* dst = reinterpret_cast<uint4*>(bmats);
-    for (int e = threadIdx.x; e < n16; e += kThreads) dst[e] = bimg[e];
-  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSplitWarps; ++i) split_cnt[i] = 0;
     for (int i = 0; i < 4; ++i) epi_cnt[i] = 0;
@@ -233,7 +228,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  fence_proxy_async();  // B images (generic writes) -> tensor core (async proxy)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -282,6 +276,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     mx = __reduce_max_sync(0xffffffffu, mx);
     if (lane == 0) atomicMax(&xmax_sh, mx);
   }
+  // ---- B images: global -> shared (16-byte copies).  The kernel is launched
+  // programmatically dependent on build_b_kernel, so everything above (the
+  // range scan reads only x, complete before build_b started) overlaps it;
+  // its output is read from here on.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  {
+    const int n16 = 2 * nkb * bimg_b / 16;
+    uint4* dst = reinterpret_cast<uint4*>(bmats);
+    for (int e = threadIdx.x; e < n16; e += kThreads) dst[e] = bimg[e];
+  }
+  fence_proxy_async();  // B images (generic writes) -> tensor core (async proxy)
   __syncthreads();
   if (threadIdx.x == 0) BIG_TRACE(7, 1, clock64());
   const int xexp = (int)(xmax_sh >> 23);  // biased exponent of the largest magnitude
@@ -702,7 +707,8 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   const uint4* bimg4 = reinterpret_cast<const uint4*>(bimg);
   auto launch = [&](auto kernel, uint64_t* done_attr) -> cudaError_t {
     cudaError_t e = set_smem_limit_once(kernel, smem_bytes(kMaxKH, kMaxKB), done_attr);
-    if (e == cudaSuccess) kernel<<<grid, kThreads, smem, st>>>(x, y, bimg4, taps_dev, a);
+    if (e == cudaSuccess)
+      e = launch_pdl(kernel, grid, dim3(kThreads), smem, st, x, y, bimg4, (const float*)taps_dev, a);
     return e;
   };
   static uint64_t attrs[kMaxKB] = {};
