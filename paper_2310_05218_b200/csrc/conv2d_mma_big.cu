@@ -38,14 +38,16 @@
 // lanes that straddle two images produce columns >= ow that are not stored.
 //
 // Warps: 0-5 split (global fp32 row -> x1 / x2 fp16 rows in shared memory,
-// 4 rows per batch, two batches of loads in flight), 6-9 epilogue (one TMEM
-// lane quarter each, 4 output rows per batch), 10 MMA issuer (3 products x K blocks x window pieces per input row, one
+// 4 rows per batch, two batches of loads in flight), 6-13 epilogue (one TMEM
+// lane quarter each, 4 output rows per batch; two groups of four on alternate
+// batches), 14 MMA issuer (3 products x K blocks x window pieces per input row, one
 // commit per batch).  Hand-offs are per batch of 4 rows (~1,000-12,000 tensor
 // cycles of work), so plain counters / mbarriers suffice.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -66,7 +68,8 @@ constexpr int kXRow = 2176;              // bytes per fp16 row (1,080 samples us
 constexpr int kXSlot = 2 * kXRow;        // x1 | x2
 constexpr int kND = 32;                  // MMA-completion barriers (one per batch, ring)
 constexpr int kSplitWarps = 6;            // warps 0..5; epilogue warps 6..9 (TMEM quarter = warp % 4); issuer 10
-constexpr int kWarpEpi0 = kSplitWarps, kWarpIssue = kSplitWarps + 4;
+constexpr int kEpiGroups = 2;             // epilogue groups of 4 warps, draining alternate batches
+constexpr int kWarpEpi0 = kSplitWarps, kWarpIssue = kSplitWarps + 4 * kEpiGroups;
 constexpr int kThreads = 32 * (kWarpIssue + 1);
 constexpr int kPad = 3;                  // zero slots in front of the B image (row phase)
 constexpr int kEStride = 12;             // epilogue staging: floats per TMEM lane (8 + 4 pad: 16-byte
@@ -84,11 +87,14 @@ struct BigMmaArgs {
   int pack, pitch, batch;    // pack > 1: that many images side by side in the strip, `pitch`
                              // samples apart (a multiple of 8, >= w); batch = images in all
   float f_scale, f_unscale;  // 2^sf applied to the taps, and 2^-sf
-  long long* trace;          // SC_MMA_BIG_TRACE: clock64 stamps of CTA (0, 0, 0), [role][index]
+  long long* trace;          // SC_MMA_BIG_TRACE: clock64 stamps of one CTA, [role][index]
+  int trace_cta[3];          // SC_MMA_BIG_TRACE_CTA=x,y,z (default 0,0,0)
 };
 #define BIG_TRACE(role, idx, v)                                                              \
   do {                                                                                       \
-    if (args.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (idx) < 1024) \
+    if (args.trace && (int)blockIdx.x == args.trace_cta[0] &&                                \
+        (int)blockIdx.y == args.trace_cta[1] && (int)blockIdx.z == args.trace_cta[2] &&      \
+        (idx) < 1024)                                                                        \
       args.trace[(role) * 1024 + (idx)] = (v);                                               \
   } while (0)
 
@@ -191,16 +197,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                           const uint4* __restrict__ bimg, const float* __restrict__ taps,
                           const __grid_constant__ BigMmaArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ int split_cnt[kSplitWarps], epi_cnt[4];       // batches done per warp (release / acquire)
+  __shared__ int split_cnt[kSplitWarps], epi_cnt[kEpiGroups][4];       // batches done per warp (release / acquire)
   __shared__ __align__(8) uint64_t done[kND];    // MMA completion, one per batch of input rows
   __shared__ __align__(8) uint64_t ring_ready;
   __shared__ uint32_t tmem_base_sh;
   unsigned char* base = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char* xrows = base;                                   // kXB * kRB slots
-  unsigned char* estage = xrows + kXB * kRB * kXSlot;            // 4 epilogue warps
-  unsigned char* bmats = estage + 4 * kEStage;                   // 2 * nkb images
+  unsigned char* estage = xrows + kXB * kRB * kXSlot;            // 4 * kEpiGroups epilogue warps
+  unsigned char* bmats = estage + 4 * kEpiGroups * kEStage;                   // 2 * nkb images
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) BIG_TRACE(7, 3, clock64());
+  // with a trace buffer: every CTA's entry / exit %globaltimer after the 8 role rows
+  const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (args.trace && threadIdx.x == 0 && cta_lin < 4096) {
+    long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.trace[8 * 1024 + 2 * cta_lin] = gt;
+  }
   constexpr int nkb = NKB;  // K blocks: compile-time so a piece's MMAs issue as one unrolled block
   const int kh = args.kh, kw = args.kw, nw = args.nw;
   const int c0 = blockIdx.x * kStrip;
@@ -216,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSplitWarps; ++i) split_cnt[i] = 0;
-    for (int i = 0; i < 4; ++i) epi_cnt[i] = 0;
+    for (int i = 0; i < 4 * kEpiGroups; ++i) (&epi_cnt[0][0])[i] = 0;
     for (int s = 0; s < kND; ++s) mbar_init(&done[s], 1);
     mbar_init(&ring_ready, 4);
     fence_mbar_init();
@@ -403,20 +417,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < kWarpIssue) {
     // ------------------------------------------------------------ epilogue
+    // two groups of 4 warps (one per TMEM lane quarter) drain alternating
+    // batches of 4 output rows: a batch is a dependent chain (TMEM loads,
+    // staging, ~32 global stores, re-zeroing) of ~2,400-4,500 cycles, more
+    // than the issuer needs per batch for windows below ~25 rows
     const int q = warp & 3;  // TMEM lane quarter
+    const int grp = (warp - kWarpEpi0) >> 2;
     const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16);
-    for (int c = 0; c < 512; c += 8) tmem_zero8(lane_base + c);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ring_ready);
+    if (grp == 0) {
+      for (int c = 0; c < 512; c += 8) tmem_zero8(lane_base + c);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ring_ready);
+    }
     const int ow = args.ow;
     const float f_unscale = args.f_unscale;
     // a TMEM lane holds 8 consecutive output columns; the warp's 256 columns
     // go through a padded shared-memory slab so that every global store is a
     // coalesced 128-byte row segment whatever the alignment of the output row
     // (per-lane 32-byte stores cost ~1,000 cycles per output row)
-    float* est = reinterpret_cast<float*>(estage + q * kEStage);
+    float* est = reinterpret_cast<float*>(estage + (4 * grp + q) * kEStage);
     const int colw = c0 + 256 * q;  // first column (one image) / strip position (packed) of this warp
     const int64_t oplane = (int64_t)args.oh * ow;
     float* ybase = y + (int64_t)img * oplane;
@@ -442,7 +463,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // two multiplications undo the scales (their product may leave the float range)
     const int n_epi = (s_valid - o_start + 3) / 4;
     int batches_done = 0;  // MMA batches known complete (waited in order)
-    for (int e = 0; e < n_epi; ++e) {
+    int drained = 0;       // batches this warp has drained (published in epi_cnt)
+    for (int e = grp; e < n_epi; e += kEpiGroups) {
       const int o0 = o_start + 4 * e;
       const int t_final = min(o0 + 3 + kh - 1, t_rows - 1);
       for (; batches_done <= t_final / kRB; ++batches_done)
@@ -490,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) st_release(&epi_cnt[q], e + 1);
+      if (lane == 0) st_release(&epi_cnt[grp][q], ++drained);
       if (warp == kWarpEpi0 && lane == 0) BIG_TRACE(6, e, clock64());
     }
   } else {
@@ -518,8 +540,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // below a + nw - kRing, i.e. epilogue batches [0, need)
         const int need = (a + nw - kRing - o_start + 3) >> 2;
         if (need > epi_known) {
+          // group g has drained batches g, g + 2, ..: all batches below
+          // min_g(2 c_g + g) are done
           int got;
-          while ((got = min_progress(epi_cnt)) < need) {
+          for (;;) {
+            got = kEpiGroups * min_progress(epi_cnt[0]);
+#pragma unroll
+            for (int g = 1; g < kEpiGroups; ++g)
+              got = min(got, kEpiGroups * min_progress(epi_cnt[g]) + g);
+            if (got >= need) break;
           }
           fence_acquire();
           epi_known = got;  // everything the counters show, not just what was needed
@@ -561,6 +590,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the reference tap order (reference.py:19-22), overwriting the MMA results
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (threadIdx.x == 0) BIG_TRACE(7, 2, clock64());
+  if (args.trace && threadIdx.x == 0 && cta_lin < 4096) {
+    long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.trace[8 * 1024 + 2 * cta_lin + 1] = gt;
+  }
   if (bad) {
     const int64_t plane_in = (int64_t)args.h * args.w;
     const int cols = min(kStrip, args.ow - c0);
@@ -590,7 +625,8 @@ int env_int(const char* name, int dflt) {
 }
 
 size_t smem_bytes(int kh, int nkb) {
-  return 1024 + (size_t)kXB * kRB * kXSlot + 4 * (size_t)kEStage + (size_t)2 * nkb * bimg_bytes(kh);
+  return 1024 + (size_t)kXB * kRB * kXSlot + 4 * kEpiGroups * (size_t)kEStage +
+         (size_t)2 * nkb * bimg_bytes(kh);
 }
 
 
@@ -674,6 +710,9 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   a.oh = (int)oh, a.ow = (int)ow, a.h = (int)h, a.w = (int)w;
   a.trace = nullptr;
   if (const char* e = getenv("SC_MMA_BIG_TRACE")) a.trace = reinterpret_cast<long long*>(strtoull(e, nullptr, 0));
+  a.trace_cta[0] = a.trace_cta[1] = a.trace_cta[2] = 0;
+  if (const char* e = getenv("SC_MMA_BIG_TRACE_CTA"))
+    sscanf(e, "%d,%d,%d", &a.trace_cta[0], &a.trace_cta[1], &a.trace_cta[2]);
   const int64_t strips = (ow + kStrip - 1) / kStrip;
   a.pack = env_int("SC_MMA_BIG_PACK", 1) ? pack_for(w, oh, ow, &a.pitch) : 1;
   if (a.pack == 1) a.pitch = 0;
