@@ -210,10 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) BIG_TRACE(7, 3, clock64());
   // with a trace buffer: every CTA's entry / exit %globaltimer after the 8 role rows
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  if (args.trace && threadIdx.x == 0 && cta_lin < 4096) {
+  if (args.trace && threadIdx.x == 0 && cta_lin < 2048) {
     long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    args.trace[8 * 1024 + 2 * cta_lin] = gt;
+    args.trace[8 * 1024 + 4 * cta_lin] = gt;
   }
   constexpr int nkb = NKB;  // K blocks: compile-time so a piece's MMAs issue as one unrolled block
   const int kh = args.kh, kw = args.kw, nw = args.nw;
@@ -294,6 +294,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   // programmatically dependent on build_b_kernel, so everything above (the
   // range scan reads only x, complete before build_b started) overlaps it;
   // its output is read from here on.
+  if (args.trace && threadIdx.x == 0 && cta_lin < 2048) {
+    long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    args.trace[8 * 1024 + 4 * cta_lin + 2] = gt;  // range scan done
+  }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   {
     const int n16 = 2 * nkb * bimg_b / 16;
@@ -385,7 +390,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (b >= kXB) {
         const int pb = b - kXB;  // the batch that used this slot: its MMAs must be complete
         // back off between probes (the waiters share sub-partitions with the
-        // MMA-issuing warp; measured neutral against plain spinning)
+        // MMA-issuing warp); polling test_wait + nanosleep instead measured
+        // 3-5 % slower and did not remove the occasional straggler CTA
         mbar_wait_sleep(&done[pb % kND], (pb / kND) & 1, 32, 256);
       }
       if (threadIdx.x == 0) BIG_TRACE(0, b, clock64());
@@ -478,6 +484,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int i = 0; i < 4; ++i) tmem_zero8(lane_base + (slot0 + i) * 8);
+      // the slots are free as soon as they are re-zeroed: publish before the
+      // staging and the global stores, so the issuer never waits on store
+      // latency (some CTAs' stores ran slow enough to eat the ring's slack
+      // and delay their second half by 12-20 us)
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) st_release(&epi_cnt[grp][q], ++drained);
       if (o0 + 3 >= 0 && any_col) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -509,10 +523,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) st_release(&epi_cnt[grp][q], ++drained);
       if (warp == kWarpEpi0 && lane == 0) BIG_TRACE(6, e, clock64());
     }
   } else {
@@ -583,6 +593,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit_elect(&done[b % kND]);
       __syncwarp();
       if (lane == 0) BIG_TRACE(4, b, clock64());
+      if (args.trace && lane == 0 && cta_lin < 2048 && (b == n_batches - 1 || b == n_batches / 2)) {
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        args.trace[8 * 1024 + 4 * cta_lin + 3] = b == n_batches - 1 ? gt : -gt;  // mid-way stamp negated
+        if (b != n_batches - 1) args.trace[8 * 1024 + 4 * 2048 + cta_lin] = gt;
+      }
     }
   }
 
@@ -591,10 +607,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (threadIdx.x == 0) BIG_TRACE(7, 2, clock64());
-  if (args.trace && threadIdx.x == 0 && cta_lin < 4096) {
+  if (args.trace && threadIdx.x == 0 && cta_lin < 2048) {
     long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    args.trace[8 * 1024 + 2 * cta_lin + 1] = gt;
+    args.trace[8 * 1024 + 4 * cta_lin + 1] = gt;
   }
   if (bad) {
     const int64_t plane_in = (int64_t)args.h * args.w;

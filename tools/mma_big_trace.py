@@ -8,7 +8,7 @@ import paper_2310_05218_b200 as sc
 b, h, w, k = (int(v) for v in sys.argv[1:5])
 x = torch.rand((b, h, w), device="cuda") * 2 - 1
 f = (np.random.default_rng(k).standard_normal((k, k)) / k).astype(np.float32)
-tr = torch.zeros(16 * 1024, dtype=torch.int64, device="cuda")
+tr = torch.zeros(8 * 1024 + 5 * 2048 + 64, dtype=torch.int64, device="cuda")
 os.environ["SC_CONV_MMA_BIG"] = "2"
 for _ in range(2):
     sc.conv2d_reference(x, f, exact=False)
@@ -17,7 +17,15 @@ sc.conv2d_reference(x, f, exact=False)
 torch.cuda.synchronize()
 raw = tr.cpu().numpy()
 t = raw[:8 * 1024].reshape(8, 1024)
-g = raw[8 * 1024:].reshape(-1, 2)
+g = raw[8 * 1024:8 * 1024 + 4 * 2048].reshape(-1, 4)
+mid = raw[8 * 1024 + 4 * 2048:8 * 1024 + 5 * 2048]
+life = (g[:, 1] - g[:, 0]) / 1e3
+order = np.argsort(-life)[:10]
+print("slowest CTAs (linear index: lifetime us, of which range scan us):",
+      [(int(i), round(float(life[i]), 1), round(float(g[i, 2] - g[i, 0]) / 1e3, 1),
+        "issuer mid/last us", round(float(mid[i] - g[i, 0]) / 1e3, 1), round(float(g[i, 3] - g[i, 0]) / 1e3, 1))
+       for i in order if g[i, 0] > 0])
+print("range scan us min/median/max", [round(float(v) / 1e3, 1) for v in np.percentile((g[:, 2] - g[:, 0])[g[:, 0] > 0], [0, 50, 100])])
 g = g[g[:, 0] > 0]
 print("CTAs", len(g), "entry spread us", (g[:, 0].max() - g[:, 0].min()) / 1e3, "lifetime us min/median/max",
       (g[:, 1] - g[:, 0]).min() / 1e3, float(np.median(g[:, 1] - g[:, 0])) / 1e3, (g[:, 1] - g[:, 0]).max() / 1e3,
