@@ -1,7 +1,8 @@
 // Large single-channel filters on the 5th-generation tensor cores (fast mode):
 // the slide-MMA formulation of _accumulate_taps (reference.py:15-23) for the
 // paper's large-filter sweep (kernels.py:248-255, conv2d_slide_compound),
-// 10 <= kw <= 57 and kh <= 53.  SURVEY 8(f)3 / 8(f)4.
+// 2 <= kw <= 57 and 2 <= kh <= 53, chosen by a cost model (roughly
+// kh kw >= 13^2 on large grids).  SURVEY 8(f)3 / 8(f)4.
 //
 // Per input row t and 1,024-column strip:
 //   M = 128 lanes m, lane m owning output columns c0 + 8 m + s (s = 0..7),
@@ -28,7 +29,9 @@
 // is an ABSOLUTE error of ~2^-25 of that maximum, i.e. fp32-accumulation
 // class); D accumulates x1 f1 + x1 f2 + x2 f1 in fp32 (the x2 f2 term is
 // ~2^-24 of a product) and the epilogue undoes the two power-of-two scales
-// (exact).  Measured ~1e-7 normwise, like the FFMA kernels.  CTAs whose
+// (exact).  Measured 0.9e-6 (11 x 11) .. 2.8e-6 (25 x 25) .. 1.2e-5 (51 x 51)
+// normwise against float64; the large-window figure is the tensor core's fp32
+// accumulation over kh x K blocks x 3 MMAs per element.  CTAs whose
 // inputs hold inf / NaN or magnitudes outside [2^-87, 2^73] skip the tensor
 // cores and compute their outputs with FMAs in the reference tap order.
 //
@@ -40,9 +43,10 @@
 // Warps: 0-5 split (global fp32 row -> x1 / x2 fp16 rows in shared memory,
 // 4 rows per batch, two batches of loads in flight), 6-13 epilogue (one TMEM
 // lane quarter each, 4 output rows per batch; two groups of four on alternate
-// batches), 14 MMA issuer (3 products x K blocks x window pieces per input row, one
-// commit per batch).  Hand-offs are per batch of 4 rows (~1,000-12,000 tensor
-// cycles of work), so plain counters / mbarriers suffice.
+// batches, the drained slots published before the global stores), 14 MMA
+// issuer (3 products x K blocks x window pieces per input row, one commit per
+// batch).  Hand-offs are per batch of 4 rows (~2,000-12,000 cycles of work)
+// through per-warp counters read with relaxed loads and one commit barrier.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
