@@ -97,3 +97,10 @@ for cmb in (16, 64):
 
     tr = t(roles)
     print(f"plain copies, {nchunk} x {cmb} MB chunks, upload-ahead role streams: {tr * 1e3:.2f} ms")
+
+# the C entry point alone, outputs preallocated (what the Python wrapper adds on top)
+from paper_2310_05218_b200 import _lib
+lib = _lib.load()
+ya = sc.pinned_empty((B, L - K + 1)); ym = sc.pinned_empty((B, L - K + 1))
+tc_ = t(lambda: lib.sc_pool1d_pair_f32_host(_lib.POOL_AVG, xh.ctypes.data, B, L, K, 0, ya.ctypes.data, ym.ctypes.data, 0))
+print(f"sc_pool1d_pair_f32_host alone (preallocated pinned outputs): {tc_ * 1e3:.2f} ms")
