@@ -757,6 +757,12 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
   const size_t bbytes = (size_t)2 * a.nkb * bimg_bytes(a.kh);
   unsigned char* scratch = nullptr;
   SC_CUDA(scratch_alloc(reinterpret_cast<void**>(&scratch), bbytes + (size_t)kh * kw * 4, st));
+  // stream-ordered free on every exit path (an early error return must not leak it)
+  struct ScratchFree {
+    void* p;
+    cudaStream_t st;
+    ~ScratchFree() { cudaFreeAsync(p, st); }
+  } scratch_free{scratch, st};
   __half* bimg = reinterpret_cast<__half*>(scratch);
   float* taps_dev = reinterpret_cast<float*>(scratch + bbytes);
   build_b_kernel<<<32, 256, 0, st>>>(taps, a.kh, a.kw, a.nkb, a.f_scale, bimg, taps_dev);
@@ -778,7 +784,6 @@ int conv2d_mma_big(const float* x, int64_t batch, int64_t h, int64_t w, const fl
     default: SC_CUDA(launch(conv2d_mma_big_kernel<4>, &attrs[3])); break;
   }
   SC_LAUNCH_CHECK("conv2d_mma_big_kernel");
-  SC_CUDA(cudaFreeAsync(scratch, st));
   return SC_OK;
 }
 
